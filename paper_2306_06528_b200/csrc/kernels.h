@@ -1,0 +1,92 @@
+// kernels.h — launchers for the CUDA-core kernels of the SVGD step (non-GEMM parts).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace push {
+namespace kern {
+
+constexpr int THIN_CHUNK = 256;  // batch rows per thin weight-gradient partial (fixed: P-invariant order)
+
+// ---------------------------------------------------------------- a0 helpers
+// hi = tf32_rn(x), lo = tf32_rn(x - hi) for x = src[p*src_pstride + t], t < count, p < batch.
+void split_hilo(const float* src, int64_t src_pstride, float* hi, float* lo, int64_t dst_pstride, int64_t count,
+                int batch, cudaStream_t s);
+
+// ---------------------------------------------------------------- a1 / a2 thin forward
+// out[p][b][o] = sigma( sum_i in(p,b,i) W_p[o][i] + bias_p[o] ), stored as tf32 (hi, lo).
+//   in(p,b,i) = in_hi[p*in_pstride + b*in + i] (+ in_lo[...] when in_lo != nullptr)
+//   W_p = theta + p*ld_theta + off_w  ([out][in] row-major), bias_p = theta + p*ld_theta + off_b
+void thin_forward(const float* in_hi, const float* in_lo, int64_t in_pstride, const float* theta, int64_t ld_theta,
+                  int64_t off_w, int64_t off_b, int in, int out, int act, float* out_hi, float* out_lo,
+                  int64_t out_pstride, int B, int batch, cudaStream_t s);
+
+// ---------------------------------------------------------------- a3 output layer + loss
+// yhat = a W^T + b (identity), e = yhat - y, err2[p][b] = sum_o e^2, delta_L = 2 e / (B d_out) as (hi, lo).
+void output_layer(const float* in_hi, const float* in_lo, int64_t in_pstride, const float* theta, int64_t ld_theta,
+                  int64_t off_w, int64_t off_b, int in, int out, const float* y, float* err2, int64_t err_pstride,
+                  float* d_hi, float* d_lo, int64_t d_pstride, int B, int batch, cudaStream_t s);
+// loss[p] = sum_b err2[p][b] / (B d_out)   (fixed-order tree reduction)
+void loss_reduce(const float* err2, int64_t err_pstride, float* loss, int B, int d_out, int batch, cudaStream_t s);
+
+// ---------------------------------------------------------------- a4 thin backprop
+// dprev[p][b][i] = (sum_o delta[p][b][o] W_p[o][i]) * sigma'(aprev[p][b][i])  -> (hi, lo)
+void thin_backward(const float* d_hi, const float* d_lo, int64_t d_pstride, const float* theta, int64_t ld_theta,
+                   int64_t off_w, int in, int out, const float* a_hi, const float* a_lo, int64_t a_pstride, int act,
+                   float* o_hi, float* o_lo, int64_t o_pstride, int B, int batch, cudaStream_t s);
+
+// ---------------------------------------------------------------- a5 thin weight gradient partials
+// part[s][p][o][i'] = sum_{b in chunk s} delta[p][b][o] * A(p,b,i'),  i' < in_eff + 1, A(.,.,in_eff) = 1
+// (in_eff = 0 gives the bias-only column sums).  chunks of THIN_CHUNK rows; returns #chunks.
+int thin_wgrad(const float* d_hi, const float* d_lo, int64_t d_pstride, const float* a_hi, const float* a_lo,
+               int64_t a_pstride, int in_eff, int out, float* part, int B, int batch, cudaStream_t s);
+
+// ---------------------------------------------------------------- a5 finalize into G
+struct PartView {
+  const float* base;
+  int splits;
+  int64_t sstride, pstride, ostride;  // element (s, p, o, i) at base + s*sstride + p*pstride + o*ostride + i
+};
+// G_p[off_w + o*in + i] = -lambda * sum_s W(s,p,o,i) + prior(theta)   (o < out, i < in)
+// G_p[off_b + o]        = -lambda * sum_s Bv(s,p,o,0) + prior(theta)
+void finalize_layer(PartView W, PartView Bv, const float* theta, float* grad, int64_t ld, int64_t off_w, int in,
+                    int out, float lambda, int prior, float inv_sigma2, int batch, cudaStream_t s);
+
+// ---------------------------------------------------------------- K0 init (R14)
+struct InitTable {
+  int n_layers;
+  int64_t off[17];   // start of layer l in the canonical row (off[L] = d)
+  float bound[16];   // fp32(1/sqrt(in_l)), rounded once on the host
+};
+void init_theta(float* theta, int64_t ld, int row0, int rows, int64_t d, uint64_t seed, const InitTable& t,
+                cudaStream_t s);
+
+// ---------------------------------------------------------------- a7 distances
+struct DistPlan {
+  int T;        // tile side (16, 32 or 64)
+  int ntile;    // ceil(n / T)
+  int npairs;   // ntile*(ntile+1)/2 upper tile pairs
+  int splits;   // S_d
+  int64_t cols; // columns per split (multiple of 32)
+};
+DistPlan dist_plan(int n, int64_t ld);
+void dist_partial(const float* theta, int64_t ld, int n, const DistPlan& pl, float* part, cudaStream_t s);
+// D[i][j] = sum_s part[s][i][j] (ascending s), D_ii = +0
+void dist_reduce(const float* part, int n, int splits, float* D, cudaStream_t s);
+
+// ---------------------------------------------------------------- a8 + a9 bandwidth and kernel matrix
+// h from D (rule, c = fp32 1/ln n or 1/ln(n+1), or fixed bw_h); K[i][j] = exp(-D[row0+i][j]/h), srow[i] = sum_j K[i][j]
+void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c_ln, float bw_h, float* h, float* K,
+                      float* srow, cudaStream_t s);
+
+// ---------------------------------------------------------------- a10 fused update
+// theta_next[row0+i][c] = theta_i[c] + (eps/n)[ sum_j K_ij (g_j[c] - r theta_j[c]) + r s_i theta_i[c] ], r = 2/h
+void svgd_update(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl, const float* K,
+                 const float* srow, const float* h, float eps_over_n, float* theta_next, cudaStream_t s);
+
+// copy rows (device, pitched) for set_grads: dst[p*ld + k] = src[p*d + k]
+void copy_rows(const float* src, int64_t d, float* dst, int64_t ld, int rows, cudaStream_t s);
+
+}  // namespace kern
+}  // namespace push

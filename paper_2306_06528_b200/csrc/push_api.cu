@@ -1,0 +1,880 @@
+// push_api.cu — the C-ABI of include/push.h: context, workspace carving, state machine,
+// the orchestration of one SVGD particle step, row exchange (NCCL or loopback), profiling.
+//
+// Step structure (PAPER.md:655-660 Fig. supp:svgd):
+//   push_particle_grads  a0-a5   (pstep on every local particle; all-gather Theta)
+//   push_svgd_step       a6-a10  (all-gather G; distances; median h; K; fused update)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/push.h"
+#include "../../include/push_debug.h"
+#include "common.cuh"
+#include "gemm.h"
+#include "kernels.h"
+#include "nccl_dl.h"
+
+namespace push {
+
+// ------------------------------------------------------------------ error state
+namespace {
+thread_local std::string t_err;
+}
+void set_error(const std::string& msg) { t_err = msg; }
+push_status fail(push_status st, const std::string& msg) {
+  t_err = msg;
+  return st;
+}
+
+// ------------------------------------------------------------------ plan
+constexpr int kMaxN = 2048;  // a10 keeps 16 kernel rows x n in shared memory
+
+struct LayerPlan {
+  int in = 0, out = 0;
+  int64_t off_w = 0, off_b = 0;  // canonical offsets in a particle row
+  bool gemm = false;             // tensor-core path (hidden layer with in, out % 32 == 0)
+  int64_t woff = 0;              // offset of this layer's hi/lo weight copy (per-particle block)
+};
+
+struct Plan {
+  int n = 0, world = 1, nl = 0, L = 0, Bmax = 0, Hmax = 0;
+  int64_t d = 0, ld = 0;
+  std::vector<LayerPlan> layers;
+  int64_t wsplit_total = 0;                 // per particle elements of the hi/lo weight copies
+  std::vector<int64_t> act_pst;             // per layer 0..L-2 activation particle stride
+  int64_t x_pst = 0;                        // replicated X split particle stride (layer 0 gemm)
+  int64_t dlt_pst = 0;                      // delta buffer particle stride
+  int64_t wpart_elems = 0, tpart_elems = 0;
+  kern::DistPlan dist{};
+  // byte offsets into the workspace
+  size_t o_theta0, o_theta1, o_grad, o_whi, o_wlo, o_xhi, o_xlo, o_dhi0, o_dlo0, o_dhi1, o_dlo1, o_err2, o_loss,
+      o_loss_all, o_wpart, o_tpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf;
+  std::vector<size_t> o_ahi, o_alo;
+  size_t total = 0;
+};
+
+static int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+static push_status validate(const push_config* c, int world) {
+  if (!c) return fail(PUSH_E_INVALID, "cfg is NULL");
+  if (world < 1) return fail(PUSH_E_INVALID, "world_size must be >= 1");
+  if (c->n_particles < 1 || c->n_particles > kMaxN)
+    return fail(PUSH_E_SHAPE, "n_particles must be in [1, " + std::to_string(kMaxN) + "]");
+  if (c->n_particles % world) return fail(PUSH_E_INVALID, "n_particles % world_size != 0 (R18)");
+  if (c->n_layers < 1 || c->n_layers > PUSH_MAX_LAYERS) return fail(PUSH_E_SHAPE, "n_layers must be in [1, 15]");
+  for (int l = 0; l <= c->n_layers; ++l)
+    if (c->dims[l] < 1) return fail(PUSH_E_SHAPE, "dims must be >= 1");
+  if (c->activation < PUSH_ACT_TANH || c->activation > PUSH_ACT_IDENTITY)
+    return fail(PUSH_E_INVALID, "bad activation");
+  if (c->prior != PUSH_PRIOR_UNIFORM && c->prior != PUSH_PRIOR_GAUSSIAN) return fail(PUSH_E_INVALID, "bad prior");
+  if (c->prior == PUSH_PRIOR_GAUSSIAN && !(c->prior_sigma > 0.f)) return fail(PUSH_E_INVALID, "prior_sigma <= 0");
+  if (!(c->lik_scale > 0.f)) return fail(PUSH_E_INVALID, "lik_scale must be > 0");
+  if (c->bw_rule < PUSH_BW_MEDIAN_LN_N || c->bw_rule > PUSH_BW_FIXED) return fail(PUSH_E_INVALID, "bad bw_rule");
+  if (c->bw_rule == PUSH_BW_FIXED && !(c->bw_h > 0.f)) return fail(PUSH_E_INVALID, "bw_h <= 0 (SPEC.md:100)");
+  if (!(c->step_size > 0.f)) return fail(PUSH_E_INVALID, "step_size must be > 0");
+  if (c->max_batch < 1) return fail(PUSH_E_SHAPE, "max_batch must be >= 1");
+  return PUSH_OK;
+}
+
+static int wgrad_splits(int B) { return gemm::effective_splits(B, std::min(8, std::max(1, B / 1024))); }
+
+static push_status make_plan(const push_config* c, int world, Plan* p) {
+  push_status st = validate(c, world);
+  if (st != PUSH_OK) return st;
+  Plan& P = *p;
+  P.n = c->n_particles;
+  P.world = world;
+  P.nl = P.n / world;
+  P.L = c->n_layers;
+  P.Bmax = c->max_batch;
+  P.layers.resize(P.L);
+  int64_t off = 0;
+  P.Hmax = 0;
+  for (int l = 0; l < P.L; ++l) {
+    LayerPlan& lp = P.layers[l];
+    lp.in = c->dims[l];
+    lp.out = c->dims[l + 1];
+    lp.off_w = off;
+    off += (int64_t)lp.in * lp.out;
+    lp.off_b = off;
+    off += lp.out;
+    lp.gemm = (l < P.L - 1) && (lp.in % 32 == 0) && (lp.out % 32 == 0);
+    P.Hmax = std::max(P.Hmax, lp.out);
+  }
+  P.d = off;
+  P.ld = round_up(P.d, 32);
+  P.wsplit_total = 0;
+  int64_t max_w = 0, max_t = 0;
+  for (auto& lp : P.layers) {
+    if (lp.gemm) {
+      lp.woff = P.wsplit_total;
+      P.wsplit_total += round_up((int64_t)lp.in * lp.out, 32);
+      max_w = std::max<int64_t>(max_w, (int64_t)lp.in * lp.out);
+      max_t = std::max<int64_t>(max_t, lp.out);
+    } else {
+      max_t = std::max<int64_t>(max_t, (int64_t)lp.out * (lp.in + 1));
+    }
+  }
+  P.act_pst.assign(std::max(P.L - 1, 0), 0);
+  for (int l = 0; l + 1 < P.L; ++l) P.act_pst[l] = round_up((int64_t)P.Bmax * P.layers[l].out, 32);
+  P.x_pst = P.layers[0].gemm ? round_up((int64_t)P.Bmax * P.layers[0].in, 32) : 0;
+  P.dlt_pst = round_up((int64_t)P.Bmax * P.Hmax, 32);
+  const int chunks_max = (P.Bmax + kern::THIN_CHUNK - 1) / kern::THIN_CHUNK;
+  P.wpart_elems = 8 * (int64_t)P.nl * max_w;
+  P.tpart_elems = (int64_t)chunks_max * P.nl * max_t;
+  P.dist = kern::dist_plan(P.n, P.ld);
+
+  size_t cur = 0;
+  auto take = [&](int64_t elems) {
+    size_t o = cur;
+    cur += (size_t)round_up(std::max<int64_t>(elems, 1) * 4, 256);
+    return o;
+  };
+  const int64_t nld = (int64_t)P.n * P.ld;
+  P.o_theta0 = take(nld);
+  P.o_theta1 = take(nld);
+  P.o_grad = take(nld);
+  P.o_whi = take(P.nl * P.wsplit_total);
+  P.o_wlo = take(P.nl * P.wsplit_total);
+  P.o_xhi = take(P.nl * P.x_pst);
+  P.o_xlo = take(P.nl * P.x_pst);
+  P.o_ahi.resize(P.act_pst.size());
+  P.o_alo.resize(P.act_pst.size());
+  for (size_t l = 0; l < P.act_pst.size(); ++l) {
+    P.o_ahi[l] = take(P.nl * P.act_pst[l]);
+    P.o_alo[l] = take(P.nl * P.act_pst[l]);
+  }
+  P.o_dhi0 = take(P.nl * P.dlt_pst);
+  P.o_dlo0 = take(P.nl * P.dlt_pst);
+  P.o_dhi1 = take(P.nl * P.dlt_pst);
+  P.o_dlo1 = take(P.nl * P.dlt_pst);
+  P.o_err2 = take((int64_t)P.nl * P.Bmax);
+  P.o_loss = take(P.nl);
+  P.o_loss_all = take(P.n);
+  P.o_wpart = take(P.wpart_elems);
+  P.o_tpart = take(P.tpart_elems);
+  P.o_dpart = take((int64_t)P.dist.splits * P.n * P.n);
+  P.o_D = take((int64_t)P.n * P.n);
+  P.o_K = take((int64_t)P.nl * P.n);
+  P.o_s = take(P.nl);
+  P.o_h = take(32);
+  P.o_xbuf = take((int64_t)P.Bmax * P.layers[0].in);
+  P.o_ybuf = take((int64_t)P.Bmax * P.layers[P.L - 1].out);
+  P.total = cur;
+  return PUSH_OK;
+}
+
+// ------------------------------------------------------------------ profiling classes
+enum PClass {
+  PC_INIT = 0, PC_SPLIT, PC_FWD_THIN, PC_FWD_GEMM, PC_OUTPUT, PC_LOSS, PC_BWD_THIN, PC_BWD_GEMM, PC_WGRAD_GEMM,
+  PC_WGRAD_THIN, PC_FINALIZE, PC_EXCHANGE, PC_DIST, PC_BANDWIDTH, PC_UPDATE, PC_COPY, PC_N
+};
+static const char* kClassNames[PC_N] = {"init",        "split_hilo",  "fwd_thin",   "fwd_gemm",
+                                        "output_loss", "loss_reduce", "bwd_thin",   "bwd_gemm",
+                                        "wgrad_gemm",  "wgrad_thin",  "finalize_g", "exchange",
+                                        "distances",   "bandwidth_k", "svgd_update", "copy"};
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t e0, e1;
+  double bytes, flops;
+  int launches;
+};
+
+struct LocalGroup;
+
+}  // namespace push
+
+// ------------------------------------------------------------------ context
+struct push_ctx {
+  push_config cfg{};
+  push::Plan P;
+  int rank = 0, world = 1;
+  int row0 = 0;
+  int device = 0;
+  uint8_t* ws = nullptr;
+  float* theta[2] = {nullptr, nullptr};
+  int cur = 0;
+  float* grad = nullptr;
+  float *whi = nullptr, *wlo = nullptr, *xhi = nullptr, *xlo = nullptr;
+  std::vector<float*> ahi, alo;
+  float *dhi[2] = {nullptr, nullptr}, *dlo[2] = {nullptr, nullptr};
+  float *err2 = nullptr, *loss = nullptr, *loss_all = nullptr, *wpart = nullptr, *tpart = nullptr;
+  float *dpart = nullptr, *D = nullptr, *K = nullptr, *srow = nullptr, *h = nullptr;
+  float *xbuf = nullptr, *ybuf = nullptr;
+  int state = 0;  // 0 READY, 1 GRADS_READY
+  bool broken = false;
+  bool has_grads = false, has_step = false;
+  float c_ln = 1.f;
+  // exchange
+  push::nccl::Comm comm = nullptr;
+  std::shared_ptr<push::LocalGroup> group;
+  // profiling
+  bool prof_on = false;
+  std::vector<push::ProfRec> recs;
+  std::vector<cudaEvent_t> ev_pool;
+  int64_t launches = 0;
+};
+
+namespace push {
+
+struct LocalGroup {
+  std::vector<push_ctx*> members;
+};
+
+static push_status sticky(push_ctx* c, push_status st) {
+  if (st == PUSH_E_CUDA || st == PUSH_E_NCCL) c->broken = true;
+  return st;
+}
+
+static cudaEvent_t get_event(push_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Run `f` (which launches `nlaunch` kernels of class `cls`), bracketing it with events when profiling.
+static push_status run_k(push_ctx* c, int cls, int nlaunch, double bytes, double flops, cudaStream_t s,
+                         const std::function<push_status()>& f) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->prof_on) {
+    e0 = get_event(c);
+    e1 = get_event(c);
+    cudaEventRecord(e0, s);
+  }
+  push_status st = f();
+  if (st == PUSH_OK) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) st = fail(PUSH_E_CUDA, std::string("kernel launch (") + kClassNames[cls] + "): " +
+                                                     cudaGetErrorString(e));
+  }
+  c->launches += nlaunch;
+  if (c->prof_on) {
+    cudaEventRecord(e1, s);
+    c->recs.push_back(ProfRec{cls, e0, e1, bytes, flops, nlaunch});
+  }
+  return st;
+}
+
+// ------------------------------------------------------------------ exchange
+enum BufKind { BUF_THETA = 0, BUF_GRAD = 1, BUF_LOSS = 2 };
+
+static float* buf_of(push_ctx* c, int kind, size_t* per_rank) {
+  if (kind == BUF_THETA) {
+    *per_rank = (size_t)c->P.nl * c->P.ld;
+    return c->theta[c->cur];
+  }
+  if (kind == BUF_GRAD) {
+    *per_rank = (size_t)c->P.nl * c->P.ld;
+    return c->grad;
+  }
+  *per_rank = (size_t)c->P.nl;
+  return c->loss_all;
+}
+
+// In-place all-gather of the row blocks of `kind` (rank r's block at r*per_rank).
+static push_status exchange(push_ctx* c, int kind, cudaStream_t s) {
+  size_t cnt = 0;
+  float* buf = buf_of(c, kind, &cnt);
+  if (kind == BUF_LOSS)
+    PUSH_CUDA_TRY(cudaMemcpyAsync(buf + c->rank * cnt, c->loss, cnt * 4, cudaMemcpyDeviceToDevice, s));
+  if (c->world == 1) return PUSH_OK;
+  const double bytes = 4.0 * cnt * (c->world - 1);
+  if (c->group) {
+    return run_k(c, PC_EXCHANGE, 0, bytes, 0, s, [&]() -> push_status {
+      for (int q = 0; q < c->world; ++q) {
+        if (q == c->rank) continue;
+        push_ctx* pc = c->group->members[q];
+        size_t cq = 0;
+        const float* src = kind == BUF_LOSS ? pc->loss : buf_of(pc, kind, &cq) + q * cnt;
+        PUSH_CUDA_TRY(cudaMemcpyAsync(buf + q * cnt, src, cnt * 4, cudaMemcpyDeviceToDevice, s));
+      }
+      return PUSH_OK;
+    });
+  }
+  return run_k(c, PC_EXCHANGE, 0, bytes, 0, s,
+               [&]() { return nccl::allgather_f32(buf + c->rank * cnt, buf, cnt, c->comm, s); });
+}
+
+// ------------------------------------------------------------------ grads (a0-a5)
+struct View {
+  const float* hi;
+  const float* lo;
+  int64_t pst;
+};
+
+static View input_view(push_ctx* c, int l, const float* x) {
+  if (l == 0) {
+    if (c->P.layers[0].gemm) return View{c->xhi, c->xlo, c->P.x_pst};
+    return View{x, nullptr, 0};
+  }
+  return View{c->ahi[l - 1], c->alo[l - 1], c->P.act_pst[l - 1]};
+}
+
+static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, cudaStream_t s) {
+  const Plan& P = c->P;
+  const int nl = P.nl, L = P.L, act = c->cfg.activation;
+  const int64_t ld = P.ld;
+  float* th = c->theta[c->cur] + (int64_t)c->row0 * ld;  // own rows
+  float* g = c->grad + (int64_t)c->row0 * ld;
+  push_status st;
+
+  // C1: Theta rows of every rank (needed by a7/a10; unchanged during the gradient phase)
+  if ((st = exchange(c, BUF_THETA, s)) != PUSH_OK) return st;
+
+  // a0: tf32 hi/lo copies of the tensor-core weights (and of X if layer 1 is a GEMM layer)
+  for (int l = 0; l < L; ++l) {
+    const LayerPlan& lp = P.layers[l];
+    if (!lp.gemm) continue;
+    const int64_t cnt = (int64_t)lp.in * lp.out;
+    st = run_k(c, PC_SPLIT, 1, 12.0 * cnt * nl, 0, s, [&] {
+      kern::split_hilo(th + lp.off_w, ld, c->whi + lp.woff, c->wlo + lp.woff, P.wsplit_total, cnt, nl, s);
+      return PUSH_OK;
+    });
+    if (st != PUSH_OK) return st;
+  }
+  if (P.layers[0].gemm) {
+    const int64_t cnt = (int64_t)B * P.layers[0].in;
+    st = run_k(c, PC_SPLIT, 1, 12.0 * cnt * nl, 0, s, [&] {
+      kern::split_hilo(x, 0, c->xhi, c->xlo, P.x_pst, cnt, nl, s);
+      return PUSH_OK;
+    });
+    if (st != PUSH_OK) return st;
+  }
+
+  // a1/a2: hidden layers forward
+  for (int l = 0; l + 1 < L; ++l) {
+    const LayerPlan& lp = P.layers[l];
+    const View in = input_view(c, l, x);
+    if (lp.gemm) {
+      gemm::Problem pb;
+      pb.M = B; pb.N = lp.out; pb.K = lp.in; pb.batch = nl; pb.splits = 1; pb.passes = 3;
+      pb.A = gemm::Operand{in.hi, in.lo, false, lp.in, in.pst};
+      pb.B = gemm::Operand{c->whi + lp.woff, c->wlo + lp.woff, false, lp.in, P.wsplit_total};
+      pb.epi = gemm::EPI_FWD; pb.act = act;
+      pb.out0 = c->ahi[l]; pb.out1 = c->alo[l]; pb.ldo = lp.out; pb.out_pstride = P.act_pst[l];
+      pb.bias = th + lp.off_b; pb.bias_pstride = ld;
+      const double fl = 2.0 * B * lp.out * (double)lp.in * nl;
+      st = run_k(c, PC_FWD_GEMM, 1, 0, fl, s, [&] { return gemm::run(pb, s); });
+    } else {
+      st = run_k(c, PC_FWD_THIN, 1, 0, 2.0 * B * lp.out * (double)lp.in * nl, s, [&] {
+        kern::thin_forward(in.hi, in.lo, in.pst, th, ld, lp.off_w, lp.off_b, lp.in, lp.out, act, c->ahi[l],
+                           c->alo[l], P.act_pst[l], B, nl, s);
+        return PUSH_OK;
+      });
+    }
+    if (st != PUSH_OK) return st;
+  }
+
+  // a3: output layer, residuals, delta_L, per-particle loss
+  {
+    const LayerPlan& lp = P.layers[L - 1];
+    const View in = input_view(c, L - 1, x);
+    st = run_k(c, PC_OUTPUT, 1, 0, 2.0 * B * lp.out * (double)lp.in * nl, s, [&] {
+      kern::output_layer(in.hi, in.lo, in.pst, th, ld, lp.off_w, lp.off_b, lp.in, lp.out, y, c->err2, P.Bmax,
+                         c->dhi[0], c->dlo[0], P.dlt_pst, B, nl, s);
+      return PUSH_OK;
+    });
+    if (st != PUSH_OK) return st;
+    st = run_k(c, PC_LOSS, 1, 0, 0, s, [&] {
+      kern::loss_reduce(c->err2, P.Bmax, c->loss, B, lp.out, nl, s);
+      return PUSH_OK;
+    });
+    if (st != PUSH_OK) return st;
+  }
+
+  // a4/a5: backprop and weight gradients, layer by layer
+  int xb = 0;
+  const float lambda = c->cfg.lik_scale;
+  const float inv_s2 = c->cfg.prior == PUSH_PRIOR_GAUSSIAN ? 1.0f / (c->cfg.prior_sigma * c->cfg.prior_sigma) : 0.f;
+  for (int l = L - 1; l >= 0; --l) {
+    const LayerPlan& lp = P.layers[l];
+    const float* dh = c->dhi[xb];
+    const float* dl = c->dlo[xb];
+    const View ap = input_view(c, l, x);
+    if (lp.gemm) {
+      const int S = wgrad_splits(B);
+      gemm::Problem pb;
+      pb.M = lp.out; pb.N = lp.in; pb.K = B; pb.batch = nl; pb.splits = S; pb.passes = 3;
+      pb.A = gemm::Operand{dh, dl, true, lp.out, P.dlt_pst};
+      pb.B = gemm::Operand{ap.hi, ap.lo, true, lp.in, ap.pst};
+      pb.epi = gemm::EPI_STORE;
+      pb.out0 = c->wpart; pb.ldo = lp.in; pb.out_pstride = (int64_t)lp.out * lp.in;
+      pb.out_sstride = (int64_t)nl * lp.out * lp.in;
+      const double fl = 2.0 * B * lp.out * (double)lp.in * nl;
+      st = run_k(c, PC_WGRAD_GEMM, 1, 0, fl, s, [&] { return gemm::run(pb, s); });
+      if (st != PUSH_OK) return st;
+      int chunks = 0;
+      st = run_k(c, PC_WGRAD_THIN, 1, 0, 0, s, [&] {
+        chunks = kern::thin_wgrad(dh, dl, P.dlt_pst, nullptr, nullptr, 0, 0, lp.out, c->tpart, B, nl, s);
+        return PUSH_OK;
+      });
+      if (st != PUSH_OK) return st;
+      kern::PartView W{c->wpart, S, (int64_t)nl * lp.out * lp.in, (int64_t)lp.out * lp.in, lp.in};
+      kern::PartView Bv{c->tpart, chunks, (int64_t)nl * lp.out, lp.out, 1};
+      st = run_k(c, PC_FINALIZE, 1, 0, 0, s, [&] {
+        kern::finalize_layer(W, Bv, th, g, ld, lp.off_w, lp.in, lp.out, lambda, c->cfg.prior, inv_s2, nl, s);
+        return PUSH_OK;
+      });
+    } else {
+      int chunks = 0;
+      st = run_k(c, PC_WGRAD_THIN, 1, 0, 2.0 * B * lp.out * (double)(lp.in + 1) * nl, s, [&] {
+        chunks = kern::thin_wgrad(dh, dl, P.dlt_pst, ap.hi, ap.lo, ap.pst, lp.in, lp.out, c->tpart, B, nl, s);
+        return PUSH_OK;
+      });
+      if (st != PUSH_OK) return st;
+      const int64_t cols = lp.in + 1;
+      kern::PartView W{c->tpart, chunks, (int64_t)nl * lp.out * cols, (int64_t)lp.out * cols, cols};
+      kern::PartView Bv{c->tpart + lp.in, chunks, (int64_t)nl * lp.out * cols, (int64_t)lp.out * cols, cols};
+      st = run_k(c, PC_FINALIZE, 1, 0, 0, s, [&] {
+        kern::finalize_layer(W, Bv, th, g, ld, lp.off_w, lp.in, lp.out, lambda, c->cfg.prior, inv_s2, nl, s);
+        return PUSH_OK;
+      });
+    }
+    if (st != PUSH_OK) return st;
+    if (l == 0) break;
+    // delta_{l-1} = (delta_l W_l) * sigma'(a_{l-1})
+    const View aprev = input_view(c, l, x);
+    float* oh = c->dhi[xb ^ 1];
+    float* ol = c->dlo[xb ^ 1];
+    if (lp.gemm) {
+      gemm::Problem pb;
+      pb.M = B; pb.N = lp.in; pb.K = lp.out; pb.batch = nl; pb.splits = 1; pb.passes = 3;
+      pb.A = gemm::Operand{dh, dl, false, lp.out, P.dlt_pst};
+      pb.B = gemm::Operand{c->whi + lp.woff, c->wlo + lp.woff, true, lp.in, P.wsplit_total};
+      pb.epi = gemm::EPI_BWD; pb.act = act;
+      pb.out0 = oh; pb.out1 = ol; pb.ldo = lp.in; pb.out_pstride = P.dlt_pst;
+      pb.aprev_hi = aprev.hi; pb.aprev_lo = aprev.lo; pb.ld_aprev = lp.in; pb.aprev_pstride = aprev.pst;
+      const double fl = 2.0 * B * lp.out * (double)lp.in * nl;
+      st = run_k(c, PC_BWD_GEMM, 1, 0, fl, s, [&] { return gemm::run(pb, s); });
+    } else {
+      st = run_k(c, PC_BWD_THIN, 1, 0, 2.0 * B * lp.out * (double)lp.in * nl, s, [&] {
+        kern::thin_backward(dh, dl, P.dlt_pst, th, ld, lp.off_w, lp.in, lp.out, aprev.hi, aprev.lo, aprev.pst, act,
+                            oh, ol, P.dlt_pst, B, nl, s);
+        return PUSH_OK;
+      });
+    }
+    if (st != PUSH_OK) return st;
+    xb ^= 1;
+  }
+  return PUSH_OK;
+}
+
+// ------------------------------------------------------------------ step (a6-a10)
+static push_status do_step(push_ctx* c, cudaStream_t s) {
+  const Plan& P = c->P;
+  push_status st;
+  // C2: g rows of every rank
+  if ((st = exchange(c, BUF_GRAD, s)) != PUSH_OK) return st;
+  const float* th = c->theta[c->cur];
+  const double nd4 = 4.0 * P.n * (double)P.d;
+  st = run_k(c, PC_DIST, 2, nd4, 3.0 * P.n * (double)P.n * P.d / 2, s, [&] {
+    kern::dist_partial(th, P.ld, P.n, P.dist, c->dpart, s);
+    kern::dist_reduce(c->dpart, P.n, P.dist.splits, c->D, s);
+    return PUSH_OK;
+  });
+  if (st != PUSH_OK) return st;
+  st = run_k(c, PC_BANDWIDTH, 1, 4.0 * P.n * P.n, 0, s, [&] {
+    kern::bandwidth_kernel(c->D, P.n, c->row0, P.nl, c->cfg.bw_rule, c->c_ln, c->cfg.bw_h, c->h, c->K, c->srow, s);
+    return PUSH_OK;
+  });
+  if (st != PUSH_OK) return st;
+  const float eps_n = c->cfg.step_size / (float)P.n;
+  float* next = c->theta[c->cur ^ 1];
+  st = run_k(c, PC_UPDATE, 1, 2.0 * nd4 + 4.0 * P.nl * (double)P.d, 2.0 * P.nl * (double)P.n * P.d, s, [&] {
+    kern::svgd_update(th, c->grad, P.ld, P.n, c->row0, P.nl, c->K, c->srow, c->h, eps_n, next, s);
+    return PUSH_OK;
+  });
+  if (st != PUSH_OK) return st;
+  c->cur ^= 1;
+  return PUSH_OK;
+}
+
+static push_status check_ctx(push_ctx* c) {
+  if (!c) return fail(PUSH_E_INVALID, "ctx is NULL");
+  if (c->broken) return fail(PUSH_E_STATE, "context is in a failed state after an earlier CUDA/NCCL error");
+  cudaSetDevice(c->device);
+  return PUSH_OK;
+}
+
+static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int world, void* ws, size_t ws_bytes,
+                            const float* theta0_host) {
+  push_status st = make_plan(cfg, world, &c->P);
+  if (st != PUSH_OK) return st;
+  if (rank < 0 || rank >= world) return fail(PUSH_E_INVALID, "rank out of range");
+  if (!ws) return fail(PUSH_E_INVALID, "dev_workspace is NULL");
+  if (reinterpret_cast<uintptr_t>(ws) % 256) return fail(PUSH_E_INVALID, "dev_workspace must be 256-byte aligned");
+  if (ws_bytes < c->P.total) return fail(PUSH_E_SHAPE, "workspace too small: need " + std::to_string(c->P.total));
+  int dev = 0;
+  PUSH_CUDA_TRY(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  PUSH_CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10) return fail(PUSH_E_UNSUPPORTED, "libpush_b200 needs an sm_100 (B200) device");
+  c->cfg = *cfg;
+  c->rank = rank;
+  c->world = world;
+  c->row0 = rank * c->P.nl;
+  c->device = dev;
+  c->ws = static_cast<uint8_t*>(ws);
+  const Plan& P = c->P;
+  auto F = [&](size_t o) { return reinterpret_cast<float*>(c->ws + o); };
+  c->theta[0] = F(P.o_theta0);
+  c->theta[1] = F(P.o_theta1);
+  c->grad = F(P.o_grad);
+  c->whi = F(P.o_whi);
+  c->wlo = F(P.o_wlo);
+  c->xhi = F(P.o_xhi);
+  c->xlo = F(P.o_xlo);
+  for (size_t l = 0; l < P.o_ahi.size(); ++l) {
+    c->ahi.push_back(F(P.o_ahi[l]));
+    c->alo.push_back(F(P.o_alo[l]));
+  }
+  c->dhi[0] = F(P.o_dhi0);
+  c->dlo[0] = F(P.o_dlo0);
+  c->dhi[1] = F(P.o_dhi1);
+  c->dlo[1] = F(P.o_dlo1);
+  c->err2 = F(P.o_err2);
+  c->loss = F(P.o_loss);
+  c->loss_all = F(P.o_loss_all);
+  c->wpart = F(P.o_wpart);
+  c->tpart = F(P.o_tpart);
+  c->dpart = F(P.o_dpart);
+  c->D = F(P.o_D);
+  c->K = F(P.o_K);
+  c->srow = F(P.o_s);
+  c->h = F(P.o_h);
+  c->xbuf = F(P.o_xbuf);
+  c->ybuf = F(P.o_ybuf);
+  // bandwidth constant c_n = fp32(1/ln n) or fp32(1/ln(n+1)), computed once in double (R4)
+  if (cfg->bw_rule == PUSH_BW_MEDIAN_LN_N)
+    c->c_ln = P.n > 1 ? (float)(1.0 / std::log((double)P.n)) : 1.f;
+  else if (cfg->bw_rule == PUSH_BW_MEDIAN_LN_N1)
+    c->c_ln = (float)(1.0 / std::log((double)P.n + 1.0));
+
+  cudaStream_t s = nullptr;
+  const size_t nld = (size_t)P.n * P.ld;
+  PUSH_CUDA_TRY(cudaMemsetAsync(c->theta[0], 0, nld * 4, s));
+  PUSH_CUDA_TRY(cudaMemsetAsync(c->theta[1], 0, nld * 4, s));
+  PUSH_CUDA_TRY(cudaMemsetAsync(c->grad, 0, nld * 4, s));
+  if (theta0_host) {
+    PUSH_CUDA_TRY(cudaMemcpy2DAsync(c->theta[0], P.ld * 4, theta0_host, P.d * 4, P.d * 4, P.n,
+                                    cudaMemcpyHostToDevice, s));
+  } else {
+    kern::InitTable t{};
+    t.n_layers = P.L;
+    for (int l = 0; l < P.L; ++l) {
+      t.off[l] = P.layers[l].off_w;
+      t.bound[l] = (float)(1.0 / std::sqrt((double)P.layers[l].in));
+    }
+    t.off[P.L] = P.d;
+    st = run_k(c, PC_INIT, 1, 4.0 * nld, 0, s, [&] {
+      kern::init_theta(c->theta[0], P.ld, 0, P.n, P.d, cfg->seed, t, s);
+      return PUSH_OK;
+    });
+    if (st != PUSH_OK) return st;
+  }
+  PUSH_CUDA_TRY(cudaStreamSynchronize(s));
+  return PUSH_OK;
+}
+
+}  // namespace push
+
+using namespace push;
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* push_version(void) {
+  return "libpush_b200 abi=1 sm_100a (tcgen05 3xTF32 GEMM, radix-select median, fused SVGD update)";
+}
+
+const char* push_last_error(void) { return push::t_err.c_str(); }
+
+push_status push_get_unique_id(uint8_t id[128]) {
+  if (!id) return fail(PUSH_E_INVALID, "id is NULL");
+  nccl::UniqueId u;
+  push_status st = nccl::get_unique_id(&u);
+  if (st != PUSH_OK) return st;
+  std::memcpy(id, u.internal, 128);
+  return PUSH_OK;
+}
+
+push_status push_workspace_size(const push_config* cfg, int32_t world_size, size_t* bytes) {
+  if (!bytes) return fail(PUSH_E_INVALID, "bytes is NULL");
+  Plan P;
+  push_status st = make_plan(cfg, world_size, &P);
+  if (st != PUSH_OK) return st;
+  *bytes = P.total;
+  return PUSH_OK;
+}
+
+push_status push_init(const push_config* cfg, int32_t rank, int32_t world_size, const uint8_t* nccl_id,
+                      void* dev_workspace, size_t ws_bytes, const float* theta0_host, push_ctx** out) {
+  if (!out) return fail(PUSH_E_INVALID, "out is NULL");
+  *out = nullptr;
+  if (world_size > 1 && !nccl_id) return fail(PUSH_E_INVALID, "nccl_id required when world_size > 1");
+  push_ctx* c = new (std::nothrow) push_ctx();
+  if (!c) return fail(PUSH_E_NOMEM, "out of host memory");
+  push_status st = init_one(c, cfg, rank, world_size, dev_workspace, ws_bytes, theta0_host);
+  if (st == PUSH_OK && world_size > 1) {
+    nccl::UniqueId u;
+    std::memcpy(u.internal, nccl_id, 128);
+    st = nccl::comm_init_rank(&c->comm, world_size, u, rank);
+  }
+  if (st != PUSH_OK) {
+    delete c;
+    return st;
+  }
+  *out = c;
+  return PUSH_OK;
+}
+
+push_status push_init_local_group(const push_config* cfg, int32_t world_size, void* const* dev_workspaces,
+                                  size_t ws_bytes, const float* theta0_host, push_ctx** out_ctxs) {
+  if (!out_ctxs || !dev_workspaces) return fail(PUSH_E_INVALID, "NULL argument");
+  if (world_size < 1) return fail(PUSH_E_INVALID, "world_size must be >= 1");
+  auto grp = std::make_shared<LocalGroup>();
+  for (int r = 0; r < world_size; ++r) out_ctxs[r] = nullptr;
+  for (int r = 0; r < world_size; ++r) {
+    push_ctx* c = new (std::nothrow) push_ctx();
+    if (!c) return fail(PUSH_E_NOMEM, "out of host memory");
+    push_status st = init_one(c, cfg, r, world_size, dev_workspaces[r], ws_bytes, theta0_host);
+    if (st != PUSH_OK) {
+      delete c;
+      for (int q = 0; q < r; ++q) {
+        delete out_ctxs[q];
+        out_ctxs[q] = nullptr;
+      }
+      return st;
+    }
+    c->group = grp;
+    grp->members.push_back(c);
+    out_ctxs[r] = c;
+  }
+  return PUSH_OK;
+}
+
+push_status push_particle_grads(push_ctx* c, const float* x_dev, const float* y_dev, int32_t B, float* loss_dev,
+                                void* stream) {
+  push_status st = check_ctx(c);
+  if (st != PUSH_OK) return st;
+  if (!x_dev || !y_dev) return fail(PUSH_E_INVALID, "x_dev / y_dev is NULL");
+  if (B < 1 || B > c->P.Bmax) return fail(PUSH_E_SHAPE, "B must be in [1, max_batch] (SPEC.md:55)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  st = do_grads(c, x_dev, y_dev, B, s);
+  if (st == PUSH_OK && loss_dev) {
+    st = run_k(c, PC_COPY, 0, 8.0 * c->P.nl, 0, s, [&]() -> push_status {
+      PUSH_CUDA_TRY(cudaMemcpyAsync(loss_dev, c->loss, 4 * c->P.nl, cudaMemcpyDeviceToDevice, s));
+      return PUSH_OK;
+    });
+  }
+  if (st != PUSH_OK) return sticky(c, st);
+  c->state = 1;
+  c->has_grads = true;
+  return PUSH_OK;
+}
+
+push_status push_set_grads(push_ctx* c, const float* g_dev, void* stream) {
+  push_status st = check_ctx(c);
+  if (st != PUSH_OK) return st;
+  if (!g_dev) return fail(PUSH_E_INVALID, "g_dev is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  st = exchange(c, BUF_THETA, s);
+  if (st == PUSH_OK)
+    st = run_k(c, PC_COPY, 1, 8.0 * c->P.nl * c->P.d, 0, s, [&] {
+      kern::copy_rows(g_dev, c->P.d, c->grad + (int64_t)c->row0 * c->P.ld, c->P.ld, c->P.nl, s);
+      return PUSH_OK;
+    });
+  if (st != PUSH_OK) return sticky(c, st);
+  c->state = 1;
+  c->has_grads = true;
+  return PUSH_OK;
+}
+
+push_status push_svgd_step(push_ctx* c, void* stream) {
+  push_status st = check_ctx(c);
+  if (st != PUSH_OK) return st;
+  if (c->state != 1) return fail(PUSH_E_STATE, "svgd_step needs fresh gradients (SPEC.md:350)");
+  st = do_step(c, static_cast<cudaStream_t>(stream));
+  if (st != PUSH_OK) return sticky(c, st);
+  c->state = 0;
+  c->has_step = true;
+  return PUSH_OK;
+}
+
+push_status push_step_host(push_ctx* c, const float* x_host, const float* y_host, int32_t B, float* loss_host,
+                           void* stream) {
+  push_status st = check_ctx(c);
+  if (st != PUSH_OK) return st;
+  if (!x_host || !y_host) return fail(PUSH_E_INVALID, "x_host / y_host is NULL");
+  if (B < 1 || B > c->P.Bmax) return fail(PUSH_E_SHAPE, "B must be in [1, max_batch]");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int din = c->P.layers[0].in, dout = c->P.layers[c->P.L - 1].out;
+  auto copy_in = [&]() -> push_status {
+    PUSH_CUDA_TRY(cudaMemcpyAsync(c->xbuf, x_host, (size_t)B * din * 4, cudaMemcpyHostToDevice, s));
+    PUSH_CUDA_TRY(cudaMemcpyAsync(c->ybuf, y_host, (size_t)B * dout * 4, cudaMemcpyHostToDevice, s));
+    return PUSH_OK;
+  };
+  if ((st = copy_in()) != PUSH_OK) return sticky(c, st);
+  if ((st = push_particle_grads(c, c->xbuf, c->ybuf, B, nullptr, stream)) != PUSH_OK) return st;
+  if ((st = push_svgd_step(c, stream)) != PUSH_OK) return st;
+  if (loss_host) {
+    cudaError_t e = cudaMemcpyAsync(loss_host, c->loss, 4 * c->P.nl, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
+  }
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
+  return PUSH_OK;
+}
+
+push_status push_gather(push_ctx* c, int32_t what, float* out_host, void* stream) {
+  push_status st = check_ctx(c);
+  if (st != PUSH_OK) return st;
+  if (!out_host) return fail(PUSH_E_INVALID, "out_host is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Plan& P = c->P;
+  auto sync = [&]() -> push_status {
+    PUSH_CUDA_TRY(cudaStreamSynchronize(s));
+    return PUSH_OK;
+  };
+  switch (what) {
+    case PUSH_WHAT_THETA:
+    case PUSH_WHAT_GRAD: {
+      if (what == PUSH_WHAT_GRAD && !c->has_grads) return fail(PUSH_E_STATE, "no gradients yet");
+      st = exchange(c, what == PUSH_WHAT_THETA ? BUF_THETA : BUF_GRAD, s);
+      if (st != PUSH_OK) return sticky(c, st);
+      const float* src = what == PUSH_WHAT_THETA ? c->theta[c->cur] : c->grad;
+      cudaError_t e = cudaMemcpy2DAsync(out_host, P.d * 4, src, P.ld * 4, P.d * 4, P.n, cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
+      break;
+    }
+    case PUSH_WHAT_DIST:
+    case PUSH_WHAT_H:
+    case PUSH_WHAT_KERNEL: {
+      if (!c->has_step) return fail(PUSH_E_STATE, "no SVGD step yet");
+      const float* src = what == PUSH_WHAT_DIST ? c->D : (what == PUSH_WHAT_H ? c->h : c->K);
+      const size_t cnt = what == PUSH_WHAT_DIST ? (size_t)P.n * P.n : (what == PUSH_WHAT_H ? 1 : (size_t)P.nl * P.n);
+      cudaError_t e = cudaMemcpyAsync(out_host, src, cnt * 4, cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
+      break;
+    }
+    case PUSH_WHAT_LOSS: {
+      if (!c->has_grads) return fail(PUSH_E_STATE, "no loss yet");
+      st = exchange(c, BUF_LOSS, s);
+      if (st != PUSH_OK) return sticky(c, st);
+      cudaError_t e = cudaMemcpyAsync(out_host, c->loss_all, (size_t)P.n * 4, cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
+      break;
+    }
+    default:
+      return fail(PUSH_E_INVALID, "unknown PUSH_WHAT");
+  }
+  st = sync();
+  return st == PUSH_OK ? PUSH_OK : sticky(c, st);
+}
+
+push_status push_profile_enable(push_ctx* c, int32_t enable) {
+  if (!c) return fail(PUSH_E_INVALID, "ctx is NULL");
+  for (auto& r : c->recs) {
+    c->ev_pool.push_back(r.e0);
+    c->ev_pool.push_back(r.e1);
+  }
+  c->recs.clear();
+  c->prof_on = enable != 0;
+  return PUSH_OK;
+}
+
+push_status push_profile_read(push_ctx* c, push_profile_row* rows, int32_t max_rows, int32_t* n_rows) {
+  if (!c || !rows || !n_rows) return fail(PUSH_E_INVALID, "NULL argument");
+  PUSH_CUDA_TRY(cudaDeviceSynchronize());
+  const int n = std::min<int>(max_rows, PC_N);
+  for (int i = 0; i < n; ++i) {
+    std::memset(&rows[i], 0, sizeof(push_profile_row));
+    std::strncpy(rows[i].name, kClassNames[i], sizeof(rows[i].name) - 1);
+  }
+  for (auto& r : c->recs) {
+    if (r.cls >= n) continue;
+    float ms = 0.f;
+    PUSH_CUDA_TRY(cudaEventElapsedTime(&ms, r.e0, r.e1));
+    rows[r.cls].ms += ms;
+    rows[r.cls].launches += r.launches;
+    rows[r.cls].alg_bytes += r.bytes;
+    rows[r.cls].alg_flops += r.flops;
+  }
+  *n_rows = n;
+  return PUSH_OK;
+}
+
+push_status push_launch_count(push_ctx* c, int64_t* count) {
+  if (!c || !count) return fail(PUSH_E_INVALID, "NULL argument");
+  *count = c->launches;
+  return PUSH_OK;
+}
+
+push_status push_destroy(push_ctx* c) {
+  if (!c) return PUSH_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  if (c->comm) nccl::comm_release(c->comm, c->broken);
+  for (auto& r : c->recs) {
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  delete c;
+  return PUSH_OK;
+}
+
+// ------------------------------------------------------------------ debug: isolated GEMM
+static push_status dbg_gemm(int passes, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N, int32_t K, int32_t batch,
+                            const float* A, const float* Bm, float* C, void* stream) {
+  if (M < 1 || N < 1 || K < 1 || batch < 1) return fail(PUSH_E_SHAPE, "empty GEMM");
+  if (N % 32) return fail(PUSH_E_SHAPE, "N % 32 != 0");
+  if (a_mn && M % 32) return fail(PUSH_E_SHAPE, "MN-major A needs M % 32 == 0");
+  if ((!a_mn || !b_mn) && K % 4) return fail(PUSH_E_SHAPE, "K-major operands need K % 4 == 0");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t na = (int64_t)M * K, nb = (int64_t)N * K;
+  const int64_t pa = (na + 31) / 32 * 32, pb_ = (nb + 31) / 32 * 32;
+  float* buf = nullptr;
+  PUSH_CUDA_TRY(cudaMallocAsync(&buf, sizeof(float) * 2 * batch * (pa + pb_), s));
+  float* ahi = buf;
+  float* alo = ahi + batch * pa;
+  float* bhi = alo + batch * pa;
+  float* blo = bhi + batch * pb_;
+  // dense inputs are [batch][.][.] with per-batch stride na / nb: split into padded copies
+  kern::split_hilo(A, na, ahi, alo, pa, na, batch, s);
+  kern::split_hilo(Bm, nb, bhi, blo, pb_, nb, batch, s);
+  gemm::Problem pb;
+  pb.M = M; pb.N = N; pb.K = K; pb.batch = batch; pb.splits = 1; pb.passes = passes;
+  pb.A = gemm::Operand{ahi, alo, a_mn != 0, a_mn ? M : K, pa};
+  pb.B = gemm::Operand{bhi, blo, b_mn != 0, b_mn ? N : K, pb_};
+  pb.epi = gemm::EPI_STORE;
+  pb.out0 = C; pb.ldo = N; pb.out_pstride = (int64_t)M * N; pb.out_sstride = 0;
+  push_status st = gemm::run(pb, s);
+  cudaFreeAsync(buf, s);
+  return st;
+}
+
+push_status pushdbg_gemm3xtf32(int32_t a_mn, int32_t b_mn, int32_t M, int32_t N, int32_t K, int32_t batch,
+                               const float* A_dev, const float* B_dev, float* C_dev, void* stream) {
+  return dbg_gemm(3, a_mn, b_mn, M, N, K, batch, A_dev, B_dev, C_dev, stream);
+}
+push_status pushdbg_gemm1xtf32(int32_t a_mn, int32_t b_mn, int32_t M, int32_t N, int32_t K, int32_t batch,
+                               const float* A_dev, const float* B_dev, float* C_dev, void* stream) {
+  return dbg_gemm(1, a_mn, b_mn, M, N, K, batch, A_dev, B_dev, C_dev, stream);
+}
+
+}  // extern "C"

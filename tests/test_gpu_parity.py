@@ -1,0 +1,268 @@
+"""GPU path (libpush_b200.so through the C-ABI) vs the float64 oracle on the same seeded inputs.
+
+Tolerances (north star / DESIGN.md §Parity):
+  * g = grad log p:         ||g_gpu - g_ref||_inf / ||g_ref||_inf <= 1e-5 per particle (3xTF32)
+  * one-step theta':        max rel err <= 1e-4 (floor 1e-3 * row max)
+  * 100-step loss:          <= 1e-2 relative
+  * init (K0), median bandwidth, sharding: bit-exact
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from inputs import WORKLOADS, synth  # noqa: E402
+from oracle import init as oinit  # noqa: E402
+from oracle import mlp as omlp  # noqa: E402
+from oracle import svgd as osvgd  # noqa: E402
+from paper_2306_06528_b200 import push  # noqa: E402
+
+from .gpu_util import inf_rel, rel_err  # noqa: E402
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def _d(dims):
+    return sum(dims[l] * dims[l + 1] + dims[l + 1] for l in range(len(dims) - 1))
+
+
+# ------------------------------------------------------------------ K0 init
+@pytest.mark.parametrize("n,dims,seed", [(4, [1, 32, 32, 1], 0), (3, [2, 7, 5, 3], 11), (16, [2, 256, 256, 1], 5)])
+def test_init_bit_exact(n, dims, seed):
+    ctx = push.Context(push.make_config(n, dims, max_batch=8, seed=seed))
+    th = ctx.gather("theta")
+    assert np.array_equal(th, oinit.init_theta(n, dims, seed))
+
+
+# ------------------------------------------------------------------ gradients a0-a5
+GRAD_CASES = [
+    # n, dims, B, act, prior, sigma, lam, data
+    (4, [1, 32, 32, 1], 256, "tanh", "uniform", 1.0, 1.0, "sine"),        # C1 shape
+    (3, [2, 64, 64, 64, 1], 300, "tanh", "uniform", 1.0, 1.0, "gauss"),   # ragged B
+    (2, [3, 96, 32, 1], 128, "relu", "uniform", 1.0, 1.0, "gauss"),
+    (3, [5, 7, 3], 50, "identity", "uniform", 1.0, 1.0, "gauss"),        # all thin layers
+    (2, [32, 64, 1], 200, "tanh", "gaussian", 0.5, 2.0, "gauss"),         # layer 1 on tensor cores (X split)
+    (2, [1, 33, 1], 64, "tanh", "uniform", 1.0, 1.0, "gauss"),            # width not % 32 -> thin path
+    (2, [2, 128, 128, 1], 1, "tanh", "uniform", 1.0, 1.0, "gauss"),       # B = 1
+    (2, [2, 256, 256, 256, 256, 1], 2048, "tanh", "uniform", 1.0, 1.0, "advection"),  # C2 net, split-K
+]
+
+
+@pytest.mark.parametrize("n,dims,B,act,prior,sigma,lam,data", GRAD_CASES)
+def test_grads_match_oracle(n, dims, B, act, prior, sigma, lam, data):
+    x, y = synth.batch(data, B, dims[0], dims[-1], step=3)
+    cfg = push.make_config(n, dims, activation=act, prior=prior, prior_sigma=sigma, lik_scale=lam, max_batch=B + 7,
+                           seed=2)
+    ctx = push.Context(cfg)
+    th = ctx.gather("theta")
+    loss = torch.empty(n, device="cuda")
+    ctx.particle_grads(_dev(x), _dev(y), loss)
+    g = ctx.gather("grad")
+    Gref, lref = omlp.grads_all(th, dims, x, y, act=act, lik_scale=lam, prior=prior, sigma=sigma)
+    assert inf_rel(g, Gref) <= 1e-5
+    np.testing.assert_allclose(loss.cpu().numpy(), lref, rtol=1e-5)
+    np.testing.assert_allclose(ctx.gather("loss"), lref, rtol=1e-5)
+
+
+# ------------------------------------------------------------------ kernel phase a7-a10
+@pytest.mark.parametrize("n,d", [(1, 100), (2, 37), (3, 1000), (16, 5000), (33, 777), (64, 2048), (100, 96)])
+def test_step_from_set_grads_matches_oracle(n, d):
+    Th = synth.random_theta(n, d, seed=n + d, scale=0.2)
+    G = synth.random_grads(n, d, seed=n * d)
+    cfg = push.make_config(n, [d - 1, 1], max_batch=1, step_size=0.05)   # d = (d-1)*1 + 1 params
+    assert _d(cfg_dims(cfg)) == d
+    ctx = push.Context(cfg, theta0=Th)
+    ctx.set_grads(_dev(G))
+    ctx.svgd_step()
+    th1 = ctx.gather("theta")
+    ref, info = osvgd.svgd_step(Th, G, 0.05)
+    assert rel_err(th1, ref) <= 1e-4
+    D = ctx.gather("dist")
+    assert np.array_equal(D, D.T) and np.all(np.diag(D) == 0)
+    np.testing.assert_allclose(D, info["D"], rtol=1e-5, atol=1e-6 * max(info["D"].max(), 1e-30))
+    h = float(ctx.gather("h")[0])
+    assert h == pytest.approx(info["h"], rel=1e-5)
+    K = ctx.gather("kernel")
+    assert np.array_equal(K, K.T) and np.all(np.diag(K) == 1.0)
+
+
+def cfg_dims(cfg):
+    return [cfg.dims[i] for i in range(cfg.n_layers + 1)]
+
+
+@pytest.mark.parametrize("n", [2, 9, 16, 25])
+def test_bandwidth_bit_exact_on_dyadic_lattice(n):
+    """Dyadic Theta: every D_ij is exact in fp32 and fp64, so the GPU median equals the
+    oracle's bit for bit and h = fp32(med) * fp32(1/ln n) (R4)."""
+    d = 512
+    Th = synth.dyadic_theta(n, d, seed=n)
+    cfg = push.make_config(n, [d - 1, 1], max_batch=1)
+    ctx = push.Context(cfg, theta0=Th)
+    ctx.set_grads(_dev(np.zeros((n, d), np.float32)))
+    ctx.svgd_step()
+    D = ctx.gather("dist")
+    Dref = osvgd.sq_dists(Th)
+    assert np.array_equal(D.astype(np.float64), Dref)
+    med = osvgd.median_all(Dref)
+    expect = np.float32(med) * np.float32(1.0 / math.log(n))
+    assert ctx.gather("h")[0] == expect
+
+
+@pytest.mark.parametrize("rule", ["median_ln_n", "median_ln_n1", "fixed"])
+@pytest.mark.parametrize("n", [5, 16, 64])
+def test_bandwidth_reproduced_from_gpu_distances(rule, n):
+    """Selection on the GPU's own fp32 D (oracle median, same precision) reproduces h bit-exactly."""
+    d = 3000
+    Th = synth.random_theta(n, d, seed=100 + n)
+    cfg = push.make_config(n, [d - 1, 1], max_batch=1, bw_rule=rule, bw_h=0.75)
+    ctx = push.Context(cfg, theta0=Th)
+    ctx.set_grads(_dev(synth.random_grads(n, d, 3)))
+    ctx.svgd_step()
+    D = ctx.gather("dist")
+    h = ctx.gather("h")[0]
+    if rule == "fixed":
+        assert h == np.float32(0.75)
+        return
+    med = np.float32(osvgd.median_all(D.astype(np.float64)))
+    c = np.float32(1.0 / math.log(n if rule == "median_ln_n" else n + 1))
+    assert h == med * c
+
+
+def test_single_particle_is_gradient_ascent():
+    dims = [1, 32, 32, 1]
+    x, y = synth.batch("sine", 256, 1, 1)
+    ctx = push.Context(push.make_config(1, dims, max_batch=256, step_size=1e-2))
+    th0 = ctx.gather("theta")
+    ctx.particle_grads(_dev(x), _dev(y))
+    ctx.svgd_step()
+    assert ctx.gather("h")[0] == 1.0
+    g, _ = omlp.grad_log_post(th0[0], dims, x, y)
+    assert rel_err(ctx.gather("theta"), (th0[0] + 1e-2 * g)[None]) <= 1e-4
+
+
+def test_coincident_particles_stay_coincident():
+    d = 200
+    th = np.tile(synth.random_theta(1, d, 1), (4, 1))
+    G = np.tile(synth.random_grads(1, d, 2), (4, 1))
+    ctx = push.Context(push.make_config(4, [d - 1, 1], max_batch=1), theta0=th)
+    ctx.set_grads(_dev(G))
+    ctx.svgd_step()
+    t1 = ctx.gather("theta")
+    assert ctx.gather("h")[0] == 1.0
+    assert np.all(t1 == t1[0])
+
+
+# ------------------------------------------------------------------ whole step, free running
+def test_loss_trajectory_c1_100_steps():
+    w = WORKLOADS["C1"]
+    dims = list(w.dims)
+    x, y = synth.workload_batch(w, 0)
+    ctx = push.Context(push.make_config(w.n_particles, dims, max_batch=w.batch, step_size=1e-2, seed=0))
+    th0 = ctx.gather("theta")
+    xd, yd = _dev(x), _dev(y)
+    losses = []
+    loss = torch.empty(w.n_particles, device="cuda")
+    for _ in range(100):
+        ctx.particle_grads(xd, yd, loss)
+        ctx.svgd_step()
+        losses.append(loss.mean().item())
+    _, ml, _, _ = osvgd.svgd_run(th0, dims, lambda t: (x, y), 100, 1e-2)
+    np.testing.assert_allclose(np.array(losses), ml, rtol=1e-2)
+    assert ml[-1] < ml[0]
+
+
+def test_step_host_equals_device_path():
+    w = WORKLOADS["C1"]
+    x, y = synth.workload_batch(w, 0)
+    a = push.Context(push.make_config(w.n_particles, list(w.dims), max_batch=w.batch, seed=4))
+    b = push.Context(push.make_config(w.n_particles, list(w.dims), max_batch=w.batch, seed=4))
+    for _ in range(3):
+        la = a.step_host(x, y)
+        lb = torch.empty(w.n_particles, device="cuda")
+        b.particle_grads(_dev(x), _dev(y), lb)
+        b.svgd_step()
+        assert np.array_equal(la, lb.cpu().numpy())
+    assert np.array_equal(a.gather("theta"), b.gather("theta"))
+
+
+def test_state_machine_errors():
+    ctx = push.Context(push.make_config(2, [1, 32, 1], max_batch=8))
+    with pytest.raises(push.PushError) as e:
+        ctx.svgd_step()
+    assert e.value.status == push.PUSH_E_STATE
+    with pytest.raises(push.PushError) as e:
+        ctx.gather("dist")
+    assert e.value.status == push.PUSH_E_STATE
+    x = torch.zeros(9, 1, device="cuda")
+    with pytest.raises(push.PushError) as e:
+        ctx.particle_grads(x, x)
+    assert e.value.status == push.PUSH_E_SHAPE
+
+
+# ------------------------------------------------------------------ sharding (loopback transport)
+@pytest.mark.parametrize("dims,n,B", [([2, 64, 64, 1], 8, 256), ([1, 32, 32, 1], 4, 256)])
+def test_sharding_bit_identical_across_P(dims, n, B):
+    """Theta after 3 steps is bit-identical for P = 1, 2, 4 ranks."""
+    x, y = synth.batch("gauss", B, dims[0], dims[-1], 1)
+    xd, yd = _dev(x), _dev(y)
+    results = {}
+    for P in (1, 2, 4):
+        if n % P:
+            continue
+        cfg = push.make_config(n, dims, max_batch=B, step_size=1e-2, seed=9)
+        ctxs = push.local_group(cfg, P)
+        for _ in range(3):
+            for c in ctxs:
+                c.particle_grads(xd, yd)
+            for c in ctxs:
+                c.svgd_step()
+        results[P] = (ctxs[0].gather("theta"), ctxs[-1].gather("loss"), ctxs[0].gather("dist"))
+    base = results[1]
+    for P, r in results.items():
+        assert np.array_equal(r[0], base[0]), P
+        assert np.array_equal(r[1], base[1]), P
+        assert np.array_equal(r[2], base[2]), P
+
+
+# ------------------------------------------------------------------ 1-D Gaussian target through set_grads
+def test_gaussian_target_closed_form_on_gpu():
+    mu, sig, n = 1.0, 2.0, 64
+    from scipy.stats import norm
+    th = (mu + sig * norm.ppf((np.arange(n) + 0.5) / n)).reshape(n, 1).astype(np.float32)
+    # dims [1, 1] -> d = 2 (w, b); the second coordinate is held at 0 with zero gradient
+    theta0 = np.concatenate([th, np.zeros((n, 1), np.float32)], 1)
+    ctx = push.Context(push.make_config(n, [1, 1], max_batch=1, step_size=0.2), theta0=theta0)
+    for _ in range(800):
+        t = torch.from_numpy(ctx.gather("theta")).cuda()
+        g = -(t - mu) / sig ** 2
+        g[:, 1] = 0.0
+        ctx.set_grads(g.contiguous())
+        ctx.svgd_step()
+    t = ctx.gather("theta")[:, 0].astype(np.float64)
+    assert abs(t.mean() - mu) < 1e-4
+    assert abs(t.var() / sig ** 2 - 1.0) <= 0.08
+
+
+# ------------------------------------------------------------------ full size (bench configuration, sampled)
+def test_c2_full_size_sampled_parity():
+    """BASELINE configs[1] at full size (16 x 198,401 params, B = 8192): g of sampled particles
+    against the oracle one by one, and theta' of the whole step against the oracle's step."""
+    w = WORKLOADS["C2"]
+    dims = list(w.dims)
+    x, y = synth.workload_batch(w, 0)
+    ctx = push.Context(push.make_config(w.n_particles, dims, max_batch=w.batch, step_size=1e-3, seed=0))
+    th0 = ctx.gather("theta")
+    ctx.particle_grads(_dev(x), _dev(y))
+    ctx.svgd_step()
+    g = ctx.gather("grad")
+    for i in (0, 7, 15):
+        gref, _ = omlp.grad_log_post(th0[i], dims, x, y)
+        assert inf_rel(g[i:i + 1], gref[None]) <= 1e-5, i
+    ref, info = osvgd.svgd_step(th0, g.astype(np.float64), 1e-3)
+    assert rel_err(ctx.gather("theta"), ref) <= 1e-4
+    assert float(ctx.gather("h")[0]) == pytest.approx(info["h"], rel=1e-5)
