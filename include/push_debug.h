@@ -34,6 +34,14 @@ push_status pushdbg_gemm3xtf32(int32_t a_mn, int32_t b_mn, int32_t M, int32_t N,
 push_status pushdbg_gemm1xtf32(int32_t a_mn, int32_t b_mn, int32_t M, int32_t N, int32_t K, int32_t batch,
                                const float* A_dev, const float* B_dev, float* C_dev, void* stream);
 
+/* ASYNC.  General form of the two entries above: passes = 1 or 3; b_split = 1 feeds B as
+ * plain fp32 split into hi/lo on the staged tile inside the kernel (the path the weight-gradient
+ * GEMM uses for its activation operand); b_split = 0 pre-splits B into a hi/lo pair in global
+ * memory (the path the forward/backward GEMMs use for the weights).  A is always split in-kernel.
+ * Same layouts, constraints and errors as pushdbg_gemm3xtf32 (PUSH_E_INVALID for bad passes). */
+push_status pushdbg_gemm(int32_t passes, int32_t a_mn, int32_t b_mn, int32_t b_split, int32_t M, int32_t N, int32_t K,
+                         int32_t batch, const float* A_dev, const float* B_dev, float* C_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,24 +1,28 @@
 // gemm.cu — batched fp32 GEMM on the 5th-gen tensor cores in 3xTF32 split precision.
 //
 // Used for the per-particle MLP contractions of the SVGD step (DESIGN.md a2/a4/a5):
-//   a2  Z_l = A_{l-1} W_l^T (+ b_l, sigma)       A K-major, W K-major      -> EPI_FWD
-//   a4  delta_{l-1} = (delta_l W_l) * sigma'     delta K-major, W MN-major -> EPI_BWD
-//   a5  dW_l = delta_l^T A_{l-1}  (split-K)      both MN-major             -> EPI_STORE
+//   a2  A_l = sigma(A_{l-1} W_l^T + b_l)            A K-major,  W K-major  (pre-split)   -> EPI_FWD
+//   a4  delta_{l-1} = (delta_l W_l) * sigma'(a_{l-1}) delta K-major, W MN-major (pre-split) -> EPI_BWD
+//   a5  dW_l = delta_l^T A_{l-1}   (split-K)          both MN-major, both split in-kernel  -> EPI_STORE
 //
-// Every operand x is stored as a pair of float32 arrays hi = tf32_rn(x),
-// lo = tf32_rn(x - hi) (written by the producing epilogue or split_hilo_kernel), and
-//   C = A_lo*B_hi + A_hi*B_lo + A_hi*B_hi            (3 tcgen05.mma kind::tf32 per k-step)
-// accumulates in TMEM in fp32 (the classic 3xTF32 scheme; lo*lo is dropped).
+// 3xTF32: every operand x is used as hi = tf32_rn(x), lo = x - hi and
+//   C = A_lo*B_hi + A_hi*B_lo + A_hi*B_hi       (3 tcgen05.mma kind::tf32 per k-step, lo*lo dropped)
+// accumulated in TMEM in fp32.  Activations and deltas live in HBM as ONE fp32 array; the hi/lo
+// split happens on the staged shared-memory tile (transform warps), so each byte is read once.
 //
-// Kernel shape (v2): one 128 x BN output tile per CTA, 6 warps:
-//   warp 0 lane 0  TMA producer (4 bulk-tensor loads per stage into swizzled smem)
-//   warp 1 lane 0  MMA issuer (single thread, tcgen05.mma + tcgen05.commit)
-//   warps 2-5      drain/epilogue: every 128 of K the TMEM partial (double-buffered, 2 x BN
-//                  columns) is added into fp32 registers with round-to-nearest — the tensor-core
-//                  accumulator truncates on each accumulate, so long chains would cost ~K/8 ulps;
-//                  then the fused op and the store.  Warp 2 also owns the TMEM allocation.
+// Kernel shape (v3): persistent, one CTA per SM, tiles of 128 x BN, 12 warps:
+//   warp 0 lane 0   TMA producer (A fp32 tile; B as hi/lo pair or fp32 tile) into a STAGES ring
+//   warp 1 lane 0   MMA issuer (single thread, tcgen05.mma + tcgen05.commit); warp 1 owns TMEM
+//   warps 2-3       transform: hi = tf32_rn(x) in place, lo = x - hi into the stage's lo slot
+//   warps 4-11      epilogue: TMEM lane quarter q = warp % 4, column half h = (warp - 4) / 4.
+//                   Every 128 of K the TMEM partial (NACC buffers of BN columns, rotating across
+//                   tiles, so the MMAs of the next tile overlap this epilogue) is added into fp32
+//                   registers with round-to-nearest — the tensor-core accumulator truncates on
+//                   each accumulate, so long chains would cost ~K/8 ulps.  The fused op is then
+//                   applied on a swizzled 32x32 smem box per warp and written with a TMA store.
 #include <cudaTypedefs.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -31,30 +35,43 @@ namespace gemm {
 constexpr int BM = 128;
 constexpr int BK = 32;          // fp32 per k-block = 128 B = one SWIZZLE_128B row
 constexpr int kChunkKB = 4;     // k-blocks per TMEM accumulation chunk (128 of K) before fp32 promotion
-constexpr int kEpiThreads = 128;
-constexpr int kThreads = 64 + kEpiThreads;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue (warp 2 owns TMEM)
+constexpr int kXfWarp0 = 2, kXfWarps = 2, kXfThreads = 32 * kXfWarps;
+constexpr int kEpiWarp0 = kXfWarp0 + kXfWarps, kEpiWarps = 8;
+constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
+constexpr int kEpiBox = 32 * 32 * 4;  // one 32 x 32 fp32 SWIZZLE_128B box per epilogue warp
+constexpr int kMaxSmem = 232448;      // 227 KB opt-in dynamic shared memory per CTA
 
 template <int BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
-  static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
+  static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // A(hi), A_lo, B_hi, B_lo
+  static constexpr int EPI_BYTES = kEpiWarps * kEpiBox;
+  static constexpr int BAR_BYTES = 512;
+  static constexpr int STAGES_RAW = (kMaxSmem - 1024 - EPI_BYTES - BAR_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
-  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered accumulator
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int NACC = 4;                       // TMEM accumulator buffers
+  static constexpr int TMEM_COLS = NACC * BN;          // 512 / 256 / 128
+  static constexpr int EPI_SPLIT = BN >= 64 ? 2 : 1;   // epilogue warps per TMEM lane quarter
+  static constexpr int CW = BN / EPI_SPLIT;            // columns per epilogue thread
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
+  static_assert(STAGES >= 2, "smem");
+  static_assert(SMEM_BYTES <= kMaxSmem, "smem");
+  static_assert(CW % 32 == 0, "epilogue box");
 };
 
 struct KParams {
-  int M, N, K, splits, kb_per_split, passes, epi, act;
-  float* out0;
-  float* out1;
-  long long ldo, out_pstride, out_sstride;
+  int M, N, K, batch, splits, kb_per_split, passes, epi, act;
+  int mt, nt, ntiles;
+  int a_pz, b_pz;  // 1: operand batched over particles; 0: shared (particle coordinate 0)
   const float* bias;
   long long bias_pstride;
-  const float* aprev_hi;
-  const float* aprev_lo;
-  long long ld_aprev, aprev_pstride;
+  float* bpart;
+  long long bp_sstride, bp_pstride;
+  const float* x;
+  int din;
+  float* xpart;
+  long long xp_sstride, xp_pstride;
 };
 
 // Stage one operand tile (ROWS along M or N, BK along K) into SWIZZLE_128B smem.
@@ -84,45 +101,81 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t base, int ks) {
     return ptx::umma_desc(base + ks * 1024, 4096, 512, 1);
 }
 
-template <int BN, bool AMN, bool BMN>
+// hi = tf32_rn(x) in place, lo = x - hi at `lo` (elementwise, so layout-agnostic).
+__device__ __forceinline__ void split_tile(uint8_t* base, uint8_t* lo, int bytes, int tx) {
+  float4* ph = reinterpret_cast<float4*>(base);
+  float4* pl = reinterpret_cast<float4*>(lo);
+#pragma unroll 4
+  for (int i = tx; i < bytes / 16; i += kXfThreads) {
+    const float4 v = ph[i];
+    float4 h, l;
+    h.x = ptx::tf32_rna(v.x); l.x = v.x - h.x;
+    h.y = ptx::tf32_rna(v.y); l.y = v.y - h.y;
+    h.z = ptx::tf32_rna(v.z); l.z = v.z - h.z;
+    h.w = ptx::tf32_rna(v.w); l.w = v.w - h.w;
+    ph[i] = h;
+    pl[i] = l;
+  }
+}
+
+// element (r, k) of a 32 x 32 fp32 SWIZZLE_128B box: 16-B chunk (k/4) of row r sits at chunk (k/4) ^ (r%8)
+__device__ __forceinline__ int box_idx(int r, int k) { return r * 32 + ((((k >> 2) ^ (r & 7)) << 2) | (k & 3)); }
+
+struct TileCoord {
+  int p, split, m0, nt;  // particle, K-split, first row, column-tile index
+};
+__device__ __forceinline__ TileCoord decode(int t, const KParams& prm) {
+  TileCoord c;
+  const int nt = t % prm.nt;
+  t /= prm.nt;
+  const int mt = t % prm.mt;
+  t /= prm.mt;
+  c.split = t % prm.splits;
+  c.p = t / prm.splits;
+  c.m0 = mt * BM;
+  c.nt = nt;
+  return c;
+}
+
+template <int BN, bool AMN, bool BMN, bool BSPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
-                      const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
-                      const KParams prm) {
+    gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tBhi,
+                      const __grid_constant__ CUtensorMap tBlo, const __grid_constant__ CUtensorMap tOut,
+                      const __grid_constant__ CUtensorMap tAux, const KParams prm) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;  // [2] accumulator b holds a finished K-chunk
-  uint64_t* tempty = tfull + 2;         // [2] accumulator b has been drained to registers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* ebuf_all = smem + C::STAGES * C::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ebuf_all + C::EPI_BYTES);
+  uint64_t* ready = full + C::STAGES;
+  uint64_t* empty = ready + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;   // [NACC] accumulator b holds a finished K-chunk
+  uint64_t* tempty = tfull + C::NACC;    // [NACC] accumulator b has been drained to registers
+  uint64_t* auxbar = tempty + C::NACC;   // [kEpiWarps] aprev box landed in the warp's smem box
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const int p = blockIdx.z / prm.splits, split = blockIdx.z % prm.splits;
   const int nkb_total = (prm.K + BK - 1) / BK;
-  const int kb0 = split * prm.kb_per_split;
-  const int kb1 = min(nkb_total, kb0 + prm.kb_per_split);
-  const int nkb = kb1 - kb0;  // >= 1 (host guarantees non-empty splits)
-  const int nchunks = (nkb + kChunkKB - 1) / kChunkKB;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&ready[s], kXfThreads);
       ptx::mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < C::NACC; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], kEpiThreads);
+      ptx::mbar_init(&tempty[b], 32 * 4 * C::EPI_SPLIT);
     }
+    for (int e = 0; e < kEpiWarps; ++e) ptx::mbar_init(&auxbar[e], 1);
     ptx::fence_mbar_init();
-    ptx::prefetch_tmap(&tA_hi);
-    ptx::prefetch_tmap(&tA_lo);
-    ptx::prefetch_tmap(&tB_hi);
-    ptx::prefetch_tmap(&tB_lo);
+    ptx::prefetch_tmap(&tA);
+    ptx::prefetch_tmap(&tBhi);
+    if (!BSPLIT) ptx::prefetch_tmap(&tBlo);
+    ptx::prefetch_tmap(&tOut);
+    if (prm.epi == EPI_BWD) ptx::prefetch_tmap(&tAux);
   }
-  if (warp == 2) {
+  if (warp == 1) {
     ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
     ptx::tmem_relinquish();
   }
@@ -131,142 +184,228 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  auto tile_kb = [&](int split, int* kb0) {
+    *kb0 = split * prm.kb_per_split;
+    return min(nkb_total, *kb0 + prm.kb_per_split) - *kb0;
+  };
+
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % C::STAGES;
-        const uint32_t round = i / C::STAGES;
-        ptx::mbar_wait(&empty[s], (round & 1) ^ 1);
-        uint8_t* st = smem + s * C::STAGE_BYTES;
-        ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-        const int k = (kb0 + i) * BK;
-        load_operand<AMN, BM>(&tA_hi, st, &full[s], m0, k, p);
-        load_operand<AMN, BM>(&tA_lo, st + C::A_BYTES, &full[s], m0, k, p);
-        load_operand<BMN, BN>(&tB_hi, st + 2 * C::A_BYTES, &full[s], n0, k, p);
-        load_operand<BMN, BN>(&tB_lo, st + 2 * C::A_BYTES + C::B_BYTES, &full[s], n0, k, p);
+      constexpr uint32_t kTx = C::A_BYTES + (BSPLIT ? C::B_BYTES : 2 * C::B_BYTES);
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < prm.ntiles; t += gridDim.x) {
+        TileCoord tc = decode(t, prm);
+        const int n0 = tc.nt * BN;
+        int kb0;
+        const int nkb = tile_kb(tc.split, &kb0);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const int s = it % C::STAGES;
+          const uint32_t u = it / C::STAGES;
+          ptx::mbar_wait(&empty[s], (u & 1) ^ 1);
+          uint8_t* st = smem + s * C::STAGE_BYTES;
+          ptx::mbar_arrive_expect_tx(&full[s], kTx);
+          const int k = (kb0 + i) * BK;
+          load_operand<AMN, BM>(&tA, st, &full[s], tc.m0, k, tc.p * prm.a_pz);
+          load_operand<BMN, BN>(&tBhi, st + 2 * C::A_BYTES, &full[s], n0, k, tc.p * prm.b_pz);
+          if (!BSPLIT) load_operand<BMN, BN>(&tBlo, st + 2 * C::A_BYTES + C::B_BYTES, &full[s], n0, k, tc.p * prm.b_pz);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer: K-chunks of kChunkKB k-blocks alternate between two TMEM accumulators
+      // ---------------- MMA issuer: K-chunks of kChunkKB k-blocks rotate over NACC TMEM accumulators
       constexpr uint32_t idesc = ptx::idesc_tf32(BM, BN, AMN, BMN);
-      for (int i = 0; i < nkb; ++i) {
-        const int c = i / kChunkKB, b = c & 1;
-        const bool first = (i % kChunkKB) == 0;
-        const bool last = (i % kChunkKB) == kChunkKB - 1 || i == nkb - 1;
-        if (first && c >= 2) ptx::mbar_wait(&tempty[b], ((c >> 1) - 1) & 1);
-        const int s = i % C::STAGES;
-        const uint32_t round = i / C::STAGES;
-        ptx::mbar_wait(&full[s], round & 1);
-        ptx::tc_fence_after();
-        const uint32_t a_hi = ptx::smem_u32(smem + s * C::STAGE_BYTES);
-        const uint32_t a_lo = a_hi + C::A_BYTES;
-        const uint32_t b_hi = a_hi + 2 * C::A_BYTES;
-        const uint32_t b_lo = b_hi + C::B_BYTES;
-        const uint32_t d = tmem_base + b * BN;
+      uint32_t it = 0, ch = 0;
+      for (int t = blockIdx.x; t < prm.ntiles; t += gridDim.x) {
+        TileCoord tc = decode(t, prm);
+        int kb0;
+        const int nkb = tile_kb(tc.split, &kb0);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const bool first = (i % kChunkKB) == 0;
+          const bool last = (i % kChunkKB) == kChunkKB - 1 || i == nkb - 1;
+          const int b = ch % C::NACC;
+          if (first) ptx::mbar_wait(&tempty[b], ((ch / C::NACC) & 1) ^ 1);
+          const int s = it % C::STAGES;
+          ptx::mbar_wait(&ready[s], (it / C::STAGES) & 1);
+          ptx::tc_fence_after();
+          const uint32_t a_hi = ptx::smem_u32(smem + s * C::STAGE_BYTES);
+          const uint32_t a_lo = a_hi + C::A_BYTES;
+          const uint32_t b_hi = a_hi + 2 * C::A_BYTES;
+          const uint32_t b_lo = b_hi + C::B_BYTES;
+          const uint32_t d = tmem_base + b * BN;
 #pragma unroll
-        for (int ks = 0; ks < BK / 8; ++ks) {
-          const uint64_t dah = op_desc<AMN>(a_hi, ks), dal = op_desc<AMN>(a_lo, ks);
-          const uint64_t dbh = op_desc<BMN>(b_hi, ks), dbl = op_desc<BMN>(b_lo, ks);
-          const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-          if (prm.passes == 3) {
-            ptx::mma_tf32(d, dal, dbh, idesc, acc);  // small terms first
-            ptx::mma_tf32(d, dah, dbl, idesc, 1u);
-            ptx::mma_tf32(d, dah, dbh, idesc, 1u);
-          } else {
-            ptx::mma_tf32(d, dah, dbh, idesc, acc);
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint64_t dah = op_desc<AMN>(a_hi, ks), dal = op_desc<AMN>(a_lo, ks);
+            const uint64_t dbh = op_desc<BMN>(b_hi, ks), dbl = op_desc<BMN>(b_lo, ks);
+            const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+            if (prm.passes == 3) {
+              ptx::mma_tf32(d, dal, dbh, idesc, acc);  // small terms first
+              ptx::mma_tf32(d, dah, dbl, idesc, 1u);
+              ptx::mma_tf32(d, dah, dbh, idesc, 1u);
+            } else {
+              ptx::mma_tf32(d, dah, dbh, idesc, acc);
+            }
+          }
+          ptx::mma_commit(&empty[s]);  // frees the smem stage when these MMAs complete
+          if (last) {
+            ptx::mma_commit(&tfull[b]);
+            ++ch;
           }
         }
-        ptx::mma_commit(&empty[s]);    // frees the smem stage when these MMAs complete
-        if (last) ptx::mma_commit(&tfull[b]);
+      }
+    }
+  } else if (warp < kEpiWarp0) {
+    // ---------------- transform warps: split the staged fp32 tiles into tf32 hi (in place) + lo
+    const int tx = threadIdx.x - 32 * kXfWarp0;
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < prm.ntiles; t += gridDim.x) {
+      TileCoord tc = decode(t, prm);
+      int kb0;
+      const int nkb = tile_kb(tc.split, &kb0);
+      for (int i = 0; i < nkb; ++i, ++it) {
+        const int s = it % C::STAGES;
+        ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
+        uint8_t* st = smem + s * C::STAGE_BYTES;
+        split_tile(st, st + C::A_BYTES, C::A_BYTES, tx);
+        if (BSPLIT) split_tile(st + 2 * C::A_BYTES, st + 2 * C::A_BYTES + C::B_BYTES, C::B_BYTES, tx);
+        ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core (async proxy)
+        ptx::mbar_arrive(&ready[s]);
       }
     }
   } else {
-    // ---------------- epilogue warps 2..5: TMEM lane quarter q = warp % 4
-    const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
-    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-    float acc[BN];
+    // ---------------- epilogue warps
+    const int e = warp - kEpiWarp0;
+    const int q = warp & 3;      // TMEM lane quarter this warp may access
+    const int h = e >> 2;        // column half
+    if (h < C::EPI_SPLIT) {
+      float* ebuf = reinterpret_cast<float*>(ebuf_all + e * kEpiBox);
+      const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+      uint32_t ch = 0, aux_ph = 0;
+      const bool bwd = prm.epi == EPI_BWD;
+      for (int t = blockIdx.x; t < prm.ntiles; t += gridDim.x) {
+        TileCoord tc = decode(t, prm);
+        const int n0 = tc.nt * BN;
+        int kb0;
+        const int nkb = tile_kb(tc.split, &kb0);
+        const int nchunks = (nkb + kChunkKB - 1) / kChunkKB;
+        const int row0 = tc.m0 + q * 32;
+        const bool live = row0 < prm.M;
+        const int colw = n0 + h * C::CW;
+        if (bwd && live && lane == 0) {  // prefetch the first aprev box while the MMAs run
+          ptx::bulk_wait_read0();
+          ptx::mbar_arrive_expect_tx(&auxbar[e], kEpiBox);
+          ptx::tma_load_3d(ebuf, &tAux, &auxbar[e], colw, row0, tc.p);
+        }
+        float acc[C::CW];
 #pragma unroll
-    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
-    // fp32 promotion: every K-chunk's TMEM partial is added (round-to-nearest) into registers,
-    // bounding the tensor-core accumulation chain to kChunkKB*BK*3/8 accumulates.
-    for (int c = 0; c < nchunks; ++c) {
-      const int b = c & 1;
-      ptx::mbar_wait(&tfull[b], (c >> 1) & 1);
-      ptx::tc_fence_after();
+        for (int j = 0; j < C::CW; ++j) acc[j] = 0.f;
+        // fp32 promotion: every K-chunk's TMEM partial is added (round-to-nearest) into registers,
+        // bounding the tensor-core accumulation chain to kChunkKB*BK*3/8 accumulates.
+        for (int c = 0; c < nchunks; ++c, ++ch) {
+          const int b = ch % C::NACC;
+          ptx::mbar_wait(&tfull[b], (ch / C::NACC) & 1);
+          ptx::tc_fence_after();
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(lane_base + b * BN + c0, r);
-        ptx::tmem_ld_wait();
+          for (int c0 = 0; c0 < C::CW; c0 += 32) {
+            uint32_t r[32];
+            ptx::tmem_ld_32x32b_x32(lane_base + b * BN + h * C::CW + c0, r);
+            ptx::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[c0 + j] += __uint_as_float(r[j]);
-      }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[b]);
-    }
-    if (row < prm.M) {
+            for (int j = 0; j < 32; ++j) acc[c0 + j] += __uint_as_float(r[j]);
+          }
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&tempty[b]);
+        }
+        if (!live) continue;
+        const int pz = prm.epi == EPI_STORE ? tc.split * prm.batch + tc.p : tc.p;
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        const int n = n0 + c0;
-        if (prm.epi == EPI_STORE) {
-          float4* o = reinterpret_cast<float4*>(prm.out0 + p * prm.out_pstride + split * prm.out_sstride +
-                                                static_cast<long long>(row) * prm.ldo + n);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            o[j] = make_float4(acc[c0 + 4 * j], acc[c0 + 4 * j + 1], acc[c0 + 4 * j + 2], acc[c0 + 4 * j + 3]);
-        } else {
-          const long long obase = p * prm.out_pstride + static_cast<long long>(row) * prm.ldo + n;
-          float4* oh = reinterpret_cast<float4*>(prm.out0 + obase);
-          float4* ol = reinterpret_cast<float4*>(prm.out1 + obase);
+        for (int j = 0; j < C::CW / 32; ++j) {
+          const int col = colw + j * 32;
+          if (bwd) {
+            if (j > 0 && lane == 0) {
+              ptx::bulk_wait_read0();
+              ptx::mbar_arrive_expect_tx(&auxbar[e], kEpiBox);
+              ptx::tma_load_3d(ebuf, &tAux, &auxbar[e], col, row0, tc.p);
+            }
+            ptx::mbar_wait(&auxbar[e], aux_ph);
+            aux_ph ^= 1;
+          } else {
+            if (lane == 0) ptx::bulk_wait_read0();  // previous store has finished reading the box
+            __syncwarp();
+          }
+          float* rowp = ebuf + lane * 32;
           if (prm.epi == EPI_FWD) {
-            const float* bias = prm.bias + p * prm.bias_pstride + n;
+            const float4* bias = reinterpret_cast<const float4*>(prm.bias + tc.p * prm.bias_pstride + col);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float h[4], l[4];
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                const float a = act_fwd(acc[c0 + 4 * j + t] + __ldg(bias + 4 * j + t), prm.act);
-                h[t] = ptx::tf32_rna(a);
-                l[t] = ptx::tf32_rna(a - h[t]);
-              }
-              oh[j] = make_float4(h[0], h[1], h[2], h[3]);
-              ol[j] = make_float4(l[0], l[1], l[2], l[3]);
+            for (int c4 = 0; c4 < 8; ++c4) {
+              const float4 bv = __ldg(bias + c4);
+              float4 v;
+              v.x = act_fwd(acc[j * 32 + 4 * c4 + 0] + bv.x, prm.act);
+              v.y = act_fwd(acc[j * 32 + 4 * c4 + 1] + bv.y, prm.act);
+              v.z = act_fwd(acc[j * 32 + 4 * c4 + 2] + bv.z, prm.act);
+              v.w = act_fwd(acc[j * 32 + 4 * c4 + 3] + bv.w, prm.act);
+              *reinterpret_cast<float4*>(rowp + ((c4 ^ (lane & 7)) << 2)) = v;
             }
-          } else {  // EPI_BWD
-            const long long abase = p * prm.aprev_pstride + static_cast<long long>(row) * prm.ld_aprev + n;
-            const float4* ah = reinterpret_cast<const float4*>(prm.aprev_hi + abase);
-            const float4* al = reinterpret_cast<const float4*>(prm.aprev_lo + abase);
+          } else if (bwd) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 xh = __ldg(ah + j), xl = __ldg(al + j);
-              const float av[4] = {xh.x + xl.x, xh.y + xl.y, xh.z + xl.z, xh.w + xl.w};
-              float h[4], l[4];
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                const float v = acc[c0 + 4 * j + t] * act_deriv_from_a(av[t], prm.act);
-                h[t] = ptx::tf32_rna(v);
-                l[t] = ptx::tf32_rna(v - h[t]);
-              }
-              oh[j] = make_float4(h[0], h[1], h[2], h[3]);
-              ol[j] = make_float4(l[0], l[1], l[2], l[3]);
+            for (int c4 = 0; c4 < 8; ++c4) {
+              float4* pp = reinterpret_cast<float4*>(rowp + ((c4 ^ (lane & 7)) << 2));
+              const float4 a = *pp;
+              float4 v;
+              v.x = acc[j * 32 + 4 * c4 + 0] * act_deriv_from_a(a.x, prm.act);
+              v.y = acc[j * 32 + 4 * c4 + 1] * act_deriv_from_a(a.y, prm.act);
+              v.z = acc[j * 32 + 4 * c4 + 2] * act_deriv_from_a(a.z, prm.act);
+              v.w = acc[j * 32 + 4 * c4 + 3] * act_deriv_from_a(a.w, prm.act);
+              *pp = v;
             }
+          } else {
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4)
+              *reinterpret_cast<float4*>(rowp + ((c4 ^ (lane & 7)) << 2)) =
+                  make_float4(acc[j * 32 + 4 * c4], acc[j * 32 + 4 * c4 + 1], acc[j * 32 + 4 * c4 + 2],
+                              acc[j * 32 + 4 * c4 + 3]);
+          }
+          __syncwarp();
+          if (bwd && prm.bpart) {
+            // a5 of the layer below: column partial sums of delta over this warp's 32 rows (rows >= M are
+            // zero: their A rows were zero-filled by TMA), in ascending row order; lane = column.
+            const int rb = row0 / 32;
+            float s = 0.f;
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) s += ebuf[box_idx(r, lane)];
+            prm.bpart[rb * prm.bp_sstride + tc.p * prm.bp_pstride + col + lane] = s;
+            for (int i = 0; i < prm.din; ++i) {
+              float sx = 0.f;
+              for (int r = 0; r < 32; ++r) {
+                const int row = row0 + r;
+                const float xv = row < prm.M ? __ldg(prm.x + (long long)row * prm.din + i) : 0.f;
+                sx = fmaf(ebuf[box_idx(r, lane)], xv, sx);
+              }
+              prm.xpart[rb * prm.xp_sstride + tc.p * prm.xp_pstride + (long long)(col + lane) * prm.din + i] = sx;
+            }
+          }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_3d(&tOut, ebuf, col, row0, pz);
+            ptx::bulk_commit();
           }
         }
       }
+      if (lane == 0) ptx::bulk_wait0();
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 2) ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
+  if (warp == 1) ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
 }
 
 // ------------------------------------------------------------------ host side
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
+int g_sms = 0;
 
 push_status get_encoder() {
   std::call_once(g_encode_once, [] {
@@ -275,59 +414,70 @@ push_status get_encoder() {
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
   });
   if (!g_encode) return fail(PUSH_E_CUDA, "cuTensorMapEncodeTiled not available from the driver");
   return PUSH_OK;
 }
 
-// 3-D fp32 tensor map {d0 (contiguous), d1, d2} with box {32, box1, 1}, SWIZZLE_128B, zero OOB fill.
+// 3-D fp32 tensor map {d0 (contiguous), d1, d2} with box {32, box1, 1}, zero OOB fill.
 push_status make_map(CUtensorMap* m, const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_el,
                      uint64_t stride2_el, uint32_t box1, CUtensorMapSwizzle swz) {
+  if (d2 <= 1) {  // a shared operand: the stride of a unit dimension is never used
+    d2 = 1;
+    stride2_el = stride1_el * d1;
+  }
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {stride1_el * 4, stride2_el * 4};
   cuuint32_t box[3] = {32, box1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(PUSH_E_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string(int(r)) + ")");
   return PUSH_OK;
 }
 
-push_status make_operand_maps(const Operand& op, int mn_extent, int K, int batch, int box_rows, CUtensorMap* mhi,
-                              CUtensorMap* mlo) {
-  push_status st;
-  if (!op.mn_major) {
-    const CUtensorMapSwizzle z = CU_TENSOR_MAP_SWIZZLE_128B;
-    if ((st = make_map(mhi, op.hi, K, mn_extent, batch, op.ld, op.pstride, box_rows, z)) != PUSH_OK) return st;
-    return make_map(mlo, op.lo, K, mn_extent, batch, op.ld, op.pstride, box_rows, z);
-  }
-  const CUtensorMapSwizzle z = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
-  if ((st = make_map(mhi, op.hi, mn_extent, K, batch, op.ld, op.pstride, 32, z)) != PUSH_OK) return st;
-  return make_map(mlo, op.lo, mn_extent, K, batch, op.ld, op.pstride, 32, z);
+push_status make_operand_map(const float* ptr, const Operand& op, int mn_extent, int K, int batch, int box_rows,
+                             CUtensorMap* m) {
+  const int b = op.pstride == 0 ? 1 : batch;
+  if (!op.mn_major)
+    return make_map(m, ptr, K, mn_extent, b, op.ld, op.pstride, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
+  return make_map(m, ptr, mn_extent, K, b, op.ld, op.pstride, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
-template <int BN, bool AMN, bool BMN>
-push_status launch_t(const CUtensorMap* maps, const KParams& kp, dim3 grid, cudaStream_t stream) {
+template <int BN, bool AMN, bool BMN, bool BS>
+push_status launch_t(const CUtensorMap* maps, const KParams& kp, cudaStream_t stream) {
   using C = Cfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    PUSH_CUDA_TRY(cudaFuncSetAttribute(gemm3xtf32_kernel<BN, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       C::SMEM_BYTES));
+    PUSH_CUDA_TRY(cudaFuncSetAttribute(gemm3xtf32_kernel<BN, AMN, BMN, BS>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
     attr_set = true;
   }
-  gemm3xtf32_kernel<BN, AMN, BMN><<<grid, kThreads, C::SMEM_BYTES, stream>>>(maps[0], maps[1], maps[2], maps[3], kp);
+  const int grid = kp.ntiles < g_sms ? kp.ntiles : g_sms;
+  gemm3xtf32_kernel<BN, AMN, BMN, BS>
+      <<<grid, kThreads, C::SMEM_BYTES, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], kp);
   PUSH_CUDA_TRY(cudaGetLastError());
   return PUSH_OK;
 }
 
 template <int BN>
-push_status launch_bn(bool amn, bool bmn, const CUtensorMap* maps, const KParams& kp, dim3 grid, cudaStream_t s) {
-  if (!amn && !bmn) return launch_t<BN, false, false>(maps, kp, grid, s);
-  if (!amn && bmn) return launch_t<BN, false, true>(maps, kp, grid, s);
-  if (amn && !bmn) return launch_t<BN, true, false>(maps, kp, grid, s);
-  return launch_t<BN, true, true>(maps, kp, grid, s);
+push_status launch_bn(bool amn, bool bmn, bool bs, const CUtensorMap* maps, const KParams& kp, cudaStream_t s) {
+  const int key = (amn ? 4 : 0) | (bmn ? 2 : 0) | (bs ? 1 : 0);
+  switch (key) {
+    case 0: return launch_t<BN, false, false, false>(maps, kp, s);
+    case 1: return launch_t<BN, false, false, true>(maps, kp, s);
+    case 2: return launch_t<BN, false, true, false>(maps, kp, s);
+    case 3: return launch_t<BN, false, true, true>(maps, kp, s);
+    case 4: return launch_t<BN, true, false, false>(maps, kp, s);
+    case 5: return launch_t<BN, true, false, true>(maps, kp, s);
+    case 6: return launch_t<BN, true, true, false>(maps, kp, s);
+    default: return launch_t<BN, true, true, true>(maps, kp, s);
+  }
 }
 }  // namespace
 
@@ -340,29 +490,54 @@ int choose_bn(int N) {
 push_status run(const Problem& pb, cudaStream_t stream) {
   if (pb.M < 1 || pb.N < 1 || pb.K < 1 || pb.batch < 1) return fail(PUSH_E_SHAPE, "gemm: empty problem");
   if (pb.N % 32) return fail(PUSH_E_SHAPE, "gemm: N must be a multiple of 32");
+  if (!pb.A.split) return fail(PUSH_E_INVALID, "gemm: A must be a plain fp32 operand (split in-kernel)");
   if (pb.A.mn_major && pb.M % 32) return fail(PUSH_E_SHAPE, "gemm: MN-major A needs M % 32 == 0");
-  if ((pb.A.ld % 4) || (pb.B.ld % 4) || (pb.A.pstride % 4) || (pb.B.pstride % 4))
-    return fail(PUSH_E_SHAPE, "gemm: operand strides must be multiples of 4 elements");
+  if ((pb.A.ld % 4) || (pb.B.ld % 4) || (pb.A.pstride % 4) || (pb.B.pstride % 4) || (pb.ldo % 4) ||
+      (pb.out_pstride % 4))
+    return fail(PUSH_E_SHAPE, "gemm: strides must be multiples of 4 elements");
+  if (pb.epi == EPI_BWD && (!pb.aprev || (pb.ld_aprev % 4) || (pb.aprev_pstride % 4)))
+    return fail(PUSH_E_SHAPE, "gemm: BWD needs aprev with strides % 4 == 0");
+  if (pb.epi != EPI_STORE && pb.splits != 1) return fail(PUSH_E_INVALID, "gemm: split-K only with EPI_STORE");
+  if (pb.splits > 1 && pb.out_sstride != (int64_t)pb.batch * pb.out_pstride)
+    return fail(PUSH_E_INVALID, "gemm: split partials must be [s][p] contiguous");
   push_status st;
   if ((st = get_encoder()) != PUSH_OK) return st;
   const int BN = choose_bn(pb.N);
   const int nkb = (pb.K + BK - 1) / BK;
   const int kbps = (nkb + pb.splits - 1) / pb.splits;
   if ((nkb + kbps - 1) / kbps != pb.splits) return fail(PUSH_E_SHAPE, "gemm: split count leaves an empty split");
-  CUtensorMap maps[4];
-  if ((st = make_operand_maps(pb.A, pb.M, pb.K, pb.batch, BM, &maps[0], &maps[1])) != PUSH_OK) return st;
-  if ((st = make_operand_maps(pb.B, pb.N, pb.K, pb.batch, BN, &maps[2], &maps[3])) != PUSH_OK) return st;
+  CUtensorMap maps[5];
+  std::memset(maps, 0, sizeof(maps));
+  if ((st = make_operand_map(pb.A.hi, pb.A, pb.M, pb.K, pb.batch, BM, &maps[0])) != PUSH_OK) return st;
+  if ((st = make_operand_map(pb.B.hi, pb.B, pb.N, pb.K, pb.batch, BN, &maps[1])) != PUSH_OK) return st;
+  if (!pb.B.split) {
+    if (!pb.B.lo) return fail(PUSH_E_INVALID, "gemm: pre-split B needs lo");
+    if ((st = make_operand_map(pb.B.lo, pb.B, pb.N, pb.K, pb.batch, BN, &maps[2])) != PUSH_OK) return st;
+  }
+  const int nout = pb.epi == EPI_STORE ? pb.splits * pb.batch : pb.batch;
+  if ((st = make_map(&maps[3], pb.out, pb.N, pb.M, nout, pb.ldo, pb.out_pstride, 32, CU_TENSOR_MAP_SWIZZLE_128B)) !=
+      PUSH_OK)
+    return st;
+  if (pb.epi == EPI_BWD &&
+      (st = make_map(&maps[4], pb.aprev, pb.N, pb.M, pb.batch, pb.ld_aprev, pb.aprev_pstride, 32,
+                     CU_TENSOR_MAP_SWIZZLE_128B)) != PUSH_OK)
+    return st;
   KParams kp;
-  kp.M = pb.M; kp.N = pb.N; kp.K = pb.K; kp.splits = pb.splits; kp.kb_per_split = kbps;
+  std::memset(&kp, 0, sizeof(kp));
+  kp.M = pb.M; kp.N = pb.N; kp.K = pb.K; kp.batch = pb.batch; kp.splits = pb.splits; kp.kb_per_split = kbps;
   kp.passes = pb.passes; kp.epi = pb.epi; kp.act = pb.act;
-  kp.out0 = pb.out0; kp.out1 = pb.out1; kp.ldo = pb.ldo; kp.out_pstride = pb.out_pstride;
-  kp.out_sstride = pb.out_sstride; kp.bias = pb.bias; kp.bias_pstride = pb.bias_pstride;
-  kp.aprev_hi = pb.aprev_hi; kp.aprev_lo = pb.aprev_lo; kp.ld_aprev = pb.ld_aprev;
-  kp.aprev_pstride = pb.aprev_pstride;
-  dim3 grid((pb.M + BM - 1) / BM, pb.N / BN, pb.batch * pb.splits);
-  if (BN == 128) return launch_bn<128>(pb.A.mn_major, pb.B.mn_major, maps, kp, grid, stream);
-  if (BN == 64) return launch_bn<64>(pb.A.mn_major, pb.B.mn_major, maps, kp, grid, stream);
-  return launch_bn<32>(pb.A.mn_major, pb.B.mn_major, maps, kp, grid, stream);
+  kp.mt = (pb.M + BM - 1) / BM;
+  kp.nt = pb.N / BN;
+  kp.ntiles = kp.mt * kp.nt * pb.splits * pb.batch;
+  kp.a_pz = pb.A.pstride == 0 ? 0 : 1;
+  kp.b_pz = pb.B.pstride == 0 ? 0 : 1;
+  kp.bias = pb.bias; kp.bias_pstride = pb.bias_pstride;
+  kp.bpart = pb.bpart; kp.bp_sstride = pb.bp_sstride; kp.bp_pstride = pb.bp_pstride;
+  kp.x = pb.x; kp.din = pb.xpart ? pb.din : 0; kp.xpart = pb.xpart;
+  kp.xp_sstride = pb.xp_sstride; kp.xp_pstride = pb.xp_pstride;
+  if (BN == 128) return launch_bn<128>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
+  if (BN == 64) return launch_bn<64>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
+  return launch_bn<32>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
 }
 
 int effective_splits(int K, int want) {

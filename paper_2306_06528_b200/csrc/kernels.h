@@ -10,37 +10,52 @@ namespace kern {
 constexpr int THIN_CHUNK = 256;  // batch rows per thin weight-gradient partial (fixed: P-invariant order)
 
 // ---------------------------------------------------------------- a0 helpers
-// hi = tf32_rn(x), lo = tf32_rn(x - hi) for x = src[p*src_pstride + t], t < count, p < batch.
+// Weights only: hi = tf32_rn(x), lo = x - hi for x = src[p*src_pstride + t], t < count, p < batch.
 void split_hilo(const float* src, int64_t src_pstride, float* hi, float* lo, int64_t dst_pstride, int64_t count,
                 int batch, cudaStream_t s);
 
 // ---------------------------------------------------------------- a1 / a2 thin forward
-// out[p][b][o] = sigma( sum_i in(p,b,i) W_p[o][i] + bias_p[o] ), stored as tf32 (hi, lo).
-//   in(p,b,i) = in_hi[p*in_pstride + b*in + i] (+ in_lo[...] when in_lo != nullptr)
+// out[p][b][o] = sigma( sum_i in[p*in_pstride + b*in + i] W_p[o][i] + bias_p[o] )   (plain fp32)
 //   W_p = theta + p*ld_theta + off_w  ([out][in] row-major), bias_p = theta + p*ld_theta + off_b
-void thin_forward(const float* in_hi, const float* in_lo, int64_t in_pstride, const float* theta, int64_t ld_theta,
-                  int64_t off_w, int64_t off_b, int in, int out, int act, float* out_hi, float* out_lo,
-                  int64_t out_pstride, int B, int batch, cudaStream_t s);
+void thin_forward(const float* in, int64_t in_pstride, const float* theta, int64_t ld_theta, int64_t off_w,
+                  int64_t off_b, int in_, int out, int act, float* dst, int64_t out_pstride, int B, int batch,
+                  cudaStream_t s);
 
-// ---------------------------------------------------------------- a3 output layer + loss
-// yhat = a W^T + b (identity), e = yhat - y, err2[p][b] = sum_o e^2, delta_L = 2 e / (B d_out) as (hi, lo).
-void output_layer(const float* in_hi, const float* in_lo, int64_t in_pstride, const float* theta, int64_t ld_theta,
-                  int64_t off_w, int64_t off_b, int in, int out, const float* y, float* err2, int64_t err_pstride,
-                  float* d_hi, float* d_lo, int64_t d_pstride, int B, int batch, cudaStream_t s);
+// ---------------------------------------------------------------- a3 fused output layer (+ top of a4/a5)
+constexpr int kMaxDout = 8;  // output width handled by output_fused
+struct OutputArgs {
+  const float* A;            // input of the output layer [p][B][H] (a_pstride; 0 = shared x)
+  int64_t a_pstride;
+  int H, dout, B, act;       // act: hidden activation (for sigma' of A when dprev != nullptr)
+  const float* theta;        // W_L at theta + p*ld + off_w ([dout][H]), b_L at off_b
+  int64_t ld, off_w, off_b;
+  const float* y;            // [B][dout]
+  float* err2;               // [p][B] sum_o e^2 (err_pstride)
+  int64_t err_pstride;
+  float* wpart;              // (rb, p, o, i) at rb*wo_sstride + p*wo_pstride + o*H + i
+  int64_t wo_sstride, wo_pstride;
+  float* bpart_out;          // (rb, p, o) at rb*bo_sstride + p*bo_pstride + o
+  int64_t bo_sstride, bo_pstride;
+  float* dprev;              // nullptr, or delta of the layer below [p][B][H] (dp_pstride)
+  int64_t dp_pstride;
+  float* bpart_prev;         // (rb, p, i) at rb*bp_sstride + p*bp_pstride + i
+  int64_t bp_sstride, bp_pstride;
+};
+void output_fused(const OutputArgs& a, int batch, cudaStream_t s);
 // loss[p] = sum_b err2[p][b] / (B d_out)   (fixed-order tree reduction)
 void loss_reduce(const float* err2, int64_t err_pstride, float* loss, int B, int d_out, int batch, cudaStream_t s);
 
-// ---------------------------------------------------------------- a4 thin backprop
-// dprev[p][b][i] = (sum_o delta[p][b][o] W_p[o][i]) * sigma'(aprev[p][b][i])  -> (hi, lo)
-void thin_backward(const float* d_hi, const float* d_lo, int64_t d_pstride, const float* theta, int64_t ld_theta,
-                   int64_t off_w, int in, int out, const float* a_hi, const float* a_lo, int64_t a_pstride, int act,
-                   float* o_hi, float* o_lo, int64_t o_pstride, int B, int batch, cudaStream_t s);
+// ---------------------------------------------------------------- a4 thin backprop (generic)
+// o[p][b][i] = (sum_k delta[p][b][k] W_p[k][i]) * sigma'(aprev[p][b][i])
+void thin_backward(const float* dl, int64_t d_pstride, const float* theta, int64_t ld_theta, int64_t off_w, int in,
+                   int out, const float* aprev, int64_t a_pstride, int act, float* o, int64_t o_pstride, int B,
+                   int batch, cudaStream_t s);
 
-// ---------------------------------------------------------------- a5 thin weight gradient partials
+// ---------------------------------------------------------------- a5 thin weight gradient partials (generic)
 // part[s][p][o][i'] = sum_{b in chunk s} delta[p][b][o] * A(p,b,i'),  i' < in_eff + 1, A(.,.,in_eff) = 1
 // (in_eff = 0 gives the bias-only column sums).  chunks of THIN_CHUNK rows; returns #chunks.
-int thin_wgrad(const float* d_hi, const float* d_lo, int64_t d_pstride, const float* a_hi, const float* a_lo,
-               int64_t a_pstride, int in_eff, int out, float* part, int B, int batch, cudaStream_t s);
+int thin_wgrad(const float* dl, int64_t d_pstride, const float* A, int64_t a_pstride, int in_eff, int out, float* part,
+               int B, int batch, cudaStream_t s);
 
 // ---------------------------------------------------------------- a5 finalize into G
 struct PartView {

@@ -1,10 +1,11 @@
 // kernels_mlp.cu — CUDA-core kernels of the per-particle gradient g_i (DESIGN.md a0-a5)
 // for the layers that are too thin for the tensor cores (d_in <= 3 input layer,
-// d_out = 1 output layer), the loss, the bias sums and the write of g into G.
+// d_out = 1 output layer), the loss, and the write of g into G.
 //
 // g_i = -lambda * grad MSE_i + grad log p0(theta_i)   (Eq. eq:grad)
-// All reductions run in a fixed order that depends only on (B, layer shape),
-// never on the number of ranks, so results are identical for every sharding.
+// Activations and deltas are plain fp32 arrays [particle][row][feature].  All
+// reductions run in a fixed order that depends only on (B, layer shape), never on
+// the number of ranks, so results are identical for every sharding.
 #include "common.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
@@ -12,21 +13,16 @@
 namespace push {
 namespace kern {
 
-__device__ __forceinline__ void store_hilo(float* hi, float* lo, int64_t idx, float v) {
-  const float h = ptx::tf32_rna(v);
-  hi[idx] = h;
-  lo[idx] = ptx::tf32_rna(v - h);
-}
-__device__ __forceinline__ float load_val(const float* hi, const float* lo, int64_t idx) {
-  return lo ? hi[idx] + lo[idx] : hi[idx];
-}
-
-// ---------------------------------------------------------------- split
+// ---------------------------------------------------------------- split (weights)
 __global__ void split_hilo_kernel(const float* __restrict__ src, int64_t src_pstride, float* __restrict__ hi,
                                   float* __restrict__ lo, int64_t dst_pstride, int64_t count) {
   const int p = blockIdx.y;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x)
-    store_hilo(hi + p * dst_pstride, lo + p * dst_pstride, t, src[p * src_pstride + t]);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+    const float v = src[p * src_pstride + t];
+    const float h = ptx::tf32_rna(v);
+    hi[p * dst_pstride + t] = h;
+    lo[p * dst_pstride + t] = v - h;
+  }
 }
 void split_hilo(const float* src, int64_t src_pstride, float* hi, float* lo, int64_t dst_pstride, int64_t count,
                 int batch, cudaStream_t s) {
@@ -35,62 +31,153 @@ void split_hilo(const float* src, int64_t src_pstride, float* hi, float* lo, int
 }
 
 // ---------------------------------------------------------------- thin forward (narrow input)
-__global__ void thin_forward_kernel(const float* __restrict__ in_hi, const float* __restrict__ in_lo,
-                                    int64_t in_pstride, const float* __restrict__ theta, int64_t ld, int64_t off_w,
-                                    int64_t off_b, int nin, int nout, int act, float* __restrict__ out_hi,
-                                    float* __restrict__ out_lo, int64_t out_pstride, int B) {
+// One thread per 4 consecutive outputs of a row when nout % 4 == 0 (float4 store), else one per output.
+template <bool VEC>
+__global__ void thin_forward_kernel(const float* __restrict__ in, int64_t in_pstride, const float* __restrict__ theta,
+                                    int64_t ld, int64_t off_w, int64_t off_b, int nin, int nout, int act,
+                                    float* __restrict__ out, int64_t out_pstride, int B) {
   const int p = blockIdx.y;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int per = VEC ? 4 : 1;
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * per;
   if (t >= (int64_t)B * nout) return;
   const int b = (int)(t / nout), o = (int)(t % nout);
-  const float* W = theta + p * ld + off_w + (int64_t)o * nin;
-  const int64_t ib = p * in_pstride + (int64_t)b * nin;
-  float z = 0.f;
-  for (int i = 0; i < nin; ++i) z = fmaf(load_val(in_hi, in_lo, ib + i), W[i], z);
-  z += theta[p * ld + off_b + o];
-  store_hilo(out_hi, out_lo, p * out_pstride + t, act_fwd(z, act));
+  const float* W = theta + p * ld + off_w;
+  const float* bias = theta + p * ld + off_b;
+  const float* x = in + p * in_pstride + (int64_t)b * nin;
+  float z[4];
+#pragma unroll
+  for (int u = 0; u < per; ++u) z[u] = 0.f;
+  for (int i = 0; i < nin; ++i) {
+    const float xi = __ldg(x + i);
+#pragma unroll
+    for (int u = 0; u < per; ++u) z[u] = fmaf(xi, __ldg(W + (int64_t)(o + u) * nin + i), z[u]);
+  }
+  float* dst = out + p * out_pstride + t;
+  if (VEC) {
+    float4 v;
+    v.x = act_fwd(z[0] + __ldg(bias + o), act);
+    v.y = act_fwd(z[1] + __ldg(bias + o + 1), act);
+    v.z = act_fwd(z[2] + __ldg(bias + o + 2), act);
+    v.w = act_fwd(z[3] + __ldg(bias + o + 3), act);
+    *reinterpret_cast<float4*>(dst) = v;
+  } else {
+    dst[0] = act_fwd(z[0] + __ldg(bias + o), act);
+  }
 }
-void thin_forward(const float* in_hi, const float* in_lo, int64_t in_pstride, const float* theta, int64_t ld_theta,
-                  int64_t off_w, int64_t off_b, int in, int out, int act, float* out_hi, float* out_lo,
-                  int64_t out_pstride, int B, int batch, cudaStream_t s) {
-  const int64_t tot = (int64_t)B * out;
-  thin_forward_kernel<<<dim3((unsigned)((tot + 255) / 256), batch), 256, 0, s>>>(
-      in_hi, in_lo, in_pstride, theta, ld_theta, off_w, off_b, in, out, act, out_hi, out_lo, out_pstride, B);
+void thin_forward(const float* in, int64_t in_pstride, const float* theta, int64_t ld_theta, int64_t off_w,
+                  int64_t off_b, int in_, int out, int act, float* dst, int64_t out_pstride, int B, int batch,
+                  cudaStream_t s) {
+  const bool vec = out % 4 == 0 && out_pstride % 4 == 0;
+  const int64_t tot = (int64_t)B * out / (vec ? 4 : 1);
+  const dim3 grid((unsigned)((tot + 255) / 256), batch);
+  if (vec)
+    thin_forward_kernel<true><<<grid, 256, 0, s>>>(in, in_pstride, theta, ld_theta, off_w, off_b, in_, out, act, dst,
+                                                   out_pstride, B);
+  else
+    thin_forward_kernel<false><<<grid, 256, 0, s>>>(in, in_pstride, theta, ld_theta, off_w, off_b, in_, out, act, dst,
+                                                    out_pstride, B);
 }
 
-// ---------------------------------------------------------------- output layer + loss terms
-// one warp per (particle, batch row); lanes split the input features; fixed xor-tree reduction.
-__global__ void output_layer_kernel(const float* __restrict__ in_hi, const float* __restrict__ in_lo,
-                                    int64_t in_pstride, const float* __restrict__ theta, int64_t ld, int64_t off_w,
-                                    int64_t off_b, int nin, int nout, const float* __restrict__ y,
-                                    float* __restrict__ err2, int64_t err_pstride, float* __restrict__ d_hi,
-                                    float* __restrict__ d_lo, int64_t d_pstride, int B) {
+// ---------------------------------------------------------------- fused output layer (a3 + a4/a5 of the top)
+// One warp per 32-row block rb of particle p:
+//   phase 1 (per row b): yhat_o = a_b . W_o + b_o (lanes split the features; fixed xor tree),
+//                        e = yhat - y, err2[b] = sum_o e^2, dL_o = 2 e_o / (B d_out)
+//   phase 2 (per feature i, lanes own features): over the block's rows in ascending order
+//        wpart[rb][p][o][i]   = sum_b dL_o(b) a_b[i]                  (dW of the output layer)
+//        dprev[b][i]          = (sum_o dL_o(b) W_o[i]) sigma'(a_b[i])  (delta of the layer below)
+//        bprev[rb][p][i]      = sum_b dprev[b][i]                     (its bias-gradient partial)
+//   and bpart[rb][p][o] = sum_b dL_o(b).
+constexpr int OUT_FPL = 4;  // features per lane per phase-2 pass
+__global__ void __launch_bounds__(256) output_fused_kernel(OutputArgs a) {
+  __shared__ float sdl[8][32][kMaxDout];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.y;
-  const int lane = threadIdx.x & 31;
-  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (b >= B) return;
-  const int64_t ib = p * in_pstride + (int64_t)b * nin;
-  const float scale = 2.0f / (float)((int64_t)B * nout);
-  float e2 = 0.f;
-  for (int o = 0; o < nout; ++o) {
-    const float* W = theta + p * ld + off_w + (int64_t)o * nin;
-    float part = 0.f;
-    for (int i = lane; i < nin; i += 32) part = fmaf(load_val(in_hi, in_lo, ib + i), W[i], part);
+  const int rb = blockIdx.x * 8 + warp;
+  const int RB = (a.B + 31) / 32;
+  if (rb >= RB) return;
+  const float* A = a.A + p * a.a_pstride;
+  const float* W = a.theta + p * a.ld + a.off_w;
+  const float* bias = a.theta + p * a.ld + a.off_b;
+  const float scale = 2.0f / (float)((int64_t)a.B * a.dout);
+  // phase 1
+  for (int r = 0; r < 32; ++r) {
+    const int b = rb * 32 + r;
+    float e2 = 0.f;
+    for (int o = 0; o < a.dout; ++o) {
+      float dl = 0.f;
+      if (b < a.B) {
+        const float* arow = A + (int64_t)b * a.H;
+        const float* wrow = W + (int64_t)o * a.H;
+        float part = 0.f;
+        for (int i = lane; i < a.H; i += 32) part = fmaf(__ldg(arow + i), __ldg(wrow + i), part);
 #pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) part += __shfl_xor_sync(0xffffffffu, part, m);
-    const float yhat = part + theta[p * ld + off_b + o];
-    const float e = yhat - y[(int64_t)b * nout + o];
-    e2 = fmaf(e, e, e2);
-    if (lane == 0) store_hilo(d_hi, d_lo, p * d_pstride + (int64_t)b * nout + o, scale * e);
+        for (int m = 16; m >= 1; m >>= 1) part += __shfl_xor_sync(0xffffffffu, part, m);
+        const float e = (part + __ldg(bias + o)) - __ldg(a.y + (int64_t)b * a.dout + o);
+        e2 = fmaf(e, e, e2);
+        dl = scale * e;
+      }
+      if (lane == 0) sdl[warp][r][o] = dl;
+    }
+    if (lane == 0 && b < a.B) a.err2[p * a.err_pstride + b] = e2;
   }
-  if (lane == 0) err2[p * err_pstride + b] = e2;
+  __syncwarp();
+  if (lane < a.dout) {
+    float sb = 0.f;
+    for (int r = 0; r < 32; ++r) sb += sdl[warp][r][lane];
+    a.bpart_out[(int64_t)rb * a.bo_sstride + p * a.bo_pstride + lane] = sb;
+  }
+  // phase 2
+  const int rows = min(32, a.B - rb * 32);
+  for (int f0 = 0; f0 < a.H; f0 += 32 * OUT_FPL) {
+    float w[OUT_FPL][kMaxDout], wacc[OUT_FPL][kMaxDout], bacc[OUT_FPL];
+#pragma unroll
+    for (int k = 0; k < OUT_FPL; ++k) {
+      const int i = f0 + k * 32 + lane;
+      bacc[k] = 0.f;
+#pragma unroll
+      for (int o = 0; o < kMaxDout; ++o) {
+        w[k][o] = (o < a.dout && i < a.H) ? __ldg(W + (int64_t)o * a.H + i) : 0.f;
+        wacc[k][o] = 0.f;
+      }
+    }
+    for (int r = 0; r < rows; ++r) {
+      const int b = rb * 32 + r;
+      float dl[kMaxDout];
+#pragma unroll
+      for (int o = 0; o < kMaxDout; ++o) dl[o] = o < a.dout ? sdl[warp][r][o] : 0.f;
+#pragma unroll
+      for (int k = 0; k < OUT_FPL; ++k) {
+        const int i = f0 + k * 32 + lane;
+        if (i < a.H) {
+          const float av = __ldg(A + (int64_t)b * a.H + i);
+          float d = 0.f;
+#pragma unroll
+          for (int o = 0; o < kMaxDout; ++o) {
+            wacc[k][o] = fmaf(dl[o], av, wacc[k][o]);
+            d = fmaf(dl[o], w[k][o], d);
+          }
+          if (a.dprev) {
+            d *= act_deriv_from_a(av, a.act);
+            a.dprev[p * a.dp_pstride + (int64_t)b * a.H + i] = d;
+            bacc[k] += d;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < OUT_FPL; ++k) {
+      const int i = f0 + k * 32 + lane;
+      if (i < a.H) {
+        for (int o = 0; o < a.dout; ++o)
+          a.wpart[(int64_t)rb * a.wo_sstride + p * a.wo_pstride + (int64_t)o * a.H + i] = wacc[k][o];
+        if (a.dprev) a.bpart_prev[(int64_t)rb * a.bp_sstride + p * a.bp_pstride + i] = bacc[k];
+      }
+    }
+  }
 }
-void output_layer(const float* in_hi, const float* in_lo, int64_t in_pstride, const float* theta, int64_t ld_theta,
-                  int64_t off_w, int64_t off_b, int in, int out, const float* y, float* err2, int64_t err_pstride,
-                  float* d_hi, float* d_lo, int64_t d_pstride, int B, int batch, cudaStream_t s) {
-  output_layer_kernel<<<dim3((B + 7) / 8, batch), 256, 0, s>>>(in_hi, in_lo, in_pstride, theta, ld_theta, off_w,
-                                                                off_b, in, out, y, err2, err_pstride, d_hi, d_lo,
-                                                                d_pstride, B);
+void output_fused(const OutputArgs& a, int batch, cudaStream_t s) {
+  const int RB = (a.B + 31) / 32;
+  output_fused_kernel<<<dim3((RB + 7) / 8, batch), 256, 0, s>>>(a);
 }
 
 __global__ void loss_reduce_kernel(const float* __restrict__ err2, int64_t err_pstride, float* __restrict__ loss,
@@ -111,36 +198,31 @@ void loss_reduce(const float* err2, int64_t err_pstride, float* loss, int B, int
   loss_reduce_kernel<<<batch, 256, 0, s>>>(err2, err_pstride, loss, B, (float)((int64_t)B * d_out));
 }
 
-// ---------------------------------------------------------------- thin backward
-__global__ void thin_backward_kernel(const float* __restrict__ d_hi, const float* __restrict__ d_lo,
-                                     int64_t d_pstride, const float* __restrict__ theta, int64_t ld, int64_t off_w,
-                                     int nin, int nout, const float* __restrict__ a_hi,
-                                     const float* __restrict__ a_lo, int64_t a_pstride, int act,
-                                     float* __restrict__ o_hi, float* __restrict__ o_lo, int64_t o_pstride, int B) {
+// ---------------------------------------------------------------- thin backward (generic)
+__global__ void thin_backward_kernel(const float* __restrict__ dl, int64_t d_pstride, const float* __restrict__ theta,
+                                     int64_t ld, int64_t off_w, int nin, int nout, const float* __restrict__ aprev,
+                                     int64_t a_pstride, int act, float* __restrict__ o, int64_t o_pstride, int B) {
   const int p = blockIdx.y;
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= (int64_t)B * nin) return;
   const int b = (int)(t / nin), i = (int)(t % nin);
   const float* W = theta + p * ld + off_w;
-  const int64_t db = p * d_pstride + (int64_t)b * nout;
+  const float* drow = dl + p * d_pstride + (int64_t)b * nout;
   float acc = 0.f;
-  for (int o = 0; o < nout; ++o) acc = fmaf(load_val(d_hi, d_lo, db + o), W[(int64_t)o * nin + i], acc);
-  const float a = load_val(a_hi, a_lo, p * a_pstride + t);
-  store_hilo(o_hi, o_lo, p * o_pstride + t, acc * act_deriv_from_a(a, act));
+  for (int k = 0; k < nout; ++k) acc = fmaf(__ldg(drow + k), __ldg(W + (int64_t)k * nin + i), acc);
+  o[p * o_pstride + t] = acc * act_deriv_from_a(aprev[p * a_pstride + t], act);
 }
-void thin_backward(const float* d_hi, const float* d_lo, int64_t d_pstride, const float* theta, int64_t ld_theta,
-                   int64_t off_w, int in, int out, const float* a_hi, const float* a_lo, int64_t a_pstride, int act,
-                   float* o_hi, float* o_lo, int64_t o_pstride, int B, int batch, cudaStream_t s) {
+void thin_backward(const float* dl, int64_t d_pstride, const float* theta, int64_t ld_theta, int64_t off_w, int in,
+                   int out, const float* aprev, int64_t a_pstride, int act, float* o, int64_t o_pstride, int B,
+                   int batch, cudaStream_t s) {
   const int64_t tot = (int64_t)B * in;
   thin_backward_kernel<<<dim3((unsigned)((tot + 255) / 256), batch), 256, 0, s>>>(
-      d_hi, d_lo, d_pstride, theta, ld_theta, off_w, in, out, a_hi, a_lo, a_pstride, act, o_hi, o_lo, o_pstride, B);
+      dl, d_pstride, theta, ld_theta, off_w, in, out, aprev, a_pstride, act, o, o_pstride, B);
 }
 
-// ---------------------------------------------------------------- thin weight-gradient partials
-__global__ void thin_wgrad_kernel(const float* __restrict__ d_hi, const float* __restrict__ d_lo,
-                                  int64_t d_pstride, const float* __restrict__ a_hi,
-                                  const float* __restrict__ a_lo, int64_t a_pstride, int nin, int nout,
-                                  float* __restrict__ part, int B) {
+// ---------------------------------------------------------------- thin weight-gradient partials (generic)
+__global__ void thin_wgrad_kernel(const float* __restrict__ dl, int64_t d_pstride, const float* __restrict__ A,
+                                  int64_t a_pstride, int nin, int nout, float* __restrict__ part, int B) {
   const int p = blockIdx.z, s = blockIdx.y, P = gridDim.z;
   const int cols = nin + 1;
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -150,22 +232,22 @@ __global__ void thin_wgrad_kernel(const float* __restrict__ d_hi, const float* _
   if (cols >= nout) { o = (int)(t / cols); i = (int)(t % cols); }     // input index fastest: coalesced A
   else { i = (int)(t / nout); o = (int)(t % nout); }                 // output index fastest: coalesced delta
   const int b0 = s * THIN_CHUNK, b1 = min(B, b0 + THIN_CHUNK);
-  const int64_t dbase = p * d_pstride + o, abase = p * a_pstride + i;
+  const float* dcol = dl + p * d_pstride + o;
   float acc = 0.f;
   if (i == nin) {
-    for (int b = b0; b < b1; ++b) acc += load_val(d_hi, d_lo, dbase + (int64_t)b * nout);
+    for (int b = b0; b < b1; ++b) acc += dcol[(int64_t)b * nout];
   } else {
-    for (int b = b0; b < b1; ++b)
-      acc = fmaf(load_val(d_hi, d_lo, dbase + (int64_t)b * nout), load_val(a_hi, a_lo, abase + (int64_t)b * nin), acc);
+    const float* acol = A + p * a_pstride + i;
+    for (int b = b0; b < b1; ++b) acc = fmaf(dcol[(int64_t)b * nout], acol[(int64_t)b * nin], acc);
   }
   part[((int64_t)s * P + p) * tot + (int64_t)o * cols + i] = acc;
 }
-int thin_wgrad(const float* d_hi, const float* d_lo, int64_t d_pstride, const float* a_hi, const float* a_lo,
-               int64_t a_pstride, int in_eff, int out, float* part, int B, int batch, cudaStream_t s) {
+int thin_wgrad(const float* dl, int64_t d_pstride, const float* A, int64_t a_pstride, int in_eff, int out, float* part,
+               int B, int batch, cudaStream_t s) {
   const int chunks = (B + THIN_CHUNK - 1) / THIN_CHUNK;
   const int64_t tot = (int64_t)out * (in_eff + 1);
-  thin_wgrad_kernel<<<dim3((unsigned)((tot + 255) / 256), chunks, batch), 256, 0, s>>>(
-      d_hi, d_lo, d_pstride, a_hi, a_lo, a_pstride, in_eff, out, part, B);
+  thin_wgrad_kernel<<<dim3((unsigned)((tot + 255) / 256), chunks, batch), 256, 0, s>>>(dl, d_pstride, A, a_pstride,
+                                                                                       in_eff, out, part, B);
   return chunks;
 }
 

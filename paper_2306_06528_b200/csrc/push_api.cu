@@ -44,20 +44,22 @@ struct LayerPlan {
   int64_t woff = 0;              // offset of this layer's hi/lo weight copy (per-particle block)
 };
 
+constexpr int kMaxX0 = 4;  // thin first layer whose weight grads are fused into layer 1's BWD epilogue
+
 struct Plan {
-  int n = 0, world = 1, nl = 0, L = 0, Bmax = 0, Hmax = 0;
+  int n = 0, world = 1, nl = 0, L = 0, Bmax = 0, Hmax = 0, RB = 0;
   int64_t d = 0, ld = 0;
   std::vector<LayerPlan> layers;
   int64_t wsplit_total = 0;                 // per particle elements of the hi/lo weight copies
   std::vector<int64_t> act_pst;             // per layer 0..L-2 activation particle stride
-  int64_t x_pst = 0;                        // replicated X split particle stride (layer 0 gemm)
   int64_t dlt_pst = 0;                      // delta buffer particle stride
   int64_t wpart_elems = 0, tpart_elems = 0;
+  bool fuse_x0 = false;                     // layer 0 thin + layer 1 GEMM: dW_0 from layer 1's BWD epilogue
   kern::DistPlan dist{};
   // byte offsets into the workspace
-  size_t o_theta0, o_theta1, o_grad, o_whi, o_wlo, o_xhi, o_xlo, o_dhi0, o_dlo0, o_dhi1, o_dlo1, o_err2, o_loss,
-      o_loss_all, o_wpart, o_tpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf;
-  std::vector<size_t> o_ahi, o_alo;
+  size_t o_theta0, o_theta1, o_grad, o_whi, o_wlo, o_dlt0, o_dlt1, o_err2, o_loss, o_loss_all, o_wpart, o_tpart,
+      o_bpart0, o_bpart1, o_opw, o_opb, o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf;
+  std::vector<size_t> o_act;
   size_t total = 0;
 };
 
@@ -72,6 +74,8 @@ static push_status validate(const push_config* c, int world) {
   if (c->n_layers < 1 || c->n_layers > PUSH_MAX_LAYERS) return fail(PUSH_E_SHAPE, "n_layers must be in [1, 15]");
   for (int l = 0; l <= c->n_layers; ++l)
     if (c->dims[l] < 1) return fail(PUSH_E_SHAPE, "dims must be >= 1");
+  if (c->dims[c->n_layers] > kern::kMaxDout)
+    return fail(PUSH_E_SHAPE, "output width d_out must be <= " + std::to_string(kern::kMaxDout));
   if (c->activation < PUSH_ACT_TANH || c->activation > PUSH_ACT_IDENTITY)
     return fail(PUSH_E_INVALID, "bad activation");
   if (c->prior != PUSH_PRIOR_UNIFORM && c->prior != PUSH_PRIOR_GAUSSIAN) return fail(PUSH_E_INVALID, "bad prior");
@@ -95,9 +99,10 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.nl = P.n / world;
   P.L = c->n_layers;
   P.Bmax = c->max_batch;
+  P.RB = (P.Bmax + gemm::kRowBlock - 1) / gemm::kRowBlock;
   P.layers.resize(P.L);
   int64_t off = 0;
-  P.Hmax = 0;
+  P.Hmax = 1;
   for (int l = 0; l < P.L; ++l) {
     LayerPlan& lp = P.layers[l];
     lp.in = c->dims[l];
@@ -107,25 +112,26 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
     lp.off_b = off;
     off += lp.out;
     lp.gemm = (l < P.L - 1) && (lp.in % 32 == 0) && (lp.out % 32 == 0);
-    P.Hmax = std::max(P.Hmax, lp.out);
+    if (l < P.L - 1) P.Hmax = std::max(P.Hmax, lp.out);
   }
   P.d = off;
   P.ld = round_up(P.d, 32);
+  P.fuse_x0 = P.L >= 3 && !P.layers[0].gemm && P.layers[1].gemm && P.layers[0].in <= kMaxX0;
   P.wsplit_total = 0;
   int64_t max_w = 0, max_t = 0;
-  for (auto& lp : P.layers) {
+  for (int l = 0; l < P.L; ++l) {
+    LayerPlan& lp = P.layers[l];
     if (lp.gemm) {
       lp.woff = P.wsplit_total;
       P.wsplit_total += round_up((int64_t)lp.in * lp.out, 32);
       max_w = std::max<int64_t>(max_w, (int64_t)lp.in * lp.out);
-      max_t = std::max<int64_t>(max_t, lp.out);
-    } else {
+      max_t = std::max<int64_t>(max_t, lp.out);  // bias-only column sums
+    } else if (l < P.L - 1) {
       max_t = std::max<int64_t>(max_t, (int64_t)lp.out * (lp.in + 1));
     }
   }
   P.act_pst.assign(std::max(P.L - 1, 0), 0);
   for (int l = 0; l + 1 < P.L; ++l) P.act_pst[l] = round_up((int64_t)P.Bmax * P.layers[l].out, 32);
-  P.x_pst = P.layers[0].gemm ? round_up((int64_t)P.Bmax * P.layers[0].in, 32) : 0;
   P.dlt_pst = round_up((int64_t)P.Bmax * P.Hmax, 32);
   const int chunks_max = (P.Bmax + kern::THIN_CHUNK - 1) / kern::THIN_CHUNK;
   P.wpart_elems = 8 * (int64_t)P.nl * max_w;
@@ -139,35 +145,33 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
     return o;
   };
   const int64_t nld = (int64_t)P.n * P.ld;
+  const LayerPlan& top = P.layers[P.L - 1];
   P.o_theta0 = take(nld);
   P.o_theta1 = take(nld);
   P.o_grad = take(nld);
   P.o_whi = take(P.nl * P.wsplit_total);
   P.o_wlo = take(P.nl * P.wsplit_total);
-  P.o_xhi = take(P.nl * P.x_pst);
-  P.o_xlo = take(P.nl * P.x_pst);
-  P.o_ahi.resize(P.act_pst.size());
-  P.o_alo.resize(P.act_pst.size());
-  for (size_t l = 0; l < P.act_pst.size(); ++l) {
-    P.o_ahi[l] = take(P.nl * P.act_pst[l]);
-    P.o_alo[l] = take(P.nl * P.act_pst[l]);
-  }
-  P.o_dhi0 = take(P.nl * P.dlt_pst);
-  P.o_dlo0 = take(P.nl * P.dlt_pst);
-  P.o_dhi1 = take(P.nl * P.dlt_pst);
-  P.o_dlo1 = take(P.nl * P.dlt_pst);
+  P.o_act.resize(P.act_pst.size());
+  for (size_t l = 0; l < P.act_pst.size(); ++l) P.o_act[l] = take(P.nl * P.act_pst[l]);
+  P.o_dlt0 = take(P.nl * P.dlt_pst);
+  P.o_dlt1 = take(P.nl * P.dlt_pst);
   P.o_err2 = take((int64_t)P.nl * P.Bmax);
   P.o_loss = take(P.nl);
   P.o_loss_all = take(P.n);
   P.o_wpart = take(P.wpart_elems);
   P.o_tpart = take(P.tpart_elems);
+  P.o_bpart0 = take((int64_t)P.RB * P.nl * P.Hmax);
+  P.o_bpart1 = take((int64_t)P.RB * P.nl * P.Hmax);
+  P.o_opw = take((int64_t)P.RB * P.nl * top.out * top.in);
+  P.o_opb = take((int64_t)P.RB * P.nl * top.out);
+  P.o_xpart = take(P.fuse_x0 ? (int64_t)P.RB * P.nl * P.layers[0].out * P.layers[0].in : 1);
   P.o_dpart = take((int64_t)P.dist.splits * P.n * P.n);
   P.o_D = take((int64_t)P.n * P.n);
   P.o_K = take((int64_t)P.nl * P.n);
   P.o_s = take(P.nl);
   P.o_h = take(32);
   P.o_xbuf = take((int64_t)P.Bmax * P.layers[0].in);
-  P.o_ybuf = take((int64_t)P.Bmax * P.layers[P.L - 1].out);
+  P.o_ybuf = take((int64_t)P.Bmax * top.out);
   P.total = cur;
   return PUSH_OK;
 }
@@ -204,10 +208,11 @@ struct push_ctx {
   float* theta[2] = {nullptr, nullptr};
   int cur = 0;
   float* grad = nullptr;
-  float *whi = nullptr, *wlo = nullptr, *xhi = nullptr, *xlo = nullptr;
-  std::vector<float*> ahi, alo;
-  float *dhi[2] = {nullptr, nullptr}, *dlo[2] = {nullptr, nullptr};
+  float *whi = nullptr, *wlo = nullptr;
+  std::vector<float*> act;             // activations A_0 .. A_{L-2}
+  float* dlt[2] = {nullptr, nullptr};  // delta ping-pong
   float *err2 = nullptr, *loss = nullptr, *loss_all = nullptr, *wpart = nullptr, *tpart = nullptr;
+  float *bpart[2] = {nullptr, nullptr}, *opw = nullptr, *opb = nullptr, *xpart = nullptr;
   float *dpart = nullptr, *D = nullptr, *K = nullptr, *srow = nullptr, *h = nullptr;
   float *xbuf = nullptr, *ybuf = nullptr;
   int state = 0;  // 0 READY, 1 GRADS_READY
@@ -310,32 +315,39 @@ static push_status exchange(push_ctx* c, int kind, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ grads (a0-a5)
-struct View {
-  const float* hi;
-  const float* lo;
-  int64_t pst;
+struct ActView {
+  const float* p;
+  int64_t pst;  // particle stride (0: shared x)
 };
 
-static View input_view(push_ctx* c, int l, const float* x) {
-  if (l == 0) {
-    if (c->P.layers[0].gemm) return View{c->xhi, c->xlo, c->P.x_pst};
-    return View{x, nullptr, 0};
-  }
-  return View{c->ahi[l - 1], c->alo[l - 1], c->P.act_pst[l - 1]};
+// Input of layer l: x for l == 0, else the activation A_{l-1}.
+static ActView layer_input(push_ctx* c, int l, const float* x) {
+  if (l == 0) return ActView{x, 0};
+  return ActView{c->act[l - 1], c->P.act_pst[l - 1]};
 }
 
 static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, cudaStream_t s) {
   const Plan& P = c->P;
   const int nl = P.nl, L = P.L, act = c->cfg.activation;
   const int64_t ld = P.ld;
+  const int RB = (B + gemm::kRowBlock - 1) / gemm::kRowBlock;
   float* th = c->theta[c->cur] + (int64_t)c->row0 * ld;  // own rows
   float* g = c->grad + (int64_t)c->row0 * ld;
+  const float lambda = c->cfg.lik_scale;
+  const float inv_s2 = c->cfg.prior == PUSH_PRIOR_GAUSSIAN ? 1.0f / (c->cfg.prior_sigma * c->cfg.prior_sigma) : 0.f;
   push_status st;
+  auto finalize = [&](int l, const kern::PartView& W, const kern::PartView& Bv) {
+    const LayerPlan& lp = P.layers[l];
+    return run_k(c, PC_FINALIZE, 1, 0, 0, s, [&] {
+      kern::finalize_layer(W, Bv, th, g, ld, lp.off_w, lp.in, lp.out, lambda, c->cfg.prior, inv_s2, nl, s);
+      return PUSH_OK;
+    });
+  };
 
   // C1: Theta rows of every rank (needed by a7/a10; unchanged during the gradient phase)
   if ((st = exchange(c, BUF_THETA, s)) != PUSH_OK) return st;
 
-  // a0: tf32 hi/lo copies of the tensor-core weights (and of X if layer 1 is a GEMM layer)
+  // a0: tf32 hi/lo copies of the tensor-core weights (activations are split inside the GEMM)
   for (int l = 0; l < L; ++l) {
     const LayerPlan& lp = P.layers[l];
     if (!lp.gemm) continue;
@@ -346,46 +358,52 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
     });
     if (st != PUSH_OK) return st;
   }
-  if (P.layers[0].gemm) {
-    const int64_t cnt = (int64_t)B * P.layers[0].in;
-    st = run_k(c, PC_SPLIT, 1, 12.0 * cnt * nl, 0, s, [&] {
-      kern::split_hilo(x, 0, c->xhi, c->xlo, P.x_pst, cnt, nl, s);
-      return PUSH_OK;
-    });
-    if (st != PUSH_OK) return st;
-  }
 
   // a1/a2: hidden layers forward
   for (int l = 0; l + 1 < L; ++l) {
     const LayerPlan& lp = P.layers[l];
-    const View in = input_view(c, l, x);
+    const ActView in = layer_input(c, l, x);
+    const double fl = 2.0 * B * lp.out * (double)lp.in * nl;
     if (lp.gemm) {
       gemm::Problem pb;
       pb.M = B; pb.N = lp.out; pb.K = lp.in; pb.batch = nl; pb.splits = 1; pb.passes = 3;
-      pb.A = gemm::Operand{in.hi, in.lo, false, lp.in, in.pst};
-      pb.B = gemm::Operand{c->whi + lp.woff, c->wlo + lp.woff, false, lp.in, P.wsplit_total};
+      pb.A = gemm::Operand{in.p, nullptr, true, false, lp.in, in.pst};
+      pb.B = gemm::Operand{c->whi + lp.woff, c->wlo + lp.woff, false, false, lp.in, P.wsplit_total};
       pb.epi = gemm::EPI_FWD; pb.act = act;
-      pb.out0 = c->ahi[l]; pb.out1 = c->alo[l]; pb.ldo = lp.out; pb.out_pstride = P.act_pst[l];
+      pb.out = c->act[l]; pb.ldo = lp.out; pb.out_pstride = P.act_pst[l];
       pb.bias = th + lp.off_b; pb.bias_pstride = ld;
-      const double fl = 2.0 * B * lp.out * (double)lp.in * nl;
       st = run_k(c, PC_FWD_GEMM, 1, 0, fl, s, [&] { return gemm::run(pb, s); });
     } else {
-      st = run_k(c, PC_FWD_THIN, 1, 0, 2.0 * B * lp.out * (double)lp.in * nl, s, [&] {
-        kern::thin_forward(in.hi, in.lo, in.pst, th, ld, lp.off_w, lp.off_b, lp.in, lp.out, act, c->ahi[l],
-                           c->alo[l], P.act_pst[l], B, nl, s);
+      st = run_k(c, PC_FWD_THIN, 1, 4.0 * B * lp.out * nl, fl, s, [&] {
+        kern::thin_forward(in.p, in.pst, th, ld, lp.off_w, lp.off_b, lp.in, lp.out, act, c->act[l], P.act_pst[l], B,
+                           nl, s);
         return PUSH_OK;
       });
     }
     if (st != PUSH_OK) return st;
   }
 
-  // a3: output layer, residuals, delta_L, per-particle loss
+  // a3 (+ the top of a4/a5): output layer, residuals, per-particle loss, dW_L / db_L partials,
+  // delta of the layer below and its bias partials, in one pass over A_{L-2}
+  std::vector<char> bias_ready(L, 0);  // bias partials of layer l sit in bpart[l & 1]
+  bool x0_ready = false;               // dW_0 partials sit in xpart
   {
     const LayerPlan& lp = P.layers[L - 1];
-    const View in = input_view(c, L - 1, x);
-    st = run_k(c, PC_OUTPUT, 1, 0, 2.0 * B * lp.out * (double)lp.in * nl, s, [&] {
-      kern::output_layer(in.hi, in.lo, in.pst, th, ld, lp.off_w, lp.off_b, lp.in, lp.out, y, c->err2, P.Bmax,
-                         c->dhi[0], c->dlo[0], P.dlt_pst, B, nl, s);
+    const ActView in = layer_input(c, L - 1, x);
+    kern::OutputArgs oa{};
+    oa.A = in.p; oa.a_pstride = in.pst; oa.H = lp.in; oa.dout = lp.out; oa.B = B; oa.act = act;
+    oa.theta = th; oa.ld = ld; oa.off_w = lp.off_w; oa.off_b = lp.off_b; oa.y = y;
+    oa.err2 = c->err2; oa.err_pstride = P.Bmax;
+    oa.wpart = c->opw; oa.wo_sstride = (int64_t)nl * lp.out * lp.in; oa.wo_pstride = (int64_t)lp.out * lp.in;
+    oa.bpart_out = c->opb; oa.bo_sstride = (int64_t)nl * lp.out; oa.bo_pstride = lp.out;
+    if (L >= 2) {
+      oa.dprev = c->dlt[0]; oa.dp_pstride = P.dlt_pst;
+      oa.bpart_prev = c->bpart[(L - 2) & 1]; oa.bp_sstride = (int64_t)nl * lp.in; oa.bp_pstride = lp.in;
+      bias_ready[L - 2] = 1;
+    }
+    const double bytes = 4.0 * B * lp.in * nl * (L >= 2 ? 2 : 1);
+    st = run_k(c, PC_OUTPUT, 1, bytes, 2.0 * B * lp.out * (double)lp.in * nl * 3, s, [&] {
+      kern::output_fused(oa, nl, s);
       return PUSH_OK;
     });
     if (st != PUSH_OK) return st;
@@ -394,78 +412,86 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
       return PUSH_OK;
     });
     if (st != PUSH_OK) return st;
+    kern::PartView W{c->opw, RB, oa.wo_sstride, oa.wo_pstride, lp.in};
+    kern::PartView Bv{c->opb, RB, oa.bo_sstride, oa.bo_pstride, 1};
+    if ((st = finalize(L - 1, W, Bv)) != PUSH_OK) return st;
   }
 
-  // a4/a5: backprop and weight gradients, layer by layer
+  // a4/a5: backprop and weight gradients, layer by layer (delta_l in dlt[xb])
   int xb = 0;
-  const float lambda = c->cfg.lik_scale;
-  const float inv_s2 = c->cfg.prior == PUSH_PRIOR_GAUSSIAN ? 1.0f / (c->cfg.prior_sigma * c->cfg.prior_sigma) : 0.f;
-  for (int l = L - 1; l >= 0; --l) {
+  for (int l = L - 2; l >= 0; --l) {
     const LayerPlan& lp = P.layers[l];
-    const float* dh = c->dhi[xb];
-    const float* dl = c->dlo[xb];
-    const View ap = input_view(c, l, x);
+    const float* dl = c->dlt[xb];
+    const ActView ap = layer_input(c, l, x);
     if (lp.gemm) {
       const int S = wgrad_splits(B);
       gemm::Problem pb;
       pb.M = lp.out; pb.N = lp.in; pb.K = B; pb.batch = nl; pb.splits = S; pb.passes = 3;
-      pb.A = gemm::Operand{dh, dl, true, lp.out, P.dlt_pst};
-      pb.B = gemm::Operand{ap.hi, ap.lo, true, lp.in, ap.pst};
+      pb.A = gemm::Operand{dl, nullptr, true, true, lp.out, P.dlt_pst};
+      pb.B = gemm::Operand{ap.p, nullptr, true, true, lp.in, ap.pst};
       pb.epi = gemm::EPI_STORE;
-      pb.out0 = c->wpart; pb.ldo = lp.in; pb.out_pstride = (int64_t)lp.out * lp.in;
+      pb.out = c->wpart; pb.ldo = lp.in; pb.out_pstride = (int64_t)lp.out * lp.in;
       pb.out_sstride = (int64_t)nl * lp.out * lp.in;
       const double fl = 2.0 * B * lp.out * (double)lp.in * nl;
       st = run_k(c, PC_WGRAD_GEMM, 1, 0, fl, s, [&] { return gemm::run(pb, s); });
       if (st != PUSH_OK) return st;
-      int chunks = 0;
-      st = run_k(c, PC_WGRAD_THIN, 1, 0, 0, s, [&] {
-        chunks = kern::thin_wgrad(dh, dl, P.dlt_pst, nullptr, nullptr, 0, 0, lp.out, c->tpart, B, nl, s);
-        return PUSH_OK;
-      });
-      if (st != PUSH_OK) return st;
       kern::PartView W{c->wpart, S, (int64_t)nl * lp.out * lp.in, (int64_t)lp.out * lp.in, lp.in};
-      kern::PartView Bv{c->tpart, chunks, (int64_t)nl * lp.out, lp.out, 1};
-      st = run_k(c, PC_FINALIZE, 1, 0, 0, s, [&] {
-        kern::finalize_layer(W, Bv, th, g, ld, lp.off_w, lp.in, lp.out, lambda, c->cfg.prior, inv_s2, nl, s);
-        return PUSH_OK;
-      });
+      kern::PartView Bv{c->bpart[l & 1], RB, (int64_t)nl * lp.out, lp.out, 1};
+      if (!bias_ready[l]) {  // delta_l came from a generic thin backward: column sums here
+        int chunks = 0;
+        st = run_k(c, PC_WGRAD_THIN, 1, 4.0 * B * lp.out * nl, 0, s, [&] {
+          chunks = kern::thin_wgrad(dl, P.dlt_pst, nullptr, 0, 0, lp.out, c->tpart, B, nl, s);
+          return PUSH_OK;
+        });
+        if (st != PUSH_OK) return st;
+        Bv = kern::PartView{c->tpart, chunks, (int64_t)nl * lp.out, lp.out, 1};
+      }
+      if ((st = finalize(l, W, Bv)) != PUSH_OK) return st;
+    } else if (l == 0 && x0_ready) {
+      kern::PartView W{c->xpart, RB, (int64_t)nl * lp.out * lp.in, (int64_t)lp.out * lp.in, lp.in};
+      kern::PartView Bv{c->bpart[0], RB, (int64_t)nl * lp.out, lp.out, 1};
+      if ((st = finalize(l, W, Bv)) != PUSH_OK) return st;
     } else {
       int chunks = 0;
-      st = run_k(c, PC_WGRAD_THIN, 1, 0, 2.0 * B * lp.out * (double)(lp.in + 1) * nl, s, [&] {
-        chunks = kern::thin_wgrad(dh, dl, P.dlt_pst, ap.hi, ap.lo, ap.pst, lp.in, lp.out, c->tpart, B, nl, s);
-        return PUSH_OK;
-      });
+      st = run_k(c, PC_WGRAD_THIN, 1, 4.0 * B * (lp.in + lp.out) * nl, 2.0 * B * lp.out * (double)(lp.in + 1) * nl,
+                 s, [&] {
+                   chunks = kern::thin_wgrad(dl, P.dlt_pst, ap.p, ap.pst, lp.in, lp.out, c->tpart, B, nl, s);
+                   return PUSH_OK;
+                 });
       if (st != PUSH_OK) return st;
       const int64_t cols = lp.in + 1;
       kern::PartView W{c->tpart, chunks, (int64_t)nl * lp.out * cols, (int64_t)lp.out * cols, cols};
       kern::PartView Bv{c->tpart + lp.in, chunks, (int64_t)nl * lp.out * cols, (int64_t)lp.out * cols, cols};
-      st = run_k(c, PC_FINALIZE, 1, 0, 0, s, [&] {
-        kern::finalize_layer(W, Bv, th, g, ld, lp.off_w, lp.in, lp.out, lambda, c->cfg.prior, inv_s2, nl, s);
-        return PUSH_OK;
-      });
+      if ((st = finalize(l, W, Bv)) != PUSH_OK) return st;
     }
-    if (st != PUSH_OK) return st;
     if (l == 0) break;
     // delta_{l-1} = (delta_l W_l) * sigma'(a_{l-1})
-    const View aprev = input_view(c, l, x);
-    float* oh = c->dhi[xb ^ 1];
-    float* ol = c->dlo[xb ^ 1];
+    const ActView aprev = layer_input(c, l, x);  // = A_{l-1}
+    float* o = c->dlt[xb ^ 1];
+    const double fl = 2.0 * B * lp.out * (double)lp.in * nl;
     if (lp.gemm) {
       gemm::Problem pb;
       pb.M = B; pb.N = lp.in; pb.K = lp.out; pb.batch = nl; pb.splits = 1; pb.passes = 3;
-      pb.A = gemm::Operand{dh, dl, false, lp.out, P.dlt_pst};
-      pb.B = gemm::Operand{c->whi + lp.woff, c->wlo + lp.woff, true, lp.in, P.wsplit_total};
+      pb.A = gemm::Operand{dl, nullptr, true, false, lp.out, P.dlt_pst};
+      pb.B = gemm::Operand{c->whi + lp.woff, c->wlo + lp.woff, false, true, lp.in, P.wsplit_total};
       pb.epi = gemm::EPI_BWD; pb.act = act;
-      pb.out0 = oh; pb.out1 = ol; pb.ldo = lp.in; pb.out_pstride = P.dlt_pst;
-      pb.aprev_hi = aprev.hi; pb.aprev_lo = aprev.lo; pb.ld_aprev = lp.in; pb.aprev_pstride = aprev.pst;
-      const double fl = 2.0 * B * lp.out * (double)lp.in * nl;
+      pb.out = o; pb.ldo = lp.in; pb.out_pstride = P.dlt_pst;
+      pb.aprev = aprev.p; pb.ld_aprev = lp.in; pb.aprev_pstride = aprev.pst;
+      pb.bpart = c->bpart[(l - 1) & 1]; pb.bp_sstride = (int64_t)nl * lp.in; pb.bp_pstride = lp.in;
+      if (l == 1 && P.fuse_x0) {
+        pb.x = x; pb.din = P.layers[0].in; pb.xpart = c->xpart;
+        pb.xp_sstride = (int64_t)nl * lp.in * P.layers[0].in; pb.xp_pstride = (int64_t)lp.in * P.layers[0].in;
+        x0_ready = true;
+      }
       st = run_k(c, PC_BWD_GEMM, 1, 0, fl, s, [&] { return gemm::run(pb, s); });
+      bias_ready[l - 1] = 1;
     } else {
-      st = run_k(c, PC_BWD_THIN, 1, 0, 2.0 * B * lp.out * (double)lp.in * nl, s, [&] {
-        kern::thin_backward(dh, dl, P.dlt_pst, th, ld, lp.off_w, lp.in, lp.out, aprev.hi, aprev.lo, aprev.pst, act,
-                            oh, ol, P.dlt_pst, B, nl, s);
+      st = run_k(c, PC_BWD_THIN, 1, 8.0 * B * lp.in * nl, fl, s, [&] {
+        kern::thin_backward(dl, P.dlt_pst, th, ld, lp.off_w, lp.in, lp.out, aprev.p, aprev.pst, act, o, P.dlt_pst, B,
+                            nl, s);
         return PUSH_OK;
       });
+      bias_ready[l - 1] = 0;
     }
     if (st != PUSH_OK) return st;
     xb ^= 1;
@@ -536,16 +562,14 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   c->grad = F(P.o_grad);
   c->whi = F(P.o_whi);
   c->wlo = F(P.o_wlo);
-  c->xhi = F(P.o_xhi);
-  c->xlo = F(P.o_xlo);
-  for (size_t l = 0; l < P.o_ahi.size(); ++l) {
-    c->ahi.push_back(F(P.o_ahi[l]));
-    c->alo.push_back(F(P.o_alo[l]));
-  }
-  c->dhi[0] = F(P.o_dhi0);
-  c->dlo[0] = F(P.o_dlo0);
-  c->dhi[1] = F(P.o_dhi1);
-  c->dlo[1] = F(P.o_dlo1);
+  for (size_t l = 0; l < P.o_act.size(); ++l) c->act.push_back(F(P.o_act[l]));
+  c->dlt[0] = F(P.o_dlt0);
+  c->dlt[1] = F(P.o_dlt1);
+  c->bpart[0] = F(P.o_bpart0);
+  c->bpart[1] = F(P.o_bpart1);
+  c->opw = F(P.o_opw);
+  c->opb = F(P.o_opb);
+  c->xpart = F(P.o_xpart);
   c->err2 = F(P.o_err2);
   c->loss = F(P.o_loss);
   c->loss_all = F(P.o_loss_all);
@@ -839,42 +863,47 @@ push_status push_destroy(push_ctx* c) {
 }
 
 // ------------------------------------------------------------------ debug: isolated GEMM
-static push_status dbg_gemm(int passes, int32_t a_mn, int32_t b_mn, int32_t M, int32_t N, int32_t K, int32_t batch,
-                            const float* A, const float* Bm, float* C, void* stream) {
+static push_status dbg_gemm(int passes, int32_t a_mn, int32_t b_mn, int32_t b_split, int32_t M, int32_t N, int32_t K,
+                            int32_t batch, const float* A, const float* Bm, float* C, void* stream) {
   if (M < 1 || N < 1 || K < 1 || batch < 1) return fail(PUSH_E_SHAPE, "empty GEMM");
   if (N % 32) return fail(PUSH_E_SHAPE, "N % 32 != 0");
   if (a_mn && M % 32) return fail(PUSH_E_SHAPE, "MN-major A needs M % 32 == 0");
   if ((!a_mn || !b_mn) && K % 4) return fail(PUSH_E_SHAPE, "K-major operands need K % 4 == 0");
+  if (a_mn && (int64_t)M * K % 4) return fail(PUSH_E_SHAPE, "batch stride must be a multiple of 4");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t na = (int64_t)M * K, nb = (int64_t)N * K;
-  const int64_t pa = (na + 31) / 32 * 32, pb_ = (nb + 31) / 32 * 32;
+  if (na % 4 || nb % 4) return fail(PUSH_E_SHAPE, "batch strides must be multiples of 4");
   float* buf = nullptr;
-  PUSH_CUDA_TRY(cudaMallocAsync(&buf, sizeof(float) * 2 * batch * (pa + pb_), s));
-  float* ahi = buf;
-  float* alo = ahi + batch * pa;
-  float* bhi = alo + batch * pa;
-  float* blo = bhi + batch * pb_;
-  // dense inputs are [batch][.][.] with per-batch stride na / nb: split into padded copies
-  kern::split_hilo(A, na, ahi, alo, pa, na, batch, s);
-  kern::split_hilo(Bm, nb, bhi, blo, pb_, nb, batch, s);
+  if (!b_split) {
+    PUSH_CUDA_TRY(cudaMallocAsync(&buf, sizeof(float) * 2 * batch * nb, s));
+    kern::split_hilo(Bm, nb, buf, buf + batch * nb, nb, nb, batch, s);
+  }
   gemm::Problem pb;
   pb.M = M; pb.N = N; pb.K = K; pb.batch = batch; pb.splits = 1; pb.passes = passes;
-  pb.A = gemm::Operand{ahi, alo, a_mn != 0, a_mn ? M : K, pa};
-  pb.B = gemm::Operand{bhi, blo, b_mn != 0, b_mn ? N : K, pb_};
+  pb.A = gemm::Operand{A, nullptr, true, a_mn != 0, a_mn ? M : K, na};
+  if (b_split)
+    pb.B = gemm::Operand{Bm, nullptr, true, b_mn != 0, b_mn ? N : K, nb};
+  else
+    pb.B = gemm::Operand{buf, buf + batch * nb, false, b_mn != 0, b_mn ? N : K, nb};
   pb.epi = gemm::EPI_STORE;
-  pb.out0 = C; pb.ldo = N; pb.out_pstride = (int64_t)M * N; pb.out_sstride = 0;
+  pb.out = C; pb.ldo = N; pb.out_pstride = (int64_t)M * N; pb.out_sstride = 0;
   push_status st = gemm::run(pb, s);
-  cudaFreeAsync(buf, s);
+  if (buf) cudaFreeAsync(buf, s);
   return st;
 }
 
 push_status pushdbg_gemm3xtf32(int32_t a_mn, int32_t b_mn, int32_t M, int32_t N, int32_t K, int32_t batch,
                                const float* A_dev, const float* B_dev, float* C_dev, void* stream) {
-  return dbg_gemm(3, a_mn, b_mn, M, N, K, batch, A_dev, B_dev, C_dev, stream);
+  return dbg_gemm(3, a_mn, b_mn, 0, M, N, K, batch, A_dev, B_dev, C_dev, stream);
 }
 push_status pushdbg_gemm1xtf32(int32_t a_mn, int32_t b_mn, int32_t M, int32_t N, int32_t K, int32_t batch,
                                const float* A_dev, const float* B_dev, float* C_dev, void* stream) {
-  return dbg_gemm(1, a_mn, b_mn, M, N, K, batch, A_dev, B_dev, C_dev, stream);
+  return dbg_gemm(1, a_mn, b_mn, 0, M, N, K, batch, A_dev, B_dev, C_dev, stream);
+}
+push_status pushdbg_gemm(int32_t passes, int32_t a_mn, int32_t b_mn, int32_t b_split, int32_t M, int32_t N, int32_t K,
+                         int32_t batch, const float* A_dev, const float* B_dev, float* C_dev, void* stream) {
+  if (passes != 1 && passes != 3) return fail(PUSH_E_INVALID, "passes must be 1 or 3");
+  return dbg_gemm(passes, a_mn, b_mn, b_split, M, N, K, batch, A_dev, B_dev, C_dev, stream);
 }
 
 }  // extern "C"

@@ -31,7 +31,7 @@ MAX_LAYERS = 15
 EXPORTS = ["push_version", "push_last_error", "push_get_unique_id", "push_workspace_size", "push_init",
            "push_init_local_group", "push_particle_grads", "push_set_grads", "push_svgd_step", "push_step_host",
            "push_gather", "push_profile_enable", "push_profile_read", "push_launch_count", "push_destroy",
-           "pushdbg_gemm3xtf32", "pushdbg_gemm1xtf32"]
+           "pushdbg_gemm3xtf32", "pushdbg_gemm1xtf32", "pushdbg_gemm"]
 
 
 class PushConfig(Structure):
@@ -82,6 +82,7 @@ def lib():
         "push_destroy": ([P], c_int32),
         "pushdbg_gemm3xtf32": ([c_int32] * 6 + [P, P, P, P], c_int32),
         "pushdbg_gemm1xtf32": ([c_int32] * 6 + [P, P, P, P], c_int32),
+        "pushdbg_gemm": ([c_int32] * 8 + [P, P, P, P], c_int32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -238,11 +239,12 @@ def local_group(cfg: PushConfig, world_size: int, theta0=None):
     return [Context(cfg, r, world_size, _handle=c_void_p(outs[r]), _ws=wss[r]) for r in range(world_size)]
 
 
-def gemm3xtf32(A, B, a_mn: bool, b_mn: bool, M: int, N: int, K: int, passes: int = 3, stream=None):
+def gemm3xtf32(A, B, a_mn: bool, b_mn: bool, M: int, N: int, K: int, passes: int = 3, b_split: bool = False,
+               stream=None):
     """Debug entry: C[p] = A[p] @ B[p] through the product's tcgen05 kernel (see include/push_debug.h)."""
     import torch
     batch = A.shape[0]
     C = torch.empty((batch, M, N), dtype=torch.float32, device=A.device)
-    f = lib().pushdbg_gemm3xtf32 if passes == 3 else lib().pushdbg_gemm1xtf32
-    check(f(int(a_mn), int(b_mn), M, N, K, batch, _ptr(A), _ptr(B), _ptr(C), _stream(stream)))
+    check(lib().pushdbg_gemm(passes, int(a_mn), int(b_mn), int(b_split), M, N, K, batch, _ptr(A), _ptr(B), _ptr(C),
+                             _stream(stream)))
     return C

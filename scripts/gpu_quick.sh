@@ -1,7 +1,13 @@
 #!/bin/bash
-# quick GPU check: gemm unit tests, parity tests, smoke, short bench
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
-timeout 300 python -m pytest tests/test_gpu_gemm.py -q 2>&1 | tail -25
-timeout 900 python -m pytest tests/test_gpu_parity.py -q 2>&1 | tail -30
-timeout 300 python __graft_entry__.py smoke 2>&1 | tail -5
-timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>&1 | tail -5
+# quick GPU check: gemm unit tests, parity tests, smoke, short bench (each under its own timeout)
+#   gpurun --timeout 1500 -- 'bash scripts/gpu_quick.sh tag'
+TAG=${1:-quick}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader > $OUT/gpu.txt
+python -c "from paper_2306_06528_b200 import build; build.build()" > $OUT/build.log 2>&1
+timeout 300 python -m pytest tests/test_gpu_gemm.py -x -q > $OUT/gemm.log 2>&1; echo "exit $?" >> $OUT/gemm.log
+timeout 600 python -m pytest tests/test_gpu_parity.py -q > $OUT/parity.log 2>&1; echo "exit $?" >> $OUT/parity.log
+timeout 300 python __graft_entry__.py smoke > $OUT/smoke.log 2>&1; echo "exit $?" >> $OUT/smoke.log
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > $OUT/bench.json 2> $OUT/bench.err
+tail -3 $OUT/gemm.log; tail -15 $OUT/parity.log; tail -2 $OUT/smoke.log; cat $OUT/bench.json | head -c 3000; tail -5 $OUT/bench.err

@@ -24,14 +24,16 @@ def _mk(batch, M, N, K, a_mn, b_mn, seed):
     return Ad, Bd, ref, scale
 
 
+@pytest.mark.parametrize("b_split", [0, 1])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 64, 96), (96, 32, 32), (300, 256, 128)])
-def test_gemm_3xtf32_matches_fp64(a_mn, b_mn, M, N, K):
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 64, 96), (96, 32, 32), (300, 256, 128), (1, 32, 4),
+                                   (640, 128, 1000)])
+def test_gemm_3xtf32_matches_fp64(a_mn, b_mn, b_split, M, N, K):
     if a_mn and M % 32:
         pytest.skip("MN-major A needs M % 32 == 0")
     batch = 3
     Ad, Bd, ref, scale = _mk(batch, M, N, K, a_mn, b_mn, 1 + M + N + K)
-    C = push.gemm3xtf32(Ad, Bd, bool(a_mn), bool(b_mn), M, N, K).double().cpu()
+    C = push.gemm3xtf32(Ad, Bd, bool(a_mn), bool(b_mn), M, N, K, b_split=bool(b_split)).double().cpu()
     err = ((C - ref).abs() / scale.clamp_min(1e-30)).max().item()
     assert err < 2e-6, err
 
@@ -40,8 +42,8 @@ def test_gemm_long_k_split_precision():
     # K = 4096: the weight-gradient shape (K = batch); 3xTF32 must beat 1xTF32 by >= 100x
     M, N, K = 128, 128, 4096
     Ad, Bd, ref, scale = _mk(2, M, N, K, 1, 1, 7)
-    C3 = push.gemm3xtf32(Ad, Bd, True, True, M, N, K, passes=3).double().cpu()
-    C1 = push.gemm3xtf32(Ad, Bd, True, True, M, N, K, passes=1).double().cpu()
+    C3 = push.gemm3xtf32(Ad, Bd, True, True, M, N, K, passes=3, b_split=True).double().cpu()
+    C1 = push.gemm3xtf32(Ad, Bd, True, True, M, N, K, passes=1, b_split=True).double().cpu()
     e3 = ((C3 - ref).abs().max() / ref.abs().max()).item()
     e1 = ((C1 - ref).abs().max() / ref.abs().max()).item()
     assert e3 < 1e-5, e3

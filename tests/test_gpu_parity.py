@@ -50,6 +50,9 @@ GRAD_CASES = [
     (2, [1, 33, 1], 64, "tanh", "uniform", 1.0, 1.0, "gauss"),            # width not % 32 -> thin path
     (2, [2, 128, 128, 1], 1, "tanh", "uniform", 1.0, 1.0, "gauss"),       # B = 1
     (2, [2, 256, 256, 256, 256, 1], 2048, "tanh", "uniform", 1.0, 1.0, "advection"),  # C2 net, split-K
+    (3, [2, 64, 64, 33, 1], 200, "tanh", "uniform", 1.0, 1.0, "gauss"),   # GEMM layer under a thin hidden layer
+    (2, [4, 64, 64, 2], 333, "tanh", "gaussian", 2.0, 1.0, "gauss"),      # d_out = 2, fused x0 with d_in = 4
+    (2, [3, 128, 1], 8192, "tanh", "uniform", 1.0, 1.0, "burgers"),       # L = 2: output layer right above thin
 ]
 
 
