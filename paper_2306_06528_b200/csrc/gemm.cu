@@ -10,16 +10,16 @@
 // accumulated in TMEM in fp32.  Activations and deltas live in HBM as ONE fp32 array; the hi/lo
 // split happens on the staged shared-memory tile (transform warps), so each byte is read once.
 //
-// Kernel shape (v3): persistent, one CTA per SM, tiles of 128 x BN, 12 warps:
+// Kernel shape (v3): persistent, one CTA per SM, tiles of 128 x BN, 14 warps:
 //   warp 0 lane 0   TMA producer (A fp32 tile; B as hi/lo pair or fp32 tile) into a STAGES ring
 //   warp 1 lane 0   MMA issuer (single thread, tcgen05.mma + tcgen05.commit); warp 1 owns TMEM
-//   warps 2-3       transform: hi = tf32_rn(x) in place, lo = x - hi into the stage's lo slot
-//   warps 4-11      epilogue: TMEM lane quarter q = warp % 4, column half h = (warp - 4) / 4.
+//   warps 2-5       transform: hi = tf32_rn(x) in place, lo = x - hi into the stage's lo slot
+//   warps 6-13      epilogue: TMEM lane quarter q = warp % 4, column half h = (warp - 6) / 4.
 //                   Every 128 of K the TMEM partial (NACC buffers of BN columns, rotating across
 //                   tiles, so the MMAs of the next tile overlap this epilogue) is added into fp32
 //                   registers with round-to-nearest — the tensor-core accumulator truncates on
 //                   each accumulate, so long chains would cost ~K/8 ulps.  The fused op is then
-//                   applied on a swizzled 32x32 smem box per warp and written with a TMA store.
+//                   applied on double-buffered swizzled 32x16 smem boxes per warp, written with TMA stores.
 #include <cudaTypedefs.h>
 
 #include <cstring>
@@ -35,10 +35,11 @@ namespace gemm {
 constexpr int BM = 128;
 constexpr int BK = 32;          // fp32 per k-block = 128 B = one SWIZZLE_128B row
 constexpr int kChunkKB = 4;     // k-blocks per TMEM accumulation chunk (128 of K) before fp32 promotion
-constexpr int kXfWarp0 = 2, kXfWarps = 2, kXfThreads = 32 * kXfWarps;
+constexpr int kXfWarp0 = 2, kXfWarps = 4, kXfThreads = 32 * kXfWarps;
 constexpr int kEpiWarp0 = kXfWarp0 + kXfWarps, kEpiWarps = 8;
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
-constexpr int kEpiBox = 32 * 32 * 4;  // one 32 x 32 fp32 SWIZZLE_128B box per epilogue warp
+constexpr int kHalfBox = 32 * 16 * 4;  // one 32 x 16 fp32 SWIZZLE_64B output box
+constexpr int kEpiBox = 2 * kHalfBox;  // double-buffered per epilogue warp
 constexpr int kMaxSmem = 232448;      // 227 KB opt-in dynamic shared memory per CTA
 
 template <int BN>
@@ -64,6 +65,7 @@ struct KParams {
   int M, N, K, batch, splits, kb_per_split, passes, epi, act;
   int mt, nt, ntiles;
   int a_pz, b_pz;  // 1: operand batched over particles; 0: shared (particle coordinate 0)
+  int dbg;         // debug experiments only (pushdbg_gemm): bit 0 = skip the hi/lo transform
   const float* bias;
   long long bias_pstride;
   float* bpart;
@@ -101,25 +103,25 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t base, int ks) {
     return ptx::umma_desc(base + ks * 1024, 4096, 512, 1);
 }
 
-// hi = tf32_rn(x) in place, lo = x - hi at `lo` (elementwise, so layout-agnostic).
-__device__ __forceinline__ void split_tile(uint8_t* base, uint8_t* lo, int bytes, int tx) {
-  float4* ph = reinterpret_cast<float4*>(base);
-  float4* pl = reinterpret_cast<float4*>(lo);
+// hi = tf32_rn(x) in place, lo = x - hi at `lo` (elementwise, so layout-agnostic; shared addresses).
+__device__ __forceinline__ void split_tile(uint32_t base, uint32_t lo, int bytes, int tx) {
 #pragma unroll 4
-  for (int i = tx; i < bytes / 16; i += kXfThreads) {
-    const float4 v = ph[i];
+  for (int i = tx * 16; i < bytes; i += kXfThreads * 16) {
+    const float4 v = ptx::lds_f4(base + i);
     float4 h, l;
-    h.x = ptx::tf32_rna(v.x); l.x = v.x - h.x;
-    h.y = ptx::tf32_rna(v.y); l.y = v.y - h.y;
-    h.z = ptx::tf32_rna(v.z); l.z = v.z - h.z;
-    h.w = ptx::tf32_rna(v.w); l.w = v.w - h.w;
-    ph[i] = h;
-    pl[i] = l;
+    h.x = ptx::tf32_rna_fast(v.x); l.x = v.x - h.x;
+    h.y = ptx::tf32_rna_fast(v.y); l.y = v.y - h.y;
+    h.z = ptx::tf32_rna_fast(v.z); l.z = v.z - h.z;
+    h.w = ptx::tf32_rna_fast(v.w); l.w = v.w - h.w;
+    ptx::sts_f4(base + i, h);
+    ptx::sts_f4(lo + i, l);
   }
 }
 
-// element (r, k) of a 32 x 32 fp32 SWIZZLE_128B box: 16-B chunk (k/4) of row r sits at chunk (k/4) ^ (r%8)
-__device__ __forceinline__ int box_idx(int r, int k) { return r * 32 + ((((k >> 2) ^ (r & 7)) << 2) | (k & 3)); }
+// generic pointer for a 32-bit shared address (the PTX wrappers take generic smem pointers)
+__device__ __forceinline__ void* ptx_ptr(uint32_t saddr) {
+  return __cvta_shared_to_generic(saddr);
+}
 
 struct TileCoord {
   int p, split, m0, nt;  // particle, K-split, first row, column-tile index
@@ -143,8 +145,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tBlo, const __grid_constant__ CUtensorMap tOut,
                       const __grid_constant__ CUtensorMap tAux, const KParams prm) {
   using C = Cfg<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B aligned base for the SWIZZLE_128B atoms; pointer arithmetic on the __shared__ array keeps
+  // every derived pointer in the shared state space (LDS/STS, not generic loads)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ebuf_all = smem + C::STAGES * C::STAGE_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(ebuf_all + C::EPI_BYTES);
   uint64_t* ready = full + C::STAGES;
@@ -182,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = ptx::lds_u32(ptx::smem_u32(tmem_slot));
 
   auto tile_kb = [&](int split, int* kb0) {
     *kb0 = split * prm.kb_per_split;
@@ -266,9 +270,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < nkb; ++i, ++it) {
         const int s = it % C::STAGES;
         ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
-        uint8_t* st = smem + s * C::STAGE_BYTES;
-        split_tile(st, st + C::A_BYTES, C::A_BYTES, tx);
-        if (BSPLIT) split_tile(st + 2 * C::A_BYTES, st + 2 * C::A_BYTES + C::B_BYTES, C::B_BYTES, tx);
+        const uint32_t st = ptx::smem_u32(smem + s * C::STAGE_BYTES);
+        if (!(prm.dbg & 1)) {
+          split_tile(st, st + C::A_BYTES, C::A_BYTES, tx);
+          if (BSPLIT) split_tile(st + 2 * C::A_BYTES, st + 2 * C::A_BYTES + C::B_BYTES, C::B_BYTES, tx);
+        }
         ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core (async proxy)
         ptx::mbar_arrive(&ready[s]);
       }
@@ -280,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int h = e >> 2;        // column half
     if (h < C::EPI_SPLIT) {
       float* ebuf = reinterpret_cast<float*>(ebuf_all + e * kEpiBox);
+      const uint32_t ebuf_s = ptx::smem_u32(ebuf);
       const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
       uint32_t ch = 0, aux_ph = 0;
       const bool bwd = prm.epi == EPI_BWD;
@@ -292,9 +299,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row0 = tc.m0 + q * 32;
         const bool live = row0 < prm.M;
         const int colw = n0 + h * C::CW;
-        if (bwd && live && lane == 0) {  // prefetch the first aprev box while the MMAs run
+        if (bwd && live && lane == 0) {  // prefetch aprev of group 0 while the MMAs run
           ptx::bulk_wait_read0();
-          ptx::mbar_arrive_expect_tx(&auxbar[e], kEpiBox);
+          ptx::mbar_arrive_expect_tx(&auxbar[e], kHalfBox);
           ptx::tma_load_3d(ebuf, &tAux, &auxbar[e], colw, row0, tc.p);
         }
         float acc[C::CW];
@@ -307,89 +314,107 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&tfull[b], (ch / C::NACC) & 1);
           ptx::tc_fence_after();
 #pragma unroll
-          for (int c0 = 0; c0 < C::CW; c0 += 32) {
-            uint32_t r[32];
-            ptx::tmem_ld_32x32b_x32(lane_base + b * BN + h * C::CW + c0, r);
+          for (int c0 = 0; c0 < C::CW; c0 += 16) {
+            uint32_t r[16];
+            ptx::tmem_ld_32x32b_x16(lane_base + b * BN + h * C::CW + c0, r);
             ptx::tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) acc[c0 + j] += __uint_as_float(r[j]);
+            for (int j = 0; j < 16; ++j) acc[c0 + j] += __uint_as_float(r[j]);
           }
           ptx::tc_fence_before();
           ptx::mbar_arrive(&tempty[b]);
         }
         if (!live) continue;
         const int pz = prm.epi == EPI_STORE ? tc.split * prm.batch + tc.p : tc.p;
+        // Output in 16-column groups g, double-buffered: group g is staged in half-box (g & 1)
+        // (32 rows x 16 fp32, SWIZZLE_64B: 16-B chunk c of row r sits at chunk c ^ ((r >> 1) & 3)),
+        // so the TMA store of group g overlaps the math of group g + 1.
+        constexpr int G = C::CW / 16;
+        const uint32_t roff = lane * 64;
+        const int swz = (lane >> 1) & 3;
 #pragma unroll
-        for (int j = 0; j < C::CW / 32; ++j) {
-          const int col = colw + j * 32;
+        for (int g = 0; g < G; ++g) {
+          const int col = colw + g * 16;
+          const uint32_t buf = ebuf_s + (g & 1) * kHalfBox;
           if (bwd) {
-            if (j > 0 && lane == 0) {
-              ptx::bulk_wait_read0();
-              ptx::mbar_arrive_expect_tx(&auxbar[e], kEpiBox);
-              ptx::tma_load_3d(ebuf, &tAux, &auxbar[e], col, row0, tc.p);
-            }
-            ptx::mbar_wait(&auxbar[e], aux_ph);
+            ptx::mbar_wait(&auxbar[e], aux_ph);  // aprev of group g has landed in buf
             aux_ph ^= 1;
           } else {
-            if (lane == 0) ptx::bulk_wait_read0();  // previous store has finished reading the box
+            if (lane == 0) ptx::bulk_wait_read1();  // the store of group g - 2 has finished reading buf
             __syncwarp();
           }
-          float* rowp = ebuf + lane * 32;
           if (prm.epi == EPI_FWD) {
-            const float4* bias = reinterpret_cast<const float4*>(prm.bias + tc.p * prm.bias_pstride + col);
+            const float* bias = prm.bias + tc.p * prm.bias_pstride + col;  // b_l need not be 16-B aligned
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
-              const float4 bv = __ldg(bias + c4);
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const float4 bv = make_float4(__ldg(bias + 4 * c4), __ldg(bias + 4 * c4 + 1), __ldg(bias + 4 * c4 + 2),
+                                            __ldg(bias + 4 * c4 + 3));
               float4 v;
-              v.x = act_fwd(acc[j * 32 + 4 * c4 + 0] + bv.x, prm.act);
-              v.y = act_fwd(acc[j * 32 + 4 * c4 + 1] + bv.y, prm.act);
-              v.z = act_fwd(acc[j * 32 + 4 * c4 + 2] + bv.z, prm.act);
-              v.w = act_fwd(acc[j * 32 + 4 * c4 + 3] + bv.w, prm.act);
-              *reinterpret_cast<float4*>(rowp + ((c4 ^ (lane & 7)) << 2)) = v;
+              v.x = act_fwd(acc[g * 16 + 4 * c4 + 0] + bv.x, prm.act);
+              v.y = act_fwd(acc[g * 16 + 4 * c4 + 1] + bv.y, prm.act);
+              v.z = act_fwd(acc[g * 16 + 4 * c4 + 2] + bv.z, prm.act);
+              v.w = act_fwd(acc[g * 16 + 4 * c4 + 3] + bv.w, prm.act);
+              ptx::sts_f4(buf + roff + ((c4 ^ swz) << 4), v);
             }
           } else if (bwd) {
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
-              float4* pp = reinterpret_cast<float4*>(rowp + ((c4 ^ (lane & 7)) << 2));
-              const float4 a = *pp;
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const uint32_t pp = buf + roff + ((c4 ^ swz) << 4);
+              const float4 a = ptx::lds_f4(pp);
               float4 v;
-              v.x = acc[j * 32 + 4 * c4 + 0] * act_deriv_from_a(a.x, prm.act);
-              v.y = acc[j * 32 + 4 * c4 + 1] * act_deriv_from_a(a.y, prm.act);
-              v.z = acc[j * 32 + 4 * c4 + 2] * act_deriv_from_a(a.z, prm.act);
-              v.w = acc[j * 32 + 4 * c4 + 3] * act_deriv_from_a(a.w, prm.act);
-              *pp = v;
+              v.x = acc[g * 16 + 4 * c4 + 0] * act_deriv_from_a(a.x, prm.act);
+              v.y = acc[g * 16 + 4 * c4 + 1] * act_deriv_from_a(a.y, prm.act);
+              v.z = acc[g * 16 + 4 * c4 + 2] * act_deriv_from_a(a.z, prm.act);
+              v.w = acc[g * 16 + 4 * c4 + 3] * act_deriv_from_a(a.w, prm.act);
+              ptx::sts_f4(pp, v);
             }
           } else {
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4)
-              *reinterpret_cast<float4*>(rowp + ((c4 ^ (lane & 7)) << 2)) =
-                  make_float4(acc[j * 32 + 4 * c4], acc[j * 32 + 4 * c4 + 1], acc[j * 32 + 4 * c4 + 2],
-                              acc[j * 32 + 4 * c4 + 3]);
+            for (int c4 = 0; c4 < 4; ++c4)
+              ptx::sts_f4(buf + roff + ((c4 ^ swz) << 4),
+                          make_float4(acc[g * 16 + 4 * c4], acc[g * 16 + 4 * c4 + 1], acc[g * 16 + 4 * c4 + 2],
+                                      acc[g * 16 + 4 * c4 + 3]));
           }
           __syncwarp();
           if (bwd && prm.bpart) {
             // a5 of the layer below: column partial sums of delta over this warp's 32 rows (rows >= M are
-            // zero: their A rows were zero-filled by TMA), in ascending row order; lane = column.
+            // zero: their A rows were zero-filled by TMA).  Lane l: column l & 15, rows 16*(l >> 4) + 0..15
+            // ascending, then the two halves added (commutative, so both lanes get the same bits).
             const int rb = row0 / 32;
-            float s = 0.f;
-#pragma unroll 8
-            for (int r = 0; r < 32; ++r) s += ebuf[box_idx(r, lane)];
-            prm.bpart[rb * prm.bp_sstride + tc.p * prm.bp_pstride + col + lane] = s;
+            const int cl = lane & 15, r0 = (lane >> 4) * 16;
+            float v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r)
+              v[r] = ptx::lds_f32(buf + (r0 + r) * 64 + ((((cl >> 2) ^ (((r0 + r) >> 1) & 3)) << 4) | ((cl & 3) << 2)));
+            float sm = 0.f;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) sm += v[r];
+            sm += __shfl_xor_sync(0xffffffffu, sm, 16);
+            if (lane < 16) prm.bpart[rb * prm.bp_sstride + tc.p * prm.bp_pstride + col + cl] = sm;
             for (int i = 0; i < prm.din; ++i) {
               float sx = 0.f;
-              for (int r = 0; r < 32; ++r) {
-                const int row = row0 + r;
+#pragma unroll
+              for (int r = 0; r < 16; ++r) {
+                const int row = row0 + r0 + r;
                 const float xv = row < prm.M ? __ldg(prm.x + (long long)row * prm.din + i) : 0.f;
-                sx = fmaf(ebuf[box_idx(r, lane)], xv, sx);
+                sx = fmaf(v[r], xv, sx);
               }
-              prm.xpart[rb * prm.xp_sstride + tc.p * prm.xp_pstride + (long long)(col + lane) * prm.din + i] = sx;
+              sx += __shfl_xor_sync(0xffffffffu, sx, 16);
+              if (lane < 16)
+                prm.xpart[rb * prm.xp_sstride + tc.p * prm.xp_pstride + (long long)(col + cl) * prm.din + i] = sx;
             }
           }
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            ptx::tma_store_3d(&tOut, ebuf, col, row0, pz);
+            ptx::tma_store_3d(&tOut, ptx_ptr(buf), col, row0, pz);
             ptx::bulk_commit();
+            if (bwd && g + 1 < G) {  // prefetch aprev of group g + 1 once the store of group g - 1 has read it
+              ptx::bulk_wait_read1();
+              const uint32_t nb = ebuf_s + ((g + 1) & 1) * kHalfBox;
+              ptx::mbar_arrive_expect_tx(&auxbar[e], kHalfBox);
+              ptx::tma_load_3d(ptx_ptr(nb), &tAux, &auxbar[e], col + 16, row0, tc.p);
+            }
           }
         }
       }
@@ -424,14 +449,14 @@ push_status get_encoder() {
 
 // 3-D fp32 tensor map {d0 (contiguous), d1, d2} with box {32, box1, 1}, zero OOB fill.
 push_status make_map(CUtensorMap* m, const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_el,
-                     uint64_t stride2_el, uint32_t box1, CUtensorMapSwizzle swz) {
+                     uint64_t stride2_el, uint32_t box1, CUtensorMapSwizzle swz, uint32_t box0 = 32) {
   if (d2 <= 1) {  // a shared operand: the stride of a unit dimension is never used
     d2 = 1;
     stride2_el = stride1_el * d1;
   }
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {stride1_el * 4, stride2_el * 4};
-  cuuint32_t box[3] = {32, box1, 1};
+  cuuint32_t box[3] = {box0, box1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -515,17 +540,18 @@ push_status run(const Problem& pb, cudaStream_t stream) {
     if ((st = make_operand_map(pb.B.lo, pb.B, pb.N, pb.K, pb.batch, BN, &maps[2])) != PUSH_OK) return st;
   }
   const int nout = pb.epi == EPI_STORE ? pb.splits * pb.batch : pb.batch;
-  if ((st = make_map(&maps[3], pb.out, pb.N, pb.M, nout, pb.ldo, pb.out_pstride, 32, CU_TENSOR_MAP_SWIZZLE_128B)) !=
-      PUSH_OK)
+  if ((st = make_map(&maps[3], pb.out, pb.N, pb.M, nout, pb.ldo, pb.out_pstride, 32, CU_TENSOR_MAP_SWIZZLE_64B,
+                     16)) != PUSH_OK)
     return st;
   if (pb.epi == EPI_BWD &&
       (st = make_map(&maps[4], pb.aprev, pb.N, pb.M, pb.batch, pb.ld_aprev, pb.aprev_pstride, 32,
-                     CU_TENSOR_MAP_SWIZZLE_128B)) != PUSH_OK)
+                     CU_TENSOR_MAP_SWIZZLE_64B, 16)) != PUSH_OK)
     return st;
   KParams kp;
   std::memset(&kp, 0, sizeof(kp));
   kp.M = pb.M; kp.N = pb.N; kp.K = pb.K; kp.batch = pb.batch; kp.splits = pb.splits; kp.kb_per_split = kbps;
-  kp.passes = pb.passes; kp.epi = pb.epi; kp.act = pb.act;
+  kp.passes = pb.passes & 0xff; kp.epi = pb.epi; kp.act = pb.act;
+  kp.dbg = pb.passes >> 8;
   kp.mt = (pb.M + BM - 1) / BM;
   kp.nt = pb.N / BN;
   kp.ntiles = kp.mt * kp.nt * pb.splits * pb.batch;

@@ -65,8 +65,9 @@ struct PartView {
 };
 // G_p[off_w + o*in + i] = -lambda * sum_s W(s,p,o,i) + prior(theta)   (o < out, i < in)
 // G_p[off_b + o]        = -lambda * sum_s Bv(s,p,o,0) + prior(theta)
-void finalize_layer(PartView W, PartView Bv, const float* theta, float* grad, int64_t ld, int64_t off_w, int in,
-                    int out, float lambda, int prior, float inv_sigma2, int batch, cudaStream_t s);
+// Returns the number of kernels launched (1 or 2).
+int finalize_layer(PartView W, PartView Bv, const float* theta, float* grad, int64_t ld, int64_t off_w, int in,
+                   int out, float lambda, int prior, float inv_sigma2, int batch, cudaStream_t s);
 
 // ---------------------------------------------------------------- K0 init (R14)
 struct InitTable {

@@ -38,9 +38,9 @@ __global__ void thin_forward_kernel(const float* __restrict__ in, int64_t in_pst
                                     float* __restrict__ out, int64_t out_pstride, int B) {
   const int p = blockIdx.y;
   const int per = VEC ? 4 : 1;
-  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * per;
-  if (t >= (int64_t)B * nout) return;
-  const int b = (int)(t / nout), o = (int)(t % nout);
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) * per;  // B * nout < 2^31 (max_batch * width)
+  if (t >= B * nout) return;
+  const int b = t / nout, o = t - b * nout;
   const float* W = theta + p * ld + off_w;
   const float* bias = theta + p * ld + off_b;
   const float* x = in + p * in_pstride + (int64_t)b * nin;
@@ -79,34 +79,33 @@ void thin_forward(const float* in, int64_t in_pstride, const float* theta, int64
 }
 
 // ---------------------------------------------------------------- fused output layer (a3 + a4/a5 of the top)
-// One warp per 32-row block rb of particle p:
-//   phase 1 (per row b): yhat_o = a_b . W_o + b_o (lanes split the features; fixed xor tree),
-//                        e = yhat - y, err2[b] = sum_o e^2, dL_o = 2 e_o / (B d_out)
-//   phase 2 (per feature i, lanes own features): over the block's rows in ascending order
+// One 256-thread block per 32-row block rb of particle p:
+//   phase 1 (warp w, rows 4w..4w+3): yhat_o = a_b . W_o + b_o (lanes split the features; fixed xor
+//            tree), e = yhat - y, err2[b] = sum_o e^2, dL_o(b) = 2 e_o / (B d_out)   -> smem
+//   phase 2 (thread t owns features i = t, t+256, ...; rows in ascending order):
 //        wpart[rb][p][o][i]   = sum_b dL_o(b) a_b[i]                  (dW of the output layer)
 //        dprev[b][i]          = (sum_o dL_o(b) W_o[i]) sigma'(a_b[i])  (delta of the layer below)
 //        bprev[rb][p][i]      = sum_b dprev[b][i]                     (its bias-gradient partial)
 //   and bpart[rb][p][o] = sum_b dL_o(b).
-constexpr int OUT_FPL = 4;  // features per lane per phase-2 pass
-__global__ void __launch_bounds__(256) output_fused_kernel(OutputArgs a) {
-  __shared__ float sdl[8][32][kMaxDout];
+__global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
+  __shared__ float sdl[32][kMaxDout];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.y;
-  const int rb = blockIdx.x * 8 + warp;
-  const int RB = (a.B + 31) / 32;
-  if (rb >= RB) return;
-  const float* A = a.A + p * a.a_pstride;
-  const float* W = a.theta + p * a.ld + a.off_w;
-  const float* bias = a.theta + p * a.ld + a.off_b;
+  const int rb = blockIdx.x;
+  const int rows = min(32, a.B - rb * 32);
+  const float* __restrict__ A = a.A + p * a.a_pstride + (int64_t)rb * 32 * a.H;
+  const float* __restrict__ W = a.theta + p * a.ld + a.off_w;
+  const float* __restrict__ bias = a.theta + p * a.ld + a.off_b;
   const float scale = 2.0f / (float)((int64_t)a.B * a.dout);
   // phase 1
-  for (int r = 0; r < 32; ++r) {
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = warp * 4 + rr;
     const int b = rb * 32 + r;
     float e2 = 0.f;
     for (int o = 0; o < a.dout; ++o) {
       float dl = 0.f;
-      if (b < a.B) {
-        const float* arow = A + (int64_t)b * a.H;
+      if (r < rows) {
+        const float* arow = A + (int64_t)r * a.H;
         const float* wrow = W + (int64_t)o * a.H;
         float part = 0.f;
         for (int i = lane; i < a.H; i += 32) part = fmaf(__ldg(arow + i), __ldg(wrow + i), part);
@@ -116,68 +115,50 @@ __global__ void __launch_bounds__(256) output_fused_kernel(OutputArgs a) {
         e2 = fmaf(e, e, e2);
         dl = scale * e;
       }
-      if (lane == 0) sdl[warp][r][o] = dl;
+      if (lane == 0) sdl[r][o] = dl;
     }
-    if (lane == 0 && b < a.B) a.err2[p * a.err_pstride + b] = e2;
+    if (lane == 0 && r < rows) a.err2[p * a.err_pstride + b] = e2;
   }
-  __syncwarp();
-  if (lane < a.dout) {
+  __syncthreads();
+  if (threadIdx.x < a.dout) {
     float sb = 0.f;
-    for (int r = 0; r < 32; ++r) sb += sdl[warp][r][lane];
-    a.bpart_out[(int64_t)rb * a.bo_sstride + p * a.bo_pstride + lane] = sb;
+    for (int r = 0; r < 32; ++r) sb += sdl[r][threadIdx.x];
+    a.bpart_out[(int64_t)rb * a.bo_sstride + p * a.bo_pstride + threadIdx.x] = sb;
   }
   // phase 2
-  const int rows = min(32, a.B - rb * 32);
-  for (int f0 = 0; f0 < a.H; f0 += 32 * OUT_FPL) {
-    float w[OUT_FPL][kMaxDout], wacc[OUT_FPL][kMaxDout], bacc[OUT_FPL];
+  float* __restrict__ dprev = a.dprev ? a.dprev + p * a.dp_pstride + (int64_t)rb * 32 * a.H : nullptr;
+  for (int i = threadIdx.x; i < a.H; i += 256) {
+    float w[kMaxDout], wacc[kMaxDout];
 #pragma unroll
-    for (int k = 0; k < OUT_FPL; ++k) {
-      const int i = f0 + k * 32 + lane;
-      bacc[k] = 0.f;
+    for (int o = 0; o < kMaxDout; ++o) {
+      w[o] = o < a.dout ? __ldg(W + (int64_t)o * a.H + i) : 0.f;
+      wacc[o] = 0.f;
+    }
+    float bacc = 0.f;
+#pragma unroll 8
+    for (int r = 0; r < rows; ++r) {
+      const float av = __ldg(A + (int64_t)r * a.H + i);
+      float d = 0.f;
 #pragma unroll
       for (int o = 0; o < kMaxDout; ++o) {
-        w[k][o] = (o < a.dout && i < a.H) ? __ldg(W + (int64_t)o * a.H + i) : 0.f;
-        wacc[k][o] = 0.f;
+        const float dl = sdl[r][o];
+        wacc[o] = fmaf(dl, av, wacc[o]);
+        d = fmaf(dl, w[o], d);
+      }
+      if (dprev) {
+        d *= act_deriv_from_a(av, a.act);
+        dprev[(int64_t)r * a.H + i] = d;
+        bacc += d;
       }
     }
-    for (int r = 0; r < rows; ++r) {
-      const int b = rb * 32 + r;
-      float dl[kMaxDout];
-#pragma unroll
-      for (int o = 0; o < kMaxDout; ++o) dl[o] = o < a.dout ? sdl[warp][r][o] : 0.f;
-#pragma unroll
-      for (int k = 0; k < OUT_FPL; ++k) {
-        const int i = f0 + k * 32 + lane;
-        if (i < a.H) {
-          const float av = __ldg(A + (int64_t)b * a.H + i);
-          float d = 0.f;
-#pragma unroll
-          for (int o = 0; o < kMaxDout; ++o) {
-            wacc[k][o] = fmaf(dl[o], av, wacc[k][o]);
-            d = fmaf(dl[o], w[k][o], d);
-          }
-          if (a.dprev) {
-            d *= act_deriv_from_a(av, a.act);
-            a.dprev[p * a.dp_pstride + (int64_t)b * a.H + i] = d;
-            bacc[k] += d;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < OUT_FPL; ++k) {
-      const int i = f0 + k * 32 + lane;
-      if (i < a.H) {
-        for (int o = 0; o < a.dout; ++o)
-          a.wpart[(int64_t)rb * a.wo_sstride + p * a.wo_pstride + (int64_t)o * a.H + i] = wacc[k][o];
-        if (a.dprev) a.bpart_prev[(int64_t)rb * a.bp_sstride + p * a.bp_pstride + i] = bacc[k];
-      }
-    }
+    for (int o = 0; o < a.dout; ++o)
+      a.wpart[(int64_t)rb * a.wo_sstride + p * a.wo_pstride + (int64_t)o * a.H + i] = wacc[o];
+    if (dprev) a.bpart_prev[(int64_t)rb * a.bp_sstride + p * a.bp_pstride + i] = bacc;
   }
 }
 void output_fused(const OutputArgs& a, int batch, cudaStream_t s) {
   const int RB = (a.B + 31) / 32;
-  output_fused_kernel<<<dim3((RB + 7) / 8, batch), 256, 0, s>>>(a);
+  output_fused_kernel<<<dim3(RB, batch), 256, 0, s>>>(a);
 }
 
 __global__ void loss_reduce_kernel(const float* __restrict__ err2, int64_t err_pstride, float* __restrict__ loss,
@@ -203,9 +184,9 @@ __global__ void thin_backward_kernel(const float* __restrict__ dl, int64_t d_pst
                                      int64_t ld, int64_t off_w, int nin, int nout, const float* __restrict__ aprev,
                                      int64_t a_pstride, int act, float* __restrict__ o, int64_t o_pstride, int B) {
   const int p = blockIdx.y;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)B * nin) return;
-  const int b = (int)(t / nin), i = (int)(t % nin);
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B * nin) return;
+  const int b = t / nin, i = t - b * nin;
   const float* W = theta + p * ld + off_w;
   const float* drow = dl + p * d_pstride + (int64_t)b * nout;
   float acc = 0.f;
@@ -225,12 +206,12 @@ __global__ void thin_wgrad_kernel(const float* __restrict__ dl, int64_t d_pstrid
                                   int64_t a_pstride, int nin, int nout, float* __restrict__ part, int B) {
   const int p = blockIdx.z, s = blockIdx.y, P = gridDim.z;
   const int cols = nin + 1;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t tot = (int64_t)nout * cols;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int tot = nout * cols;
   if (t >= tot) return;
   int o, i;
-  if (cols >= nout) { o = (int)(t / cols); i = (int)(t % cols); }     // input index fastest: coalesced A
-  else { i = (int)(t / nout); o = (int)(t % nout); }                 // output index fastest: coalesced delta
+  if (cols >= nout) { o = t / cols; i = t - o * cols; }     // input index fastest: coalesced A
+  else { i = t / nout; o = t - i * nout; }                 // output index fastest: coalesced delta
   const int b0 = s * THIN_CHUNK, b1 = min(B, b0 + THIN_CHUNK);
   const float* dcol = dl + p * d_pstride + o;
   float acc = 0.f;
@@ -252,32 +233,80 @@ int thin_wgrad(const float* dl, int64_t d_pstride, const float* A, int64_t a_pst
 }
 
 // ---------------------------------------------------------------- finalize G rows of one layer
-__global__ void finalize_kernel(PartView W, PartView Bv, const float* __restrict__ theta, float* __restrict__ grad,
-                                int64_t ld, int64_t off_w, int nin, int nout, float lambda, int prior,
-                                float inv_sigma2) {
-  const int p = blockIdx.y;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nw = (int64_t)nin * nout;
-  if (t >= nw + nout) return;
-  float v = 0.f;
+// G_p[off_w + t] = -lambda * sum_s part(s, p, t) + grad log p0(theta_p[off_w + t]) for t in [t0, t1)
+// (t < in*out: weight (o, i) = (t / in, t % in) from W; else bias o = t - in*out from Bv).
+// Few partials (<= kThreadSplits): one thread per element, ascending s.  Many partials: one warp
+// per element, lane l sums s = l, l+32, ... ascending, then a fixed xor tree.  Either order
+// depends only on the partial count, never on the sharding.
+constexpr int kThreadSplits = 16;
+__device__ __forceinline__ const float* part_ptr(const PartView& W, const PartView& Bv, int p, int64_t t, int nin,
+                                                 int64_t nw, int* splits, int64_t* sstride) {
   if (t < nw) {
-    const int o = (int)(t / nin), i = (int)(t % nin);
-    const float* src = W.base + p * W.pstride + (int64_t)o * W.ostride + i;
-    for (int s = 0; s < W.splits; ++s) v += src[s * W.sstride];
-  } else {
-    const int o = (int)(t - nw);
-    const float* src = Bv.base + p * Bv.pstride + (int64_t)o * Bv.ostride;
-    for (int s = 0; s < Bv.splits; ++s) v += src[s * Bv.sstride];
+    *splits = W.splits;
+    *sstride = W.sstride;
+    const int o = (int)t / nin;  // t < in*out < 2^31
+    return W.base + p * W.pstride + (int64_t)o * W.ostride + ((int)t - o * nin);
   }
-  const int64_t idx = p * ld + off_w + t;
+  *splits = Bv.splits;
+  *sstride = Bv.sstride;
+  return Bv.base + p * Bv.pstride + (t - nw) * Bv.ostride;
+}
+__device__ __forceinline__ void finalize_store(const float* theta, float* grad, int64_t idx, float v, float lambda,
+                                               int prior, float inv_sigma2) {
   const float pr = (prior == PUSH_PRIOR_GAUSSIAN) ? -theta[idx] * inv_sigma2 : 0.f;
   grad[idx] = fmaf(-lambda, v, pr);
 }
-void finalize_layer(PartView W, PartView Bv, const float* theta, float* grad, int64_t ld, int64_t off_w, int in,
-                    int out, float lambda, int prior, float inv_sigma2, int batch, cudaStream_t s) {
-  const int64_t tot = (int64_t)in * out + out;
-  finalize_kernel<<<dim3((unsigned)((tot + 255) / 256), batch), 256, 0, s>>>(W, Bv, theta, grad, ld, off_w, in, out,
-                                                                             lambda, prior, inv_sigma2);
+__global__ void finalize_thread_kernel(PartView W, PartView Bv, const float* __restrict__ theta,
+                                       float* __restrict__ grad, int64_t ld, int64_t off_w, int nin, int nout,
+                                       int64_t t0, int64_t t1, float lambda, int prior, float inv_sigma2) {
+  const int p = blockIdx.y;
+  const int64_t t = t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= t1) return;
+  int splits;
+  int64_t ss;
+  const float* src = part_ptr(W, Bv, p, t, nin, (int64_t)nin * nout, &splits, &ss);
+  float v = 0.f;
+  for (int s = 0; s < splits; ++s) v += src[s * ss];
+  finalize_store(theta, grad, p * ld + off_w + t, v, lambda, prior, inv_sigma2);
+}
+__global__ void finalize_warp_kernel(PartView W, PartView Bv, const float* __restrict__ theta,
+                                     float* __restrict__ grad, int64_t ld, int64_t off_w, int nin, int nout,
+                                     int64_t t0, int64_t t1, float lambda, int prior, float inv_sigma2) {
+  const int p = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int64_t t = t0 + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  if (t >= t1) return;
+  int splits;
+  int64_t ss;
+  const float* src = part_ptr(W, Bv, p, t, nin, (int64_t)nin * nout, &splits, &ss);
+  float v = 0.f;
+  for (int s = lane; s < splits; s += 32) v += src[s * ss];
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  if (lane == 0) finalize_store(theta, grad, p * ld + off_w + t, v, lambda, prior, inv_sigma2);
+}
+int finalize_layer(PartView W, PartView Bv, const float* theta, float* grad, int64_t ld, int64_t off_w, int in,
+                   int out, float lambda, int prior, float inv_sigma2, int batch, cudaStream_t s) {
+  const int64_t nw = (int64_t)in * out;
+  int launches = 0;
+  auto launch = [&](int64_t t0, int64_t t1, int splits) {
+    if (t1 <= t0) return;
+    if (splits <= kThreadSplits) {
+      finalize_thread_kernel<<<dim3((unsigned)((t1 - t0 + 255) / 256), batch), 256, 0, s>>>(
+          W, Bv, theta, grad, ld, off_w, in, out, t0, t1, lambda, prior, inv_sigma2);
+    } else {
+      finalize_warp_kernel<<<dim3((unsigned)((t1 - t0 + 7) / 8), batch), 256, 0, s>>>(
+          W, Bv, theta, grad, ld, off_w, in, out, t0, t1, lambda, prior, inv_sigma2);
+    }
+    ++launches;
+  };
+  if ((W.splits <= kThreadSplits) == (Bv.splits <= kThreadSplits)) {
+    launch(0, nw + out, W.splits);
+  } else {
+    launch(0, nw, W.splits);
+    launch(nw, nw + out, Bv.splits);
+  }
+  return launches;
 }
 
 // ---------------------------------------------------------------- set_grads copy

@@ -124,25 +124,31 @@ void dist_partial(const float* theta, int64_t ld, int n, const DistPlan& pl, flo
     dist_partial_kernel<64><<<grid, 256, 0, s>>>(theta, ld, n, pl.ntile, pl.cols, part);
 }
 
+// One warp per D entry: lane l sums splits s = l, l+32, ... ascending, then a fixed xor tree
+// (order depends only on the split count, which depends only on (n, ld)).
 __global__ void dist_reduce_kernel(const float* __restrict__ part, int n, int splits, float* __restrict__ D) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nn = (int64_t)n * n;
   if (t >= nn) return;
-  const int i = (int)(t / n), j = (int)(t % n);
+  const int i = (int)(t / n), j = (int)(t - (int64_t)i * n);
   float v = 0.f;
   if (i != j)
-    for (int s = 0; s < splits; ++s) v += part[s * nn + t];
-  D[t] = v;  // diagonal is exactly +0
+    for (int s = lane; s < splits; s += 32) v += part[s * nn + t];
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  if (lane == 0) D[t] = v;  // diagonal is exactly +0
 }
 void dist_reduce(const float* part, int n, int splits, float* D, cudaStream_t s) {
   const int64_t nn = (int64_t)n * n;
-  dist_reduce_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(part, n, splits, D);
+  dist_reduce_kernel<<<(unsigned)((nn * 32 + 255) / 256), 256, 0, s>>>(part, n, splits, D);
 }
 
 // ---------------------------------------------------------------- a8 + a9
 // Block-wide radix select of the rank-th smallest key among N non-negative floats
 // (their IEEE bit patterns order like the values).  Histogram counts are
-// order-independent, so the result is deterministic.
+// order-independent, so the result is deterministic.  The 256-bin prefix search is
+// done by warp 0 (8 bins per lane + a shuffle scan), not serially.
 __device__ uint32_t block_select(const float* __restrict__ D, int64_t N, uint32_t rank, uint32_t* hist,
                                  uint32_t* sh) {
   uint32_t prefix = 0, mask = 0;
@@ -154,15 +160,32 @@ __device__ uint32_t block_select(const float* __restrict__ D, int64_t N, uint32_
       if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t cum = 0;
-      int b = 0;
-      for (; b < 255; ++b) {
-        if (cum + hist[b] > rank) break;
-        cum += hist[b];
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      uint32_t c[8], tot = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        c[k] = hist[lane * 8 + k];
+        tot += c[k];
       }
-      sh[0] = prefix | (static_cast<uint32_t>(b) << shift);
-      sh[1] = rank - cum;
+      uint32_t incl = tot;  // inclusive scan of per-lane totals
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, m);
+        if (lane >= m) incl += v;
+      }
+      const uint32_t excl = incl - tot;
+      // the lane whose range [excl, incl) contains `rank` finds the bin
+      if (rank >= excl && rank < incl) {
+        uint32_t cum = excl;
+        int b = lane * 8;
+        for (int k = 0; k < 8; ++k, ++b) {
+          if (cum + c[k] > rank) break;
+          cum += c[k];
+        }
+        sh[0] = prefix | (static_cast<uint32_t>(b) << shift);
+        sh[1] = rank - cum;
+      }
     }
     __syncthreads();
     prefix = sh[0];

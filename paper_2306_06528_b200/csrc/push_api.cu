@@ -41,7 +41,8 @@ struct LayerPlan {
   int in = 0, out = 0;
   int64_t off_w = 0, off_b = 0;  // canonical offsets in a particle row
   bool gemm = false;             // tensor-core path (hidden layer with in, out % 32 == 0)
-  int64_t woff = 0;              // offset of this layer's hi/lo weight copy (per-particle block)
+  bool wraw = false;             // GEMM reads W straight from Theta (16-B aligned) and splits it in smem
+  int64_t woff = 0;              // offset of this layer's hi/lo weight copy (per-particle block), !wraw only
 };
 
 constexpr int kMaxX0 = 4;  // thin first layer whose weight grads are fused into layer 1's BWD epilogue
@@ -121,9 +122,12 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   int64_t max_w = 0, max_t = 0;
   for (int l = 0; l < P.L; ++l) {
     LayerPlan& lp = P.layers[l];
-    if (lp.gemm) {
+    lp.wraw = lp.gemm && (lp.off_w % 4 == 0);
+    if (lp.gemm && !lp.wraw) {
       lp.woff = P.wsplit_total;
       P.wsplit_total += round_up((int64_t)lp.in * lp.out, 32);
+    }
+    if (lp.gemm) {
       max_w = std::max<int64_t>(max_w, (int64_t)lp.in * lp.out);
       max_t = std::max<int64_t>(max_t, lp.out);  // bias-only column sums
     } else if (l < P.L - 1) {
@@ -338,19 +342,23 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
   push_status st;
   auto finalize = [&](int l, const kern::PartView& W, const kern::PartView& Bv) {
     const LayerPlan& lp = P.layers[l];
-    return run_k(c, PC_FINALIZE, 1, 0, 0, s, [&] {
-      kern::finalize_layer(W, Bv, th, g, ld, lp.off_w, lp.in, lp.out, lambda, c->cfg.prior, inv_s2, nl, s);
+    int nk = 0;
+    push_status r = run_k(c, PC_FINALIZE, 0, 0, 0, s, [&] {
+      nk = kern::finalize_layer(W, Bv, th, g, ld, lp.off_w, lp.in, lp.out, lambda, c->cfg.prior, inv_s2, nl, s);
       return PUSH_OK;
     });
+    c->launches += nk;
+    return r;
   };
 
   // C1: Theta rows of every rank (needed by a7/a10; unchanged during the gradient phase)
   if ((st = exchange(c, BUF_THETA, s)) != PUSH_OK) return st;
 
-  // a0: tf32 hi/lo copies of the tensor-core weights (activations are split inside the GEMM)
+  // a0: tf32 hi/lo copies of tensor-core weights that are not 16-B aligned in Theta (the others, and all
+  // activations, are split on the staged tile inside the GEMM)
   for (int l = 0; l < L; ++l) {
     const LayerPlan& lp = P.layers[l];
-    if (!lp.gemm) continue;
+    if (!lp.gemm || lp.wraw) continue;
     const int64_t cnt = (int64_t)lp.in * lp.out;
     st = run_k(c, PC_SPLIT, 1, 12.0 * cnt * nl, 0, s, [&] {
       kern::split_hilo(th + lp.off_w, ld, c->whi + lp.woff, c->wlo + lp.woff, P.wsplit_total, cnt, nl, s);
@@ -368,7 +376,8 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
       gemm::Problem pb;
       pb.M = B; pb.N = lp.out; pb.K = lp.in; pb.batch = nl; pb.splits = 1; pb.passes = 3;
       pb.A = gemm::Operand{in.p, nullptr, true, false, lp.in, in.pst};
-      pb.B = gemm::Operand{c->whi + lp.woff, c->wlo + lp.woff, false, false, lp.in, P.wsplit_total};
+      pb.B = lp.wraw ? gemm::Operand{th + lp.off_w, nullptr, true, false, lp.in, ld}
+                     : gemm::Operand{c->whi + lp.woff, c->wlo + lp.woff, false, false, lp.in, P.wsplit_total};
       pb.epi = gemm::EPI_FWD; pb.act = act;
       pb.out = c->act[l]; pb.ldo = lp.out; pb.out_pstride = P.act_pst[l];
       pb.bias = th + lp.off_b; pb.bias_pstride = ld;
@@ -473,7 +482,8 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
       gemm::Problem pb;
       pb.M = B; pb.N = lp.in; pb.K = lp.out; pb.batch = nl; pb.splits = 1; pb.passes = 3;
       pb.A = gemm::Operand{dl, nullptr, true, false, lp.out, P.dlt_pst};
-      pb.B = gemm::Operand{c->whi + lp.woff, c->wlo + lp.woff, false, true, lp.in, P.wsplit_total};
+      pb.B = lp.wraw ? gemm::Operand{th + lp.off_w, nullptr, true, true, lp.in, ld}
+                     : gemm::Operand{c->whi + lp.woff, c->wlo + lp.woff, false, true, lp.in, P.wsplit_total};
       pb.epi = gemm::EPI_BWD; pb.act = act;
       pb.out = o; pb.ldo = lp.in; pb.out_pstride = P.dlt_pst;
       pb.aprev = aprev.p; pb.ld_aprev = lp.in; pb.aprev_pstride = aprev.pst;
@@ -902,7 +912,8 @@ push_status pushdbg_gemm1xtf32(int32_t a_mn, int32_t b_mn, int32_t M, int32_t N,
 }
 push_status pushdbg_gemm(int32_t passes, int32_t a_mn, int32_t b_mn, int32_t b_split, int32_t M, int32_t N, int32_t K,
                          int32_t batch, const float* A_dev, const float* B_dev, float* C_dev, void* stream) {
-  if (passes != 1 && passes != 3) return fail(PUSH_E_INVALID, "passes must be 1 or 3");
+  // low byte: 1 or 3 passes; bits 8+: kernel experiment flags (bit 8: skip the in-smem hi/lo split)
+  if ((passes & 0xff) != 1 && (passes & 0xff) != 3) return fail(PUSH_E_INVALID, "passes must be 1 or 3");
   return dbg_gemm(passes, a_mn, b_mn, b_split, M, N, K, batch, A_dev, B_dev, C_dev, stream);
 }
 

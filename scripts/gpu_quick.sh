@@ -10,4 +10,4 @@ timeout 300 python -m pytest tests/test_gpu_gemm.py -x -q > $OUT/gemm.log 2>&1; 
 timeout 600 python -m pytest tests/test_gpu_parity.py -q > $OUT/parity.log 2>&1; echo "exit $?" >> $OUT/parity.log
 timeout 300 python __graft_entry__.py smoke > $OUT/smoke.log 2>&1; echo "exit $?" >> $OUT/smoke.log
 timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > $OUT/bench.json 2> $OUT/bench.err
-tail -3 $OUT/gemm.log; tail -15 $OUT/parity.log; tail -2 $OUT/smoke.log; cat $OUT/bench.json | head -c 3000; tail -5 $OUT/bench.err
+grep -E "^FAILED|passed|failed" $OUT/gemm.log | head -20; grep -E "^FAILED|passed|failed|^E " $OUT/parity.log | head -30; tail -2 $OUT/smoke.log; cat $OUT/bench.json | head -c 3000; tail -5 $OUT/bench.err

@@ -53,6 +53,7 @@ GRAD_CASES = [
     (3, [2, 64, 64, 33, 1], 200, "tanh", "uniform", 1.0, 1.0, "gauss"),   # GEMM layer under a thin hidden layer
     (2, [4, 64, 64, 2], 333, "tanh", "gaussian", 2.0, 1.0, "gauss"),      # d_out = 2, fused x0 with d_in = 4
     (2, [3, 128, 1], 8192, "tanh", "uniform", 1.0, 1.0, "burgers"),       # L = 2: output layer right above thin
+    (2, [1, 33, 32, 32, 1], 160, "tanh", "uniform", 1.0, 1.0, "gauss"),   # GEMM layer with W not 16-B aligned
 ]
 
 
