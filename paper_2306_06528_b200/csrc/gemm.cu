@@ -7,13 +7,19 @@
 //
 // 3xTF32: every operand x is used as hi = tf32_rn(x), lo = x - hi and
 //   C = A_lo*B_hi + A_hi*B_lo + A_hi*B_hi       (3 tcgen05.mma kind::tf32 per k-step, lo*lo dropped)
-// accumulated in TMEM in fp32.  Activations and deltas live in HBM as ONE fp32 array; the hi/lo
-// split happens on the staged shared-memory tile (transform warps), so each byte is read once.
+// accumulated in TMEM in fp32.  Activations, deltas and weights live in HBM as ONE fp32 array; the
+// hi/lo split happens on chip (transform warps), so each byte is read once.
 //
-// Kernel shape (v3): persistent, one CTA per SM, tiles of 128 x BN, 14 warps:
+// Shared-memory bandwidth is the binding resource of a 3-pass tf32 GEMM (TMA writes, the split and
+// three operand reads per k-step all go through it), so the A operand is kept out of it: the
+// transform warps write A's hi/lo straight into TMEM and the MMAs read A from TMEM (".kind::tf32
+// [d], [a_tmem], b_desc"); only B is read from shared memory.
+//
+// Kernel shape (v4): persistent, one CTA per SM, tiles of 128 x BN, 14 warps:
 //   warp 0 lane 0   TMA producer (A fp32 tile; B as hi/lo pair or fp32 tile) into a STAGES ring
 //   warp 1 lane 0   MMA issuer (single thread, tcgen05.mma + tcgen05.commit); warp 1 owns TMEM
-//   warps 2-5       transform: hi = tf32_rn(x) in place, lo = x - hi into the stage's lo slot
+//   warps 2-5       transform: thread = row of A -> tf32 hi/lo into one of NSLOT TMEM slots
+//                   (tcgen05.st); a plain-fp32 B tile is split in smem (hi in place, lo alongside)
 //   warps 6-13      epilogue: TMEM lane quarter q = warp % 4, column half h = (warp - 6) / 4.
 //                   Every 128 of K the TMEM partial (NACC buffers of BN columns, rotating across
 //                   tiles, so the MMAs of the next tile overlap this epilogue) is added into fp32
@@ -46,26 +52,31 @@ template <int BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // A(hi), A_lo, B_hi, B_lo
+  static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // A (fp32), B_hi, B_lo
   static constexpr int EPI_BYTES = kEpiWarps * kEpiBox;
   static constexpr int BAR_BYTES = 512;
   static constexpr int STAGES_RAW = (kMaxSmem - 1024 - EPI_BYTES - BAR_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
-  static constexpr int NACC = 4;                       // TMEM accumulator buffers
-  static constexpr int TMEM_COLS = NACC * BN;          // 512 / 256 / 128
+  static constexpr int NACC = 2;                       // TMEM accumulator buffers (BN columns each)
+  static constexpr int NSLOT = 4;                      // TMEM A slots (hi: 32 columns, lo: 32 columns)
+  static constexpr int ASLOT0 = NACC * BN;             // first TMEM column of the A slots
+  static constexpr int TMEM_COLS = 512;
   static constexpr int EPI_SPLIT = BN >= 64 ? 2 : 1;   // epilogue warps per TMEM lane quarter
   static constexpr int CW = BN / EPI_SPLIT;            // columns per epilogue thread
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
   static_assert(STAGES >= 2, "smem");
   static_assert(SMEM_BYTES <= kMaxSmem, "smem");
   static_assert(CW % 32 == 0, "epilogue box");
+  static_assert(ASLOT0 + 64 * NSLOT <= TMEM_COLS, "tmem");
 };
 
 struct KParams {
   int M, N, K, batch, splits, kb_per_split, passes, epi, act;
   int mt, nt, ntiles;
   int a_pz, b_pz;  // 1: operand batched over particles; 0: shared (particle coordinate 0)
-  int dbg;         // debug experiments only (pushdbg_gemm): bit 0 = skip the hi/lo transform
+  int dbg;         // debug experiments only (pushdbg_gemm): bit 0 raw fp32 operands (no hi/lo split),
+                   // bit 1 skip the epilogue math/stores, bit 2 skip the MMAs (commits only),
+                   // bit 3 accumulate the whole K in TMEM (no fp32 promotion)
   const float* bias;
   long long bias_pstride;
   float* bpart;
@@ -103,17 +114,19 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t base, int ks) {
     return ptx::umma_desc(base + ks * 1024, 4096, 512, 1);
 }
 
-// hi = tf32_rn(x) in place, lo = x - hi at `lo` (elementwise, so layout-agnostic; shared addresses).
+// B split on the staged tile: the tensor core TRUNCATES fp32 operands to tf32 (measured on B200 by
+// scripts/tf32_probe.py: the raw-operand product matches truncated inputs to fp32 rounding and
+// differs from round-to-nearest inputs by ~1e-3 relative), so the staged fp32 x already IS hi =
+// trunc_tf32(x); only lo = x - trunc_tf32(x) (exact in fp32, |lo| < 2^-10 |x|) is written.
 __device__ __forceinline__ void split_tile(uint32_t base, uint32_t lo, int bytes, int tx) {
 #pragma unroll 4
   for (int i = tx * 16; i < bytes; i += kXfThreads * 16) {
     const float4 v = ptx::lds_f4(base + i);
-    float4 h, l;
-    h.x = ptx::tf32_rna_fast(v.x); l.x = v.x - h.x;
-    h.y = ptx::tf32_rna_fast(v.y); l.y = v.y - h.y;
-    h.z = ptx::tf32_rna_fast(v.z); l.z = v.z - h.z;
-    h.w = ptx::tf32_rna_fast(v.w); l.w = v.w - h.w;
-    ptx::sts_f4(base + i, h);
+    float4 l;
+    l.x = v.x - ptx::tf32_trunc(v.x);
+    l.y = v.y - ptx::tf32_trunc(v.y);
+    l.z = v.z - ptx::tf32_trunc(v.z);
+    l.w = v.w - ptx::tf32_trunc(v.w);
     ptx::sts_f4(lo + i, l);
   }
 }
@@ -153,7 +166,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(ebuf_all + C::EPI_BYTES);
   uint64_t* ready = full + C::STAGES;
   uint64_t* empty = ready + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;   // [NACC] accumulator b holds a finished K-chunk
+  uint64_t* aempty = empty + C::STAGES;  // [NSLOT] the MMAs reading TMEM A slot j have completed
+  uint64_t* tfull = aempty + C::NSLOT;   // [NACC] accumulator b holds a finished K-chunk
   uint64_t* tempty = tfull + C::NACC;    // [NACC] accumulator b has been drained to registers
   uint64_t* auxbar = tempty + C::NACC;   // [kEpiWarps] aprev box landed in the warp's smem box
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + kEpiWarps);
@@ -167,6 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&ready[s], kXfThreads);
       ptx::mbar_init(&empty[s], 1);
     }
+    for (int j = 0; j < C::NSLOT; ++j) ptx::mbar_init(&aempty[j], 1);
     for (int b = 0; b < C::NACC; ++b) {
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], 32 * 4 * C::EPI_SPLIT);
@@ -211,47 +226,49 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_arrive_expect_tx(&full[s], kTx);
           const int k = (kb0 + i) * BK;
           load_operand<AMN, BM>(&tA, st, &full[s], tc.m0, k, tc.p * prm.a_pz);
-          load_operand<BMN, BN>(&tBhi, st + 2 * C::A_BYTES, &full[s], n0, k, tc.p * prm.b_pz);
-          if (!BSPLIT) load_operand<BMN, BN>(&tBlo, st + 2 * C::A_BYTES + C::B_BYTES, &full[s], n0, k, tc.p * prm.b_pz);
+          load_operand<BMN, BN>(&tBhi, st + C::A_BYTES, &full[s], n0, k, tc.p * prm.b_pz);
+          if (!BSPLIT) load_operand<BMN, BN>(&tBlo, st + C::A_BYTES + C::B_BYTES, &full[s], n0, k, tc.p * prm.b_pz);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer: K-chunks of kChunkKB k-blocks rotate over NACC TMEM accumulators
-      constexpr uint32_t idesc = ptx::idesc_tf32(BM, BN, AMN, BMN);
+      constexpr uint32_t idesc = ptx::idesc_tf32(BM, BN, false, BMN);  // A from TMEM (K along columns)
       uint32_t it = 0, ch = 0;
       for (int t = blockIdx.x; t < prm.ntiles; t += gridDim.x) {
         TileCoord tc = decode(t, prm);
         int kb0;
         const int nkb = tile_kb(tc.split, &kb0);
         for (int i = 0; i < nkb; ++i, ++it) {
-          const bool first = (i % kChunkKB) == 0;
-          const bool last = (i % kChunkKB) == kChunkKB - 1 || i == nkb - 1;
+          const int ckb = (prm.dbg & 8) ? nkb : kChunkKB;  // experiment: one chunk = no fp32 promotion
+          const bool first = (i % ckb) == 0;
+          const bool last = (i % ckb) == ckb - 1 || i == nkb - 1;
           const int b = ch % C::NACC;
           if (first) ptx::mbar_wait(&tempty[b], ((ch / C::NACC) & 1) ^ 1);
           const int s = it % C::STAGES;
+          const int slot = it % C::NSLOT;
           ptx::mbar_wait(&ready[s], (it / C::STAGES) & 1);
           ptx::tc_fence_after();
-          const uint32_t a_hi = ptx::smem_u32(smem + s * C::STAGE_BYTES);
-          const uint32_t a_lo = a_hi + C::A_BYTES;
-          const uint32_t b_hi = a_hi + 2 * C::A_BYTES;
+          const uint32_t b_hi = ptx::smem_u32(smem + s * C::STAGE_BYTES) + C::A_BYTES;
           const uint32_t b_lo = b_hi + C::B_BYTES;
+          const uint32_t ta_hi = tmem_base + C::ASLOT0 + slot * 64, ta_lo = ta_hi + 32;
           const uint32_t d = tmem_base + b * BN;
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {
-            const uint64_t dah = op_desc<AMN>(a_hi, ks), dal = op_desc<AMN>(a_lo, ks);
             const uint64_t dbh = op_desc<BMN>(b_hi, ks), dbl = op_desc<BMN>(b_lo, ks);
             const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-            if (prm.passes == 3) {
-              ptx::mma_tf32(d, dal, dbh, idesc, acc);  // small terms first
-              ptx::mma_tf32(d, dah, dbl, idesc, 1u);
-              ptx::mma_tf32(d, dah, dbh, idesc, 1u);
+            if (prm.dbg & 4) {
+            } else if (prm.passes == 3) {
+              ptx::mma_tf32_ts(d, ta_lo + ks * 8, dbh, idesc, acc);  // small terms first
+              ptx::mma_tf32_ts(d, ta_hi + ks * 8, dbl, idesc, 1u);
+              ptx::mma_tf32_ts(d, ta_hi + ks * 8, dbh, idesc, 1u);
             } else {
-              ptx::mma_tf32(d, dah, dbh, idesc, acc);
+              ptx::mma_tf32_ts(d, ta_hi + ks * 8, dbh, idesc, acc);
             }
           }
-          ptx::mma_commit(&empty[s]);  // frees the smem stage when these MMAs complete
+          ptx::mma_commit(&empty[s]);      // frees the smem stage when these MMAs complete
+          ptx::mma_commit(&aempty[slot]);  // frees the TMEM A slot
           if (last) {
             ptx::mma_commit(&tfull[b]);
             ++ch;
@@ -260,8 +277,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp < kEpiWarp0) {
-    // ---------------- transform warps: split the staged fp32 tiles into tf32 hi (in place) + lo
+    // ---------------- transform warps: A tile -> tf32 hi/lo in a TMEM slot (thread = row of A);
+    // a plain-fp32 B tile is split in smem (hi in place, lo into the B_lo slot)
     const int tx = threadIdx.x - 32 * kXfWarp0;
+    const int q = warp & 3;                  // TMEM lane quarter = rows 32q .. 32q+31 of the A tile
+    const int m = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     uint32_t it = 0;
     for (int t = blockIdx.x; t < prm.ntiles; t += gridDim.x) {
       TileCoord tc = decode(t, prm);
@@ -269,13 +290,49 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nkb = tile_kb(tc.split, &kb0);
       for (int i = 0; i < nkb; ++i, ++it) {
         const int s = it % C::STAGES;
+        const int slot = it % C::NSLOT;
         ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
+        ptx::mbar_wait(&aempty[slot], ((it / C::NSLOT) & 1) ^ 1);
+        ptx::tc_fence_after();
         const uint32_t st = ptx::smem_u32(smem + s * C::STAGE_BYTES);
-        if (!(prm.dbg & 1)) {
-          split_tile(st, st + C::A_BYTES, C::A_BYTES, tx);
-          if (BSPLIT) split_tile(st + 2 * C::A_BYTES, st + 2 * C::A_BYTES + C::B_BYTES, C::B_BYTES, tx);
+        uint32_t hi[32], lo[32];
+        if constexpr (!AMN) {
+          // K-major SWIZZLE_128B: row m is 128 B at m*128, 16-B chunk c stored at chunk c ^ (m % 8)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 v = ptx::lds_f4(st + m * 128 + ((c ^ (m & 7)) << 4));
+            const float xv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float h = ptx::tf32_rna_fast(xv[u]);
+              hi[4 * c + u] = __float_as_uint(h);
+              lo[4 * c + u] = __float_as_uint(xv[u] - h);
+            }
+          }
+        } else {
+          // MN-major, unswizzled boxes [32 k][32 m] per 32-row chunk: element (k, m) at q*4096 + k*128 + lane*4
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float x = ptx::lds_f32(st + q * 4096 + k * 128 + lane * 4);
+            const float h = ptx::tf32_rna_fast(x);
+            hi[k] = __float_as_uint(h);
+            lo[k] = __float_as_uint(x - h);
+          }
         }
-        ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core (async proxy)
+        if (prm.dbg & 1) {  // experiment: hand the raw fp32 bits to the tensor core (lo = 0, B unsplit)
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            hi[k] = __float_as_uint(__uint_as_float(hi[k]) + __uint_as_float(lo[k]));
+            lo[k] = 0u;
+          }
+        }
+        const uint32_t ta = tmem_base + lane_off + C::ASLOT0 + slot * 64;
+        ptx::tmem_st_32x32b_x32(ta, hi);
+        ptx::tmem_st_32x32b_x32(ta + 32, lo);
+        if (BSPLIT && !(prm.dbg & 1)) split_tile(st + C::A_BYTES, st + C::A_BYTES + C::B_BYTES, C::B_BYTES, tx);
+        ptx::tmem_st_wait();
+        ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+        ptx::tc_fence_before();
         ptx::mbar_arrive(&ready[s]);
       }
     }
@@ -295,7 +352,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n0 = tc.nt * BN;
         int kb0;
         const int nkb = tile_kb(tc.split, &kb0);
-        const int nchunks = (nkb + kChunkKB - 1) / kChunkKB;
+        const int ckb = (prm.dbg & 8) ? nkb : kChunkKB;
+        const int nchunks = (nkb + ckb - 1) / ckb;
         const int row0 = tc.m0 + q * 32;
         const bool live = row0 < prm.M;
         const int colw = n0 + h * C::CW;
@@ -324,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tc_fence_before();
           ptx::mbar_arrive(&tempty[b]);
         }
-        if (!live) continue;
+        if (!live || (prm.dbg & 2)) continue;
         const int pz = prm.epi == EPI_STORE ? tc.split * prm.batch + tc.p : tc.p;
         // Output in 16-column groups g, double-buffered: group g is staged in half-box (g & 1)
         // (32 rows x 16 fp32, SWIZZLE_64B: 16-B chunk c of row r sits at chunk c ^ ((r >> 1) & 3)),
@@ -466,12 +524,15 @@ push_status make_map(CUtensorMap* m, const float* base, uint64_t d0, uint64_t d1
   return PUSH_OK;
 }
 
+// B operands are staged in UMMA-canonical swizzled layouts; the A operand only feeds the transform
+// warps (which write it to TMEM), so an MN-major A is staged unswizzled for conflict-free column reads.
 push_status make_operand_map(const float* ptr, const Operand& op, int mn_extent, int K, int batch, int box_rows,
-                             CUtensorMap* m) {
+                             CUtensorMap* m, bool is_a) {
   const int b = op.pstride == 0 ? 1 : batch;
   if (!op.mn_major)
     return make_map(m, ptr, K, mn_extent, b, op.ld, op.pstride, box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
-  return make_map(m, ptr, mn_extent, K, b, op.ld, op.pstride, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  return make_map(m, ptr, mn_extent, K, b, op.ld, op.pstride, 32,
+                  is_a ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
 template <int BN, bool AMN, bool BMN, bool BS>
@@ -533,11 +594,11 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   if ((nkb + kbps - 1) / kbps != pb.splits) return fail(PUSH_E_SHAPE, "gemm: split count leaves an empty split");
   CUtensorMap maps[5];
   std::memset(maps, 0, sizeof(maps));
-  if ((st = make_operand_map(pb.A.hi, pb.A, pb.M, pb.K, pb.batch, BM, &maps[0])) != PUSH_OK) return st;
-  if ((st = make_operand_map(pb.B.hi, pb.B, pb.N, pb.K, pb.batch, BN, &maps[1])) != PUSH_OK) return st;
+  if ((st = make_operand_map(pb.A.hi, pb.A, pb.M, pb.K, pb.batch, BM, &maps[0], true)) != PUSH_OK) return st;
+  if ((st = make_operand_map(pb.B.hi, pb.B, pb.N, pb.K, pb.batch, BN, &maps[1], false)) != PUSH_OK) return st;
   if (!pb.B.split) {
     if (!pb.B.lo) return fail(PUSH_E_INVALID, "gemm: pre-split B needs lo");
-    if ((st = make_operand_map(pb.B.lo, pb.B, pb.N, pb.K, pb.batch, BN, &maps[2])) != PUSH_OK) return st;
+    if ((st = make_operand_map(pb.B.lo, pb.B, pb.N, pb.K, pb.batch, BN, &maps[2], false)) != PUSH_OK) return st;
   }
   const int nout = pb.epi == EPI_STORE ? pb.splits * pb.batch : pb.batch;
   if ((st = make_map(&maps[3], pb.out, pb.N, pb.M, nout, pb.ldo, pb.out_pstride, 32, CU_TENSOR_MAP_SWIZZLE_64B,
