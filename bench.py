@@ -51,8 +51,8 @@ def load_peaks():
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, ws, local
 
@@ -182,20 +182,16 @@ def run_reference(args, w):
 # ---------------------------------------------------------------------------- our path
 def run_ours(args, w):
     import torch
-    import torch.distributed as dist
 
+    from paper_2306_06528_b200 import dist as pdist
     from paper_2306_06528_b200 import push
 
     rank, ws, local = dist_env()
     assert ws == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={ws}"
     torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        obj = [push.get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
-    else:
-        nid = None
+    dev = torch.device("cuda", local)
+    pdist.init("nccl", dev)
+    nid = pdist.bootstrap_nccl_id(rank, ws)
     dims = list(w.dims)
     cfg = push.make_config(w.n_particles, dims, max_batch=w.batch, step_size=1e-3, seed=0)
     ctx = push.Context(cfg, rank, ws, nid)
@@ -206,16 +202,11 @@ def run_ours(args, w):
     stream = torch.cuda.current_stream()
 
     def barrier():
-        if ws > 1:
-            dist.barrier()
+        pdist.barrier(ws)
         torch.cuda.synchronize()
 
     def maxall(v):
-        if ws == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return pdist.max_over_ranks(v, ws, dev)
 
     for s in range(args.warmup):
         ctx.particle_grads(xs[s], ys[s])
@@ -264,8 +255,7 @@ def run_ours(args, w):
 
     if rank != 0:
         ctx.close()
-        if ws > 1:
-            dist.destroy_process_group()
+        pdist.finalize(ws)
         return
 
     peaks, peak_kind = load_peaks()
@@ -308,8 +298,7 @@ def run_ours(args, w):
         line["cpu_baseline"] = cpu_baseline(w)
     print(json.dumps(line), flush=True)
     ctx.close()
-    if ws > 1:
-        dist.destroy_process_group()
+    pdist.finalize(ws)
 
 
 def main():
