@@ -28,6 +28,7 @@
 //                   applied on double-buffered swizzled 32x16 smem boxes per warp, written with TMA stores.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -151,6 +152,107 @@ __device__ __forceinline__ TileCoord decode(int t, const KParams& prm) {
   c.nt = nt;
   return c;
 }
+
+// Fused epilogue of one 32-row x CW-column slab held in registers (acc), written through the
+// warp's double-buffered swizzled 32x16 smem half-boxes with TMA stores (see the v3 notes above).
+// aux_ph: parity of the warp's aprev barrier (BWD); the aprev box of group 0 must already be in flight.
+template <int CW>
+__device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& prm, const CUtensorMap* tOut,
+                                         const CUtensorMap* tAux, uint64_t* auxbar, uint32_t& aux_ph,
+                                         uint32_t ebuf_s, int lane, int row0, int colw, int p, int pz) {
+  const bool bwd = prm.epi == EPI_BWD;
+        // Output in 16-column groups g, double-buffered: group g is staged in half-box (g & 1)
+        // (32 rows x 16 fp32, SWIZZLE_64B: 16-B chunk c of row r sits at chunk c ^ ((r >> 1) & 3)),
+        // so the TMA store of group g overlaps the math of group g + 1.
+        constexpr int G = CW / 16;
+        const uint32_t roff = lane * 64;
+        const int swz = (lane >> 1) & 3;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int col = colw + g * 16;
+          const uint32_t buf = ebuf_s + (g & 1) * kHalfBox;
+          if (bwd) {
+            ptx::mbar_wait(auxbar, aux_ph);  // aprev of group g has landed in buf
+            aux_ph ^= 1;
+          } else {
+            if (lane == 0) ptx::bulk_wait_read1();  // the store of group g - 2 has finished reading buf
+            __syncwarp();
+          }
+          if (prm.epi == EPI_FWD) {
+            const float* bias = prm.bias + p * prm.bias_pstride + col;  // b_l need not be 16-B aligned
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const float4 bv = make_float4(__ldg(bias + 4 * c4), __ldg(bias + 4 * c4 + 1), __ldg(bias + 4 * c4 + 2),
+                                            __ldg(bias + 4 * c4 + 3));
+              float4 v;
+              v.x = act_fwd(acc[g * 16 + 4 * c4 + 0] + bv.x, prm.act);
+              v.y = act_fwd(acc[g * 16 + 4 * c4 + 1] + bv.y, prm.act);
+              v.z = act_fwd(acc[g * 16 + 4 * c4 + 2] + bv.z, prm.act);
+              v.w = act_fwd(acc[g * 16 + 4 * c4 + 3] + bv.w, prm.act);
+              ptx::sts_f4(buf + roff + ((c4 ^ swz) << 4), v);
+            }
+          } else if (bwd) {
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const uint32_t pp = buf + roff + ((c4 ^ swz) << 4);
+              const float4 a = ptx::lds_f4(pp);
+              float4 v;
+              v.x = acc[g * 16 + 4 * c4 + 0] * act_deriv_from_a(a.x, prm.act);
+              v.y = acc[g * 16 + 4 * c4 + 1] * act_deriv_from_a(a.y, prm.act);
+              v.z = acc[g * 16 + 4 * c4 + 2] * act_deriv_from_a(a.z, prm.act);
+              v.w = acc[g * 16 + 4 * c4 + 3] * act_deriv_from_a(a.w, prm.act);
+              ptx::sts_f4(pp, v);
+            }
+          } else {
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4)
+              ptx::sts_f4(buf + roff + ((c4 ^ swz) << 4),
+                          make_float4(acc[g * 16 + 4 * c4], acc[g * 16 + 4 * c4 + 1], acc[g * 16 + 4 * c4 + 2],
+                                      acc[g * 16 + 4 * c4 + 3]));
+          }
+          __syncwarp();
+          if (bwd && prm.bpart) {
+            // a5 of the layer below: column partial sums of delta over this warp's 32 rows (rows >= M are
+            // zero: their A rows were zero-filled by TMA).  Lane l: column l & 15, rows 16*(l >> 4) + 0..15
+            // ascending, then the two halves added (commutative, so both lanes get the same bits).
+            const int rb = row0 / 32;
+            const int cl = lane & 15, r0 = (lane >> 4) * 16;
+            float v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r)
+              v[r] = ptx::lds_f32(buf + (r0 + r) * 64 + ((((cl >> 2) ^ (((r0 + r) >> 1) & 3)) << 4) | ((cl & 3) << 2)));
+            float sm = 0.f;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) sm += v[r];
+            sm += __shfl_xor_sync(0xffffffffu, sm, 16);
+            if (lane < 16) prm.bpart[rb * prm.bp_sstride + p * prm.bp_pstride + col + cl] = sm;
+            for (int i = 0; i < prm.din; ++i) {
+              float sx = 0.f;
+#pragma unroll
+              for (int r = 0; r < 16; ++r) {
+                const int row = row0 + r0 + r;
+                const float xv = row < prm.M ? __ldg(prm.x + (long long)row * prm.din + i) : 0.f;
+                sx = fmaf(v[r], xv, sx);
+              }
+              sx += __shfl_xor_sync(0xffffffffu, sx, 16);
+              if (lane < 16)
+                prm.xpart[rb * prm.xp_sstride + p * prm.xp_pstride + (long long)(col + cl) * prm.din + i] = sx;
+            }
+          }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_3d(tOut, ptx_ptr(buf), col, row0, pz);
+            ptx::bulk_commit();
+            if (bwd && g + 1 < G) {  // prefetch aprev of group g + 1 once the store of group g - 1 has read it
+              ptx::bulk_wait_read1();
+              const uint32_t nb = ebuf_s + ((g + 1) & 1) * kHalfBox;
+              ptx::mbar_arrive_expect_tx(auxbar, kHalfBox);
+              ptx::tma_load_3d(ptx_ptr(nb), tAux, auxbar, col + 16, row0, p);
+            }
+          }
+        }
+      }
 
 template <int BN, bool AMN, bool BMN, bool BSPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -384,97 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!live || (prm.dbg & 2)) continue;
         const int pz = prm.epi == EPI_STORE ? tc.split * prm.batch + tc.p : tc.p;
-        // Output in 16-column groups g, double-buffered: group g is staged in half-box (g & 1)
-        // (32 rows x 16 fp32, SWIZZLE_64B: 16-B chunk c of row r sits at chunk c ^ ((r >> 1) & 3)),
-        // so the TMA store of group g overlaps the math of group g + 1.
-        constexpr int G = C::CW / 16;
-        const uint32_t roff = lane * 64;
-        const int swz = (lane >> 1) & 3;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const int col = colw + g * 16;
-          const uint32_t buf = ebuf_s + (g & 1) * kHalfBox;
-          if (bwd) {
-            ptx::mbar_wait(&auxbar[e], aux_ph);  // aprev of group g has landed in buf
-            aux_ph ^= 1;
-          } else {
-            if (lane == 0) ptx::bulk_wait_read1();  // the store of group g - 2 has finished reading buf
-            __syncwarp();
-          }
-          if (prm.epi == EPI_FWD) {
-            const float* bias = prm.bias + tc.p * prm.bias_pstride + col;  // b_l need not be 16-B aligned
-#pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {
-              const float4 bv = make_float4(__ldg(bias + 4 * c4), __ldg(bias + 4 * c4 + 1), __ldg(bias + 4 * c4 + 2),
-                                            __ldg(bias + 4 * c4 + 3));
-              float4 v;
-              v.x = act_fwd(acc[g * 16 + 4 * c4 + 0] + bv.x, prm.act);
-              v.y = act_fwd(acc[g * 16 + 4 * c4 + 1] + bv.y, prm.act);
-              v.z = act_fwd(acc[g * 16 + 4 * c4 + 2] + bv.z, prm.act);
-              v.w = act_fwd(acc[g * 16 + 4 * c4 + 3] + bv.w, prm.act);
-              ptx::sts_f4(buf + roff + ((c4 ^ swz) << 4), v);
-            }
-          } else if (bwd) {
-#pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {
-              const uint32_t pp = buf + roff + ((c4 ^ swz) << 4);
-              const float4 a = ptx::lds_f4(pp);
-              float4 v;
-              v.x = acc[g * 16 + 4 * c4 + 0] * act_deriv_from_a(a.x, prm.act);
-              v.y = acc[g * 16 + 4 * c4 + 1] * act_deriv_from_a(a.y, prm.act);
-              v.z = acc[g * 16 + 4 * c4 + 2] * act_deriv_from_a(a.z, prm.act);
-              v.w = acc[g * 16 + 4 * c4 + 3] * act_deriv_from_a(a.w, prm.act);
-              ptx::sts_f4(pp, v);
-            }
-          } else {
-#pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4)
-              ptx::sts_f4(buf + roff + ((c4 ^ swz) << 4),
-                          make_float4(acc[g * 16 + 4 * c4], acc[g * 16 + 4 * c4 + 1], acc[g * 16 + 4 * c4 + 2],
-                                      acc[g * 16 + 4 * c4 + 3]));
-          }
-          __syncwarp();
-          if (bwd && prm.bpart) {
-            // a5 of the layer below: column partial sums of delta over this warp's 32 rows (rows >= M are
-            // zero: their A rows were zero-filled by TMA).  Lane l: column l & 15, rows 16*(l >> 4) + 0..15
-            // ascending, then the two halves added (commutative, so both lanes get the same bits).
-            const int rb = row0 / 32;
-            const int cl = lane & 15, r0 = (lane >> 4) * 16;
-            float v[16];
-#pragma unroll
-            for (int r = 0; r < 16; ++r)
-              v[r] = ptx::lds_f32(buf + (r0 + r) * 64 + ((((cl >> 2) ^ (((r0 + r) >> 1) & 3)) << 4) | ((cl & 3) << 2)));
-            float sm = 0.f;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) sm += v[r];
-            sm += __shfl_xor_sync(0xffffffffu, sm, 16);
-            if (lane < 16) prm.bpart[rb * prm.bp_sstride + tc.p * prm.bp_pstride + col + cl] = sm;
-            for (int i = 0; i < prm.din; ++i) {
-              float sx = 0.f;
-#pragma unroll
-              for (int r = 0; r < 16; ++r) {
-                const int row = row0 + r0 + r;
-                const float xv = row < prm.M ? __ldg(prm.x + (long long)row * prm.din + i) : 0.f;
-                sx = fmaf(v[r], xv, sx);
-              }
-              sx += __shfl_xor_sync(0xffffffffu, sx, 16);
-              if (lane < 16)
-                prm.xpart[rb * prm.xp_sstride + tc.p * prm.xp_pstride + (long long)(col + cl) * prm.din + i] = sx;
-            }
-          }
-          ptx::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            ptx::tma_store_3d(&tOut, ptx_ptr(buf), col, row0, pz);
-            ptx::bulk_commit();
-            if (bwd && g + 1 < G) {  // prefetch aprev of group g + 1 once the store of group g - 1 has read it
-              ptx::bulk_wait_read1();
-              const uint32_t nb = ebuf_s + ((g + 1) & 1) * kHalfBox;
-              ptx::mbar_arrive_expect_tx(&auxbar[e], kHalfBox);
-              ptx::tma_load_3d(ptx_ptr(nb), &tAux, &auxbar[e], col + 16, row0, tc.p);
-            }
-          }
-        }
+        epi_tile<C::CW>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, tc.p, pz);
       }
       if (lane == 0) ptx::bulk_wait0();
     }
@@ -482,6 +494,284 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 1) ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
+}
+
+
+// ================================================================== v5: CTA-pair kernel (cta_group::2)
+// Tiles of 256 x 256 per CTA pair (a 2-CTA cluster): CTA r stages rows [128r, 128r+128) of A (split
+// into its own TMEM) and rows [128r, 128r+128) of the B tile; the leader (r = 0) issues
+// tcgen05.mma.cta_group::2 (M = 256, N = 256), each CTA's TMEM receives its 128 x 256 slab of D.
+// Per SM and k-block this halves the B bytes fetched from L2 and staged in smem relative to the
+// 1-CTA kernel at the same MMA work, which is what bounds the 1-CTA kernel.
+//   warpgroup 0: warp 0 lane 0 TMA producer; warp 1 lane 0 MMA issuer (leader only), warp 1 owns TMEM
+//   warpgroup 1: transform (thread = row of A -> TMEM slot; B lo split in smem when B is plain fp32)
+//   warpgroups 2-3: epilogue, 128 accumulator columns per thread (setmaxnreg moves registers there)
+// Cross-CTA signalling: transform and epilogue warps of both CTAs arrive on the LEADER's ready /
+// tempty barriers (mapa + release.cluster); the leader's commits multicast to both CTAs' empty,
+// aempty and tfull barriers.
+constexpr int k2Warps = 16, k2Threads = 32 * k2Warps;
+constexpr int k2XfWarp0 = 4, k2EpiWarp0 = 8;
+constexpr int k2BN = 256, k2CW = 128;
+
+struct Cfg2 {
+  static constexpr int A_BYTES = BM * BK * 4;
+  static constexpr int B_BYTES = (k2BN / 2) * BK * 4;
+  static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;
+  static constexpr int EPI_BYTES = kEpiWarps * kEpiBox;
+  static constexpr int BAR_BYTES = 512;
+  static constexpr int STAGES_RAW = (kMaxSmem - 1024 - EPI_BYTES - BAR_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+  static constexpr int NSLOT = 4;
+  static constexpr int ASLOT0 = k2BN;  // accumulator: columns [0, 256); A slots: [256, 512)
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
+  static_assert(STAGES >= 2 && SMEM_BYTES <= kMaxSmem, "smem");
+};
+
+template <bool AMN, bool BMN, bool BSPLIT>
+__global__ void __launch_bounds__(k2Threads, 1)
+    gemm3xtf32_2sm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tBhi,
+                          const __grid_constant__ CUtensorMap tBlo, const __grid_constant__ CUtensorMap tOut,
+                          const __grid_constant__ CUtensorMap tAux, const KParams prm) {
+  using C = Cfg2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* ebuf_all = smem + C::STAGES * C::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ebuf_all + C::EPI_BYTES);
+  uint64_t* ready = full + C::STAGES;     // leader: both CTAs' transforms done with stage s
+  uint64_t* empty = ready + C::STAGES;    // the pair's MMAs reading stage s have completed
+  uint64_t* aempty = empty + C::STAGES;   // [NSLOT] the MMAs reading TMEM A slot j have completed
+  uint64_t* tfull = aempty + C::NSLOT;    // the accumulator holds a finished K-chunk
+  uint64_t* tempty = tfull + 1;           // leader: both CTAs have drained the accumulator
+  uint64_t* auxbar = tempty + 1;          // [kEpiWarps]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + kEpiWarps);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = ptx::cluster_ctarank();
+  const int nkb_total = (prm.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&ready[s], 2 * 4);  // one arrival per transform warp of each CTA
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int j = 0; j < C::NSLOT; ++j) ptx::mbar_init(&aempty[j], 1);
+    ptx::mbar_init(tfull, 1);
+    ptx::mbar_init(tempty, 2 * kEpiWarps);  // one arrival per epilogue warp of each CTA
+    for (int e = 0; e < kEpiWarps; ++e) ptx::mbar_init(&auxbar[e], 1);
+    ptx::fence_mbar_init();
+    ptx::prefetch_tmap(&tA);
+    ptx::prefetch_tmap(&tBhi);
+    if (!BSPLIT) ptx::prefetch_tmap(&tBlo);
+    ptx::prefetch_tmap(&tOut);
+    if (prm.epi == EPI_BWD) ptx::prefetch_tmap(&tAux);
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc2(tmem_slot, C::TMEM_COLS);
+    ptx::tmem_relinquish2();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();  // the peer's barriers are initialised before any remote arrive
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = ptx::lds_u32(ptx::smem_u32(tmem_slot));
+
+  const int cid = (int)ptx::cluster_id_x(), ncl = (int)ptx::ncluster_x();
+  auto tile_kb = [&](int split, int* kb0) {
+    *kb0 = split * prm.kb_per_split;
+    return min(nkb_total, *kb0 + prm.kb_per_split) - *kb0;
+  };
+  // pair tile t -> (particle, split, 256-row block, 256-column block)
+  auto decode2 = [&](int t, int* p, int* split, int* mp, int* nt) {
+    *nt = t % prm.nt;
+    t /= prm.nt;
+    *mp = t % prm.mt;
+    t /= prm.mt;
+    *split = t % prm.splits;
+    *p = t / prm.splits;
+  };
+
+  // setmaxnreg sits at the top of each role's branch so ptxas allocates that region to the new limit
+  // (warpgroup 0: producer + MMA issuer + 2 idle warps -> 40; transform -> 104; epilogue -> 184).
+  if (warp == 0) {
+    ptx::setmaxnreg_dec<40>();
+    if (lane == 0) {
+      // ---------------- TMA producer (each CTA: its A rows and its half of the B tile)
+      constexpr uint32_t kTx = C::A_BYTES + (BSPLIT ? C::B_BYTES : 2 * C::B_BYTES);
+      uint32_t it = 0;
+      for (int t = cid; t < prm.ntiles; t += ncl) {
+        int p, split, mp, nt;
+        decode2(t, &p, &split, &mp, &nt);
+        const int m0 = mp * 256 + (int)crank * 128;
+        const int nb0 = nt * k2BN + (int)crank * (k2BN / 2);
+        int kb0;
+        const int nkb = tile_kb(split, &kb0);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const int s = it % C::STAGES;
+          ptx::mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+          uint8_t* st = smem + s * C::STAGE_BYTES;
+          ptx::mbar_arrive_expect_tx(&full[s], kTx);
+          const int k = (kb0 + i) * BK;
+          load_operand<AMN, BM>(&tA, st, &full[s], m0, k, p * prm.a_pz);
+          load_operand<BMN, k2BN / 2>(&tBhi, st + C::A_BYTES, &full[s], nb0, k, p * prm.b_pz);
+          if (!BSPLIT)
+            load_operand<BMN, k2BN / 2>(&tBlo, st + C::A_BYTES + C::B_BYTES, &full[s], nb0, k, p * prm.b_pz);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    ptx::setmaxnreg_dec<40>();
+    if (lane == 0 && crank == 0) {
+      // ---------------- MMA issuer (leader): M = 256 across the pair, N = 256
+      constexpr uint32_t idesc = ptx::idesc_tf32(256, k2BN, false, BMN);
+      uint32_t it = 0, ch = 0;
+      for (int t = cid; t < prm.ntiles; t += ncl) {
+        int p, split, mp, nt;
+        decode2(t, &p, &split, &mp, &nt);
+        int kb0;
+        const int nkb = tile_kb(split, &kb0);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const bool first = (i % kChunkKB) == 0;
+          const bool last = (i % kChunkKB) == kChunkKB - 1 || i == nkb - 1;
+          if (first) ptx::mbar_wait(tempty, (ch & 1) ^ 1);
+          const int s = it % C::STAGES;
+          const int slot = it % C::NSLOT;
+          ptx::mbar_wait(&ready[s], (it / C::STAGES) & 1);
+          ptx::tc_fence_after();
+          const uint32_t b_hi = ptx::smem_u32(smem + s * C::STAGE_BYTES) + C::A_BYTES;
+          const uint32_t b_lo = b_hi + C::B_BYTES;
+          const uint32_t ta_hi = tmem_base + C::ASLOT0 + slot * 64, ta_lo = ta_hi + 32;
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint64_t dbh = op_desc<BMN>(b_hi, ks), dbl = op_desc<BMN>(b_lo, ks);
+            const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+            if (prm.dbg & 4) {
+            } else if (prm.passes == 3) {
+              ptx::mma2_tf32_ts(tmem_base, ta_lo + ks * 8, dbh, idesc, acc);
+              ptx::mma2_tf32_ts(tmem_base, ta_hi + ks * 8, dbl, idesc, 1u);
+              ptx::mma2_tf32_ts(tmem_base, ta_hi + ks * 8, dbh, idesc, 1u);
+            } else {
+              ptx::mma2_tf32_ts(tmem_base, ta_hi + ks * 8, dbh, idesc, acc);
+            }
+          }
+          ptx::mma2_commit_mc(&empty[s], 3);
+          ptx::mma2_commit_mc(&aempty[slot], 3);
+          if (last) {
+            ptx::mma2_commit_mc(tfull, 3);
+            ++ch;
+          }
+        }
+      }
+    }
+  } else if (warp < k2XfWarp0) {
+    ptx::setmaxnreg_dec<40>();  // idle warps of warpgroup 0
+  } else if (warp < k2EpiWarp0) {
+    // ---------------- transform warps (warpgroup 1: lane quarters 0..3)
+    ptx::setmaxnreg_dec<104>();
+    const int tx = threadIdx.x - 32 * k2XfWarp0;
+    const int q = warp & 3;
+    const int m = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    uint32_t it = 0;
+    for (int t = cid; t < prm.ntiles; t += ncl) {
+      int p, split, mp, nt;
+      decode2(t, &p, &split, &mp, &nt);
+      int kb0;
+      const int nkb = tile_kb(split, &kb0);
+      for (int i = 0; i < nkb; ++i, ++it) {
+        const int s = it % C::STAGES;
+        const int slot = it % C::NSLOT;
+        ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
+        ptx::mbar_wait(&aempty[slot], ((it / C::NSLOT) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t st = ptx::smem_u32(smem + s * C::STAGE_BYTES);
+        uint32_t hi[32], lo[32];
+        if constexpr (!AMN) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 v = ptx::lds_f4(st + m * 128 + ((c ^ (m & 7)) << 4));
+            const float xv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float h = ptx::tf32_rna_fast(xv[u]);
+              hi[4 * c + u] = __float_as_uint(h);
+              lo[4 * c + u] = __float_as_uint(xv[u] - h);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float x = ptx::lds_f32(st + q * 4096 + k * 128 + lane * 4);
+            const float h = ptx::tf32_rna_fast(x);
+            hi[k] = __float_as_uint(h);
+            lo[k] = __float_as_uint(x - h);
+          }
+        }
+        const uint32_t ta = tmem_base + lane_off + C::ASLOT0 + slot * 64;
+        ptx::tmem_st_32x32b_x32(ta, hi);
+        ptx::tmem_st_32x32b_x32(ta + 32, lo);
+        if (BSPLIT) split_tile(st + C::A_BYTES, st + C::A_BYTES + C::B_BYTES, C::B_BYTES, tx);
+        ptx::tmem_st_wait();
+        ptx::fence_proxy_async_smem();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&ready[s]), 0), 1);
+      }
+    }
+  } else {
+    // ---------------- epilogue warps (warpgroups 2-3): quarter q, column half h of the 256 columns
+    ptx::setmaxnreg_inc<184>();  // the 128-column fp32 running sum lives in registers
+    const int e = warp - k2EpiWarp0;
+    const int q = warp & 3;
+    const int h = e >> 2;
+    const uint32_t ebuf_s = ptx::smem_u32(ebuf_all + e * kEpiBox);
+    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(tempty), 0);
+    uint32_t ch = 0, aux_ph = 0;
+    const bool bwd = prm.epi == EPI_BWD;
+    for (int t = cid; t < prm.ntiles; t += ncl) {
+      int p, split, mp, nt;
+      decode2(t, &p, &split, &mp, &nt);
+      int kb0;
+      const int nkb = tile_kb(split, &kb0);
+      const int nchunks = (nkb + kChunkKB - 1) / kChunkKB;
+      const int row0 = mp * 256 + (int)crank * 128 + q * 32;
+      const bool live = row0 < prm.M;
+      const int colw = nt * k2BN + h * k2CW;
+      if (bwd && live && lane == 0) {
+        ptx::bulk_wait_read0();
+        ptx::mbar_arrive_expect_tx(&auxbar[e], kHalfBox);
+        ptx::tma_load_3d(ptx_ptr(ebuf_s), &tAux, &auxbar[e], colw, row0, p);
+      }
+      float acc[k2CW];
+#pragma unroll
+      for (int j = 0; j < k2CW; ++j) acc[j] = 0.f;
+      for (int c = 0; c < nchunks; ++c, ++ch) {
+        ptx::mbar_wait(tfull, ch & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < k2CW; c0 += 16) {
+          uint32_t r[16];
+          ptx::tmem_ld_32x32b_x16(lane_base + h * k2CW + c0, r);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[c0 + j] += __uint_as_float(r[j]);
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader, 1);
+      }
+      if (!live || (prm.dbg & 2)) continue;
+      const int pz = prm.epi == EPI_STORE ? split * prm.batch + p : p;
+      epi_tile<k2CW>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, p, pz);
+    }
+    if (lane == 0) ptx::bulk_wait0();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync();  // no CTA leaves while its peer may still signal it or read its TMEM
+  if (warp == 1) ptx::tmem_dealloc2(tmem_base, C::TMEM_COLS);
 }
 
 // ------------------------------------------------------------------ host side
@@ -565,6 +855,62 @@ push_status launch_bn(bool amn, bool bmn, bool bs, const CUtensorMap* maps, cons
     default: return launch_t<BN, true, true, true>(maps, kp, s);
   }
 }
+template <bool AMN, bool BMN, bool BS>
+push_status launch2_t(const CUtensorMap* maps, const KParams& kp, cudaStream_t stream) {
+  static int max_pairs = 0;
+  auto kern = gemm3xtf32_2sm_kernel<AMN, BMN, BS>;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(k2Threads);
+  cfg.dynamicSmemBytes = Cfg2::SMEM_BYTES;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (!max_pairs) {
+    PUSH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM_BYTES));
+    cfg.gridDim = dim3(g_sms);
+    int n = 0;
+    PUSH_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+    max_pairs = n > 0 ? n : g_sms / 2;
+  }
+  const int pairs = kp.ntiles < max_pairs ? kp.ntiles : max_pairs;
+  cfg.gridDim = dim3(2 * pairs);
+  PUSH_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], kp));
+  return PUSH_OK;
+}
+
+push_status launch2(bool amn, bool bmn, bool bs, const CUtensorMap* maps, const KParams& kp, cudaStream_t s) {
+  const int key = (amn ? 4 : 0) | (bmn ? 2 : 0) | (bs ? 1 : 0);
+  switch (key) {
+    case 0: return launch2_t<false, false, false>(maps, kp, s);
+    case 1: return launch2_t<false, false, true>(maps, kp, s);
+    case 2: return launch2_t<false, true, false>(maps, kp, s);
+    case 3: return launch2_t<false, true, true>(maps, kp, s);
+    case 4: return launch2_t<true, false, false>(maps, kp, s);
+    case 5: return launch2_t<true, false, true>(maps, kp, s);
+    case 6: return launch2_t<true, true, false>(maps, kp, s);
+    default: return launch2_t<true, true, true>(maps, kp, s);
+  }
+}
+
+bool force_1sm() {
+  static const int v = [] {
+    const char* e = getenv("PUSH_GEMM_1SM");
+    return e && *e && *e != '0' ? 1 : 0;
+  }();
+  return v != 0;
+}
+bool force_pair() {
+  static const int v = [] {
+    const char* e = getenv("PUSH_GEMM_PAIR");
+    return e && *e && *e != '0' ? 1 : 0;
+  }();
+  return v != 0;
+}
 }  // namespace
 
 int choose_bn(int N) {
@@ -588,17 +934,24 @@ push_status run(const Problem& pb, cudaStream_t stream) {
     return fail(PUSH_E_INVALID, "gemm: split partials must be [s][p] contiguous");
   push_status st;
   if ((st = get_encoder()) != PUSH_OK) return st;
-  const int BN = choose_bn(pb.N);
+  // CTA-pair kernel for the weight-gradient GEMMs over 256-wide column blocks (measured faster there:
+  // 89 vs 113 us on the C2 shape); the 1-CTA kernel keeps the forward/backward GEMMs, whose fused
+  // epilogues overlap better with its two TMEM accumulators (profiles/r01_gemm.md).  PUSH_GEMM_1SM=1
+  // forces the 1-CTA kernel, PUSH_GEMM_PAIR=1 the pair kernel wherever N % 256 == 0 (A/B comparisons).
+  const bool pair = pb.N % k2BN == 0 && !(pb.passes >> 8 & (1 | 8)) && !force_1sm() &&
+                    (pb.epi == EPI_STORE || force_pair());
+  const int BN = pair ? k2BN : choose_bn(pb.N);
+  const int box_b = pair ? k2BN / 2 : BN;
   const int nkb = (pb.K + BK - 1) / BK;
   const int kbps = (nkb + pb.splits - 1) / pb.splits;
   if ((nkb + kbps - 1) / kbps != pb.splits) return fail(PUSH_E_SHAPE, "gemm: split count leaves an empty split");
   CUtensorMap maps[5];
   std::memset(maps, 0, sizeof(maps));
   if ((st = make_operand_map(pb.A.hi, pb.A, pb.M, pb.K, pb.batch, BM, &maps[0], true)) != PUSH_OK) return st;
-  if ((st = make_operand_map(pb.B.hi, pb.B, pb.N, pb.K, pb.batch, BN, &maps[1], false)) != PUSH_OK) return st;
+  if ((st = make_operand_map(pb.B.hi, pb.B, pb.N, pb.K, pb.batch, box_b, &maps[1], false)) != PUSH_OK) return st;
   if (!pb.B.split) {
     if (!pb.B.lo) return fail(PUSH_E_INVALID, "gemm: pre-split B needs lo");
-    if ((st = make_operand_map(pb.B.lo, pb.B, pb.N, pb.K, pb.batch, BN, &maps[2], false)) != PUSH_OK) return st;
+    if ((st = make_operand_map(pb.B.lo, pb.B, pb.N, pb.K, pb.batch, box_b, &maps[2], false)) != PUSH_OK) return st;
   }
   const int nout = pb.epi == EPI_STORE ? pb.splits * pb.batch : pb.batch;
   if ((st = make_map(&maps[3], pb.out, pb.N, pb.M, nout, pb.ldo, pb.out_pstride, 32, CU_TENSOR_MAP_SWIZZLE_64B,
@@ -613,7 +966,7 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   kp.M = pb.M; kp.N = pb.N; kp.K = pb.K; kp.batch = pb.batch; kp.splits = pb.splits; kp.kb_per_split = kbps;
   kp.passes = pb.passes & 0xff; kp.epi = pb.epi; kp.act = pb.act;
   kp.dbg = pb.passes >> 8;
-  kp.mt = (pb.M + BM - 1) / BM;
+  kp.mt = (pb.M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM);
   kp.nt = pb.N / BN;
   kp.ntiles = kp.mt * kp.nt * pb.splits * pb.batch;
   kp.a_pz = pb.A.pstride == 0 ? 0 : 1;
@@ -622,6 +975,7 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   kp.bpart = pb.bpart; kp.bp_sstride = pb.bp_sstride; kp.bp_pstride = pb.bp_pstride;
   kp.x = pb.x; kp.din = pb.xpart ? pb.din : 0; kp.xpart = pb.xpart;
   kp.xp_sstride = pb.xp_sstride; kp.xp_pstride = pb.xp_pstride;
+  if (pair) return launch2(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
   if (BN == 128) return launch_bn<128>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
   if (BN == 64) return launch_bn<64>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
   return launch_bn<32>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);

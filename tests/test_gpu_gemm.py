@@ -27,7 +27,7 @@ def _mk(batch, M, N, K, a_mn, b_mn, seed):
 @pytest.mark.parametrize("b_split", [0, 1])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 64, 96), (96, 32, 32), (300, 256, 128), (1, 32, 4),
-                                   (640, 128, 1000)])
+                                   (640, 128, 1000), (512, 512, 256), (96, 256, 40), (1000, 768, 512)])
 def test_gemm_3xtf32_matches_fp64(a_mn, b_mn, b_split, M, N, K):
     if a_mn and M % 32:
         pytest.skip("MN-major A needs M % 32 == 0")
