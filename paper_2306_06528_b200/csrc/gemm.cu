@@ -935,11 +935,12 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   push_status st;
   if ((st = get_encoder()) != PUSH_OK) return st;
   // CTA-pair kernel for the weight-gradient GEMMs over 256-wide column blocks (measured faster there:
-  // 89 vs 113 us on the C2 shape); the 1-CTA kernel keeps the forward/backward GEMMs, whose fused
-  // epilogues overlap better with its two TMEM accumulators (profiles/r01_gemm.md).  PUSH_GEMM_1SM=1
+  // 89 vs 113 us on the C2 shape) and for forward/backward GEMMs with K >= 512 (C3: 19.5 -> 15.4 ms
+  // forward); at K = 256 the 1-CTA kernel's two TMEM accumulators overlap the fused epilogue better
+  // (C2 forward 129 vs 150 us) (profiles/r01_gemm.md).  PUSH_GEMM_1SM=1
   // forces the 1-CTA kernel, PUSH_GEMM_PAIR=1 the pair kernel wherever N % 256 == 0 (A/B comparisons).
   const bool pair = pb.N % k2BN == 0 && !(pb.passes >> 8 & (1 | 8)) && !force_1sm() &&
-                    (pb.epi == EPI_STORE || force_pair());
+                    (pb.epi == EPI_STORE || pb.K >= 512 || force_pair());
   const int BN = pair ? k2BN : choose_bn(pb.N);
   const int box_b = pair ? k2BN / 2 : BN;
   const int nkb = (pb.K + BK - 1) / BK;

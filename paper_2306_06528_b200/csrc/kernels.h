@@ -98,8 +98,10 @@ void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c
 
 // ---------------------------------------------------------------- a10 fused update
 // theta_next[row0+i][c] = theta_i[c] + (eps/n)[ sum_j K_ij (g_j[c] - r theta_j[c]) + r s_i theta_i[c] ], r = 2/h
-void svgd_update(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl, const float* K,
-                 const float* srow, const float* h, float eps_over_n, float* theta_next, cudaStream_t s);
+// Returns the number of kernels launched (1).
+int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl, const float* K,
+                const float* srow, const float* h, float eps_over_n, float* theta_next, cudaStream_t s);
+int update_row_block(int n, int nl, int64_t ld);
 
 // copy rows (device, pitched) for set_grads: dst[p*ld + k] = src[p*d + k]
 void copy_rows(const float* src, int64_t d, float* dst, int64_t ld, int rows, cudaStream_t s);

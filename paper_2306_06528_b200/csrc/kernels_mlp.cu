@@ -31,51 +31,69 @@ void split_hilo(const float* src, int64_t src_pstride, float* hi, float* lo, int
 }
 
 // ---------------------------------------------------------------- thin forward (narrow input)
-// One thread per 4 consecutive outputs of a row when nout % 4 == 0 (float4 store), else one per output.
-template <bool VEC>
+// Narrow input (in <= kThinIn): thread = output feature o, W_o and b_o held in registers, looping
+// over the rows of a 32-row block (x[b][:] is a broadcast load, the store of row b is coalesced).
+constexpr int kThinIn = 8;
+template <int NIN>
+__global__ void __launch_bounds__(256) thin_forward_narrow_kernel(const float* __restrict__ in, int64_t in_pstride,
+                                                                  const float* __restrict__ theta, int64_t ld,
+                                                                  int64_t off_w, int64_t off_b, int nin, int nout,
+                                                                  int act, float* __restrict__ out,
+                                                                  int64_t out_pstride, int B) {
+  const int p = blockIdx.y;
+  const int b0 = blockIdx.x * 32, b1 = min(B, b0 + 32);
+  const float* x = in + p * in_pstride;
+  const float* W = theta + p * ld + off_w;
+  const float* bias = theta + p * ld + off_b;
+  float* o_ = out + p * out_pstride;
+  for (int o = threadIdx.x; o < nout; o += blockDim.x) {
+    float w[kThinIn];
+#pragma unroll
+    for (int i = 0; i < kThinIn; ++i) w[i] = i < nin ? __ldg(W + (int64_t)o * nin + i) : 0.f;
+    const float bo = __ldg(bias + o);
+    for (int b = b0; b < b1; ++b) {
+      float z = 0.f;
+#pragma unroll
+      for (int i = 0; i < (NIN > 0 ? NIN : kThinIn); ++i)
+        if (NIN > 0 || i < nin) z = fmaf(__ldg(x + (int64_t)b * nin + i), w[i], z);
+      o_[(int64_t)b * nout + o] = act_fwd(z + bo, act);
+    }
+  }
+}
+// Generic thin layer (wide input): one thread per output element.
 __global__ void thin_forward_kernel(const float* __restrict__ in, int64_t in_pstride, const float* __restrict__ theta,
                                     int64_t ld, int64_t off_w, int64_t off_b, int nin, int nout, int act,
                                     float* __restrict__ out, int64_t out_pstride, int B) {
   const int p = blockIdx.y;
-  const int per = VEC ? 4 : 1;
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) * per;  // B * nout < 2^31 (max_batch * width)
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;  // B * nout < 2^31 (max_batch * width)
   if (t >= B * nout) return;
   const int b = t / nout, o = t - b * nout;
-  const float* W = theta + p * ld + off_w;
-  const float* bias = theta + p * ld + off_b;
+  const float* W = theta + p * ld + off_w + (int64_t)o * nin;
   const float* x = in + p * in_pstride + (int64_t)b * nin;
-  float z[4];
-#pragma unroll
-  for (int u = 0; u < per; ++u) z[u] = 0.f;
-  for (int i = 0; i < nin; ++i) {
-    const float xi = __ldg(x + i);
-#pragma unroll
-    for (int u = 0; u < per; ++u) z[u] = fmaf(xi, __ldg(W + (int64_t)(o + u) * nin + i), z[u]);
-  }
-  float* dst = out + p * out_pstride + t;
-  if (VEC) {
-    float4 v;
-    v.x = act_fwd(z[0] + __ldg(bias + o), act);
-    v.y = act_fwd(z[1] + __ldg(bias + o + 1), act);
-    v.z = act_fwd(z[2] + __ldg(bias + o + 2), act);
-    v.w = act_fwd(z[3] + __ldg(bias + o + 3), act);
-    *reinterpret_cast<float4*>(dst) = v;
-  } else {
-    dst[0] = act_fwd(z[0] + __ldg(bias + o), act);
-  }
+  float z = 0.f;
+  for (int i = 0; i < nin; ++i) z = fmaf(__ldg(x + i), __ldg(W + i), z);
+  out[p * out_pstride + t] = act_fwd(z + __ldg(theta + p * ld + off_b + o), act);
 }
 void thin_forward(const float* in, int64_t in_pstride, const float* theta, int64_t ld_theta, int64_t off_w,
                   int64_t off_b, int in_, int out, int act, float* dst, int64_t out_pstride, int B, int batch,
                   cudaStream_t s) {
-  const bool vec = out % 4 == 0 && out_pstride % 4 == 0;
-  const int64_t tot = (int64_t)B * out / (vec ? 4 : 1);
-  const dim3 grid((unsigned)((tot + 255) / 256), batch);
-  if (vec)
-    thin_forward_kernel<true><<<grid, 256, 0, s>>>(in, in_pstride, theta, ld_theta, off_w, off_b, in_, out, act, dst,
-                                                   out_pstride, B);
-  else
-    thin_forward_kernel<false><<<grid, 256, 0, s>>>(in, in_pstride, theta, ld_theta, off_w, off_b, in_, out, act, dst,
-                                                    out_pstride, B);
+  if (in_ <= kThinIn) {
+    const dim3 grid((unsigned)((B + 31) / 32), batch);
+    const int threads = out >= 256 ? 256 : ((out + 31) / 32) * 32;
+#define PUSH_THIN_FWD(N)                                                                                         \
+  thin_forward_narrow_kernel<N><<<grid, threads, 0, s>>>(in, in_pstride, theta, ld_theta, off_w, off_b, in_, out, \
+                                                         act, dst, out_pstride, B)
+    if (in_ == 1) PUSH_THIN_FWD(1);
+    else if (in_ == 2) PUSH_THIN_FWD(2);
+    else if (in_ == 3) PUSH_THIN_FWD(3);
+    else PUSH_THIN_FWD(0);
+#undef PUSH_THIN_FWD
+    return;
+  }
+  const int64_t tot = (int64_t)B * out;
+  thin_forward_kernel<<<dim3((unsigned)((tot + 255) / 256), batch), 256, 0, s>>>(in, in_pstride, theta, ld_theta, off_w,
+                                                                                 off_b, in_, out, act, dst,
+                                                                                 out_pstride, B);
 }
 
 // ---------------------------------------------------------------- fused output layer (a3 + a4/a5 of the top)
@@ -87,8 +105,10 @@ void thin_forward(const float* in, int64_t in_pstride, const float* theta, int64
 //        dprev[b][i]          = (sum_o dL_o(b) W_o[i]) sigma'(a_b[i])  (delta of the layer below)
 //        bprev[rb][p][i]      = sum_b dprev[b][i]                     (its bias-gradient partial)
 //   and bpart[rb][p][o] = sum_b dL_o(b).
+template <int DOUT>  // compile-time bound on d_out (loops below run to DOUT, masked by a.dout)
 __global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
-  __shared__ float sdl[32][kMaxDout];
+  __shared__ float sdl[32][DOUT];
+  __shared__ float serr[32][DOUT];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.y;
   const int rb = blockIdx.x;
@@ -97,27 +117,41 @@ __global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
   const float* __restrict__ W = a.theta + p * a.ld + a.off_w;
   const float* __restrict__ bias = a.theta + p * a.ld + a.off_b;
   const float scale = 2.0f / (float)((int64_t)a.B * a.dout);
-  // phase 1
-  for (int rr = 0; rr < 4; ++rr) {
-    const int r = warp * 4 + rr;
-    const int b = rb * 32 + r;
-    float e2 = 0.f;
-    for (int o = 0; o < a.dout; ++o) {
+  // phase 1: the warp's 4 rows advance together (4 independent chains, loads in flight together);
+  // per row the order is lane-strided accumulation then the fixed xor tree
+  for (int o = 0; o < a.dout; ++o) {
+    const float* wrow = W + (int64_t)o * a.H;
+    float part[4] = {0.f, 0.f, 0.f, 0.f};
+    const int r0 = warp * 4;
+#pragma unroll 2
+    for (int i = lane; i < a.H; i += 32) {
+      const float w = __ldg(wrow + i);
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr)
+        if (r0 + rr < rows) part[rr] = fmaf(__ldg(A + (int64_t)(r0 + rr) * a.H + i), w, part[rr]);
+    }
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) part[rr] += __shfl_xor_sync(0xffffffffu, part[rr], m);
+      const int r = r0 + rr, b = rb * 32 + r;
       float dl = 0.f;
       if (r < rows) {
-        const float* arow = A + (int64_t)r * a.H;
-        const float* wrow = W + (int64_t)o * a.H;
-        float part = 0.f;
-        for (int i = lane; i < a.H; i += 32) part = fmaf(__ldg(arow + i), __ldg(wrow + i), part);
-#pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) part += __shfl_xor_sync(0xffffffffu, part, m);
-        const float e = (part + __ldg(bias + o)) - __ldg(a.y + (int64_t)b * a.dout + o);
-        e2 = fmaf(e, e, e2);
+        const float e = (part[rr] + __ldg(bias + o)) - __ldg(a.y + (int64_t)b * a.dout + o);
         dl = scale * e;
+        if (lane == 0) serr[r][o] = e;
       }
       if (lane == 0) sdl[r][o] = dl;
     }
-    if (lane == 0 && r < rows) a.err2[p * a.err_pstride + b] = e2;
+  }
+  __syncwarp();
+  if (lane < 4) {
+    const int r = warp * 4 + lane;
+    if (r < rows) {
+      float e2 = 0.f;
+      for (int o = 0; o < a.dout; ++o) e2 = fmaf(serr[r][o], serr[r][o], e2);
+      a.err2[p * a.err_pstride + rb * 32 + r] = e2;
+    }
   }
   __syncthreads();
   if (threadIdx.x < a.dout) {
@@ -128,9 +162,9 @@ __global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
   // phase 2
   float* __restrict__ dprev = a.dprev ? a.dprev + p * a.dp_pstride + (int64_t)rb * 32 * a.H : nullptr;
   for (int i = threadIdx.x; i < a.H; i += 256) {
-    float w[kMaxDout], wacc[kMaxDout];
+    float w[DOUT], wacc[DOUT];
 #pragma unroll
-    for (int o = 0; o < kMaxDout; ++o) {
+    for (int o = 0; o < DOUT; ++o) {
       w[o] = o < a.dout ? __ldg(W + (int64_t)o * a.H + i) : 0.f;
       wacc[o] = 0.f;
     }
@@ -140,7 +174,7 @@ __global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
       const float av = __ldg(A + (int64_t)r * a.H + i);
       float d = 0.f;
 #pragma unroll
-      for (int o = 0; o < kMaxDout; ++o) {
+      for (int o = 0; o < DOUT; ++o) {
         const float dl = sdl[r][o];
         wacc[o] = fmaf(dl, av, wacc[o]);
         d = fmaf(dl, w[o], d);
@@ -158,7 +192,11 @@ __global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
 }
 void output_fused(const OutputArgs& a, int batch, cudaStream_t s) {
   const int RB = (a.B + 31) / 32;
-  output_fused_kernel<<<dim3(RB, batch), 256, 0, s>>>(a);
+  const dim3 grid(RB, batch);
+  if (a.dout == 1) output_fused_kernel<1><<<grid, 256, 0, s>>>(a);
+  else if (a.dout == 2) output_fused_kernel<2><<<grid, 256, 0, s>>>(a);
+  else if (a.dout <= 4) output_fused_kernel<4><<<grid, 256, 0, s>>>(a);
+  else output_fused_kernel<kMaxDout><<<grid, 256, 0, s>>>(a);
 }
 
 __global__ void loss_reduce_kernel(const float* __restrict__ err2, int64_t err_pstride, float* __restrict__ loss,
@@ -256,57 +294,52 @@ __device__ __forceinline__ void finalize_store(const float* theta, float* grad, 
   const float pr = (prior == PUSH_PRIOR_GAUSSIAN) ? -theta[idx] * inv_sigma2 : 0.f;
   grad[idx] = fmaf(-lambda, v, pr);
 }
-__global__ void finalize_thread_kernel(PartView W, PartView Bv, const float* __restrict__ theta,
-                                       float* __restrict__ grad, int64_t ld, int64_t off_w, int nin, int nout,
-                                       int64_t t0, int64_t t1, float lambda, int prior, float inv_sigma2) {
-  const int p = blockIdx.y;
-  const int64_t t = t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// One launch per layer: blocks [0, nb_w) reduce the weight partials, blocks [nb_w, ...) the bias
+// partials, each part with the thread- or warp-per-element scheme its partial count calls for.
+__device__ __forceinline__ void finalize_range(const PartView& W, const PartView& Bv, const float* theta,
+                                               float* grad, int64_t ld, int64_t off_w, int nin, int nout,
+                                               int64_t t0, int64_t t1, bool warp_mode, int64_t blk, float lambda,
+                                               int prior, float inv_sigma2, int p) {
+  const int64_t nw = (int64_t)nin * nout;
+  const int lane = threadIdx.x & 31;
+  const int64_t t = warp_mode ? t0 + (blk * blockDim.x + threadIdx.x) / 32 : t0 + blk * blockDim.x + threadIdx.x;
   if (t >= t1) return;
   int splits;
   int64_t ss;
-  const float* src = part_ptr(W, Bv, p, t, nin, (int64_t)nin * nout, &splits, &ss);
+  const float* src = part_ptr(W, Bv, p, t, nin, nw, &splits, &ss);
   float v = 0.f;
-  for (int s = 0; s < splits; ++s) v += src[s * ss];
+  if (warp_mode) {
+    for (int s = lane; s < splits; s += 32) v += src[s * ss];
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    if (lane != 0) return;
+  } else {
+    for (int s = 0; s < splits; ++s) v += src[s * ss];
+  }
   finalize_store(theta, grad, p * ld + off_w + t, v, lambda, prior, inv_sigma2);
 }
-__global__ void finalize_warp_kernel(PartView W, PartView Bv, const float* __restrict__ theta,
-                                     float* __restrict__ grad, int64_t ld, int64_t off_w, int nin, int nout,
-                                     int64_t t0, int64_t t1, float lambda, int prior, float inv_sigma2) {
+__global__ void finalize_kernel(PartView W, PartView Bv, const float* __restrict__ theta, float* __restrict__ grad,
+                                int64_t ld, int64_t off_w, int nin, int nout, int nb_w, float lambda, int prior,
+                                float inv_sigma2) {
   const int p = blockIdx.y;
-  const int lane = threadIdx.x & 31;
-  const int64_t t = t0 + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
-  if (t >= t1) return;
-  int splits;
-  int64_t ss;
-  const float* src = part_ptr(W, Bv, p, t, nin, (int64_t)nin * nout, &splits, &ss);
-  float v = 0.f;
-  for (int s = lane; s < splits; s += 32) v += src[s * ss];
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-  if (lane == 0) finalize_store(theta, grad, p * ld + off_w + t, v, lambda, prior, inv_sigma2);
+  const int64_t nw = (int64_t)nin * nout;
+  if ((int)blockIdx.x < nb_w)
+    finalize_range(W, Bv, theta, grad, ld, off_w, nin, nout, 0, nw, W.splits > kThreadSplits, blockIdx.x, lambda,
+                   prior, inv_sigma2, p);
+  else
+    finalize_range(W, Bv, theta, grad, ld, off_w, nin, nout, nw, nw + nout, Bv.splits > kThreadSplits,
+                   blockIdx.x - nb_w, lambda, prior, inv_sigma2, p);
 }
 int finalize_layer(PartView W, PartView Bv, const float* theta, float* grad, int64_t ld, int64_t off_w, int in,
                    int out, float lambda, int prior, float inv_sigma2, int batch, cudaStream_t s) {
   const int64_t nw = (int64_t)in * out;
-  int launches = 0;
-  auto launch = [&](int64_t t0, int64_t t1, int splits) {
-    if (t1 <= t0) return;
-    if (splits <= kThreadSplits) {
-      finalize_thread_kernel<<<dim3((unsigned)((t1 - t0 + 255) / 256), batch), 256, 0, s>>>(
-          W, Bv, theta, grad, ld, off_w, in, out, t0, t1, lambda, prior, inv_sigma2);
-    } else {
-      finalize_warp_kernel<<<dim3((unsigned)((t1 - t0 + 7) / 8), batch), 256, 0, s>>>(
-          W, Bv, theta, grad, ld, off_w, in, out, t0, t1, lambda, prior, inv_sigma2);
-    }
-    ++launches;
+  auto blocks = [](int64_t elems, int splits) {
+    return (unsigned)(splits > kThreadSplits ? (elems + 7) / 8 : (elems + 255) / 256);
   };
-  if ((W.splits <= kThreadSplits) == (Bv.splits <= kThreadSplits)) {
-    launch(0, nw + out, W.splits);
-  } else {
-    launch(0, nw, W.splits);
-    launch(nw, nw + out, Bv.splits);
-  }
-  return launches;
+  const unsigned nb_w = blocks(nw, W.splits), nb_b = blocks(out, Bv.splits);
+  finalize_kernel<<<dim3(nb_w + nb_b, batch), 256, 0, s>>>(W, Bv, theta, grad, ld, off_w, in, out, (int)nb_w, lambda,
+                                                           prior, inv_sigma2);
+  return 1;
 }
 
 // ---------------------------------------------------------------- set_grads copy

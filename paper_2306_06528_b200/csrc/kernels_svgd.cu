@@ -45,53 +45,85 @@ void init_theta(float* theta, int64_t ld, int row0, int rows, int64_t d, uint64_
 }
 
 // ---------------------------------------------------------------- a7 distances
+// Tile shapes (rows per tile side T, pairs per thread RT x RT, column groups G per CTA):
+//   n <= 8: T=8 RT=1 G=4 | n <= 16: T=16 RT=2 G=4 | n <= 32: T=32 RT=2 G=1 | else T=64 RT=4 G=1
+// Each CTA owns one upper-triangular tile pair (bi <= bj) and a fixed column range (split s);
+// sub-chunks of kDistCW columns of both row tiles are double-buffered in smem with cp.async.
+// Every accumulation order depends only on (n, ld), never on the number of ranks.
+constexpr int kDistCW = 64;
+constexpr int kDistPad = 4;  // row stride 68 floats: 16-B aligned rows, 2-way bank conflicts at most
+
 DistPlan dist_plan(int n, int64_t ld) {
   DistPlan pl;
-  pl.T = n <= 16 ? 16 : (n <= 32 ? 32 : 64);
+  pl.T = n <= 8 ? 8 : (n <= 16 ? 16 : (n <= 32 ? 32 : 64));
   pl.ntile = (n + pl.T - 1) / pl.T;
   pl.npairs = pl.ntile * (pl.ntile + 1) / 2;
-  const int64_t chunks = ld / 32;
+  const int64_t chunks = (ld + kDistCW - 1) / kDistCW;
   int64_t want = (4 * 148 + pl.npairs - 1) / pl.npairs;
   if (want > chunks) want = chunks;
   if (want < 1) want = 1;
-  pl.cols = ((ld + want - 1) / want + 31) / 32 * 32;
+  pl.cols = (((ld + want - 1) / want) + kDistCW - 1) / kDistCW * kDistCW;
   pl.splits = (int)((ld + pl.cols - 1) / pl.cols);
   return pl;
 }
 
-template <int T>
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int T, int RT>
 __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restrict__ theta, int64_t ld, int n,
                                                            int ntile, int64_t cols, float* __restrict__ part) {
-  constexpr int RT = T / 16;
-  __shared__ float si[T][33];
-  __shared__ float sj[T][33];
-  // decode upper-triangular tile pair (bi <= bj)
-  int q = blockIdx.x, bi = 0;
+  constexpr int TP = T / RT, PT = TP * TP, G = 256 / PT, RS = kDistCW + kDistPad;
+  extern __shared__ __align__(16) float dsm[];  // [2 bufs][2 tiles][T][RS], then G*PT*RT*RT reduction
+  int q = blockIdx.x, bi = 0;  // decode upper-triangular tile pair (bi <= bj)
   while (q >= ntile - bi) { q -= ntile - bi; ++bi; }
   const int bj = bi + q;
+  const bool diag = bi == bj;
   const int s = blockIdx.y;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int tid = threadIdx.x, g = tid / PT, pt = tid % PT, ty = pt / TP, tx = pt % TP;
+  const int64_t c_begin = s * cols, c_end = min(ld, c_begin + cols);
+  const int nsub = (int)((c_end - c_begin + kDistCW - 1) / kDistCW);
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));
+  auto stage = [&](int sub) {
+    const int buf = sub & 1;
+    const int64_t c0 = c_begin + (int64_t)sub * kDistCW;
+    const int ntiles_ld = diag ? 1 : 2;
+    for (int idx = tid; idx < ntiles_ld * T * (kDistCW / 4); idx += 256) {
+      const int tl = idx / (T * (kDistCW / 4));
+      const int rem = idx - tl * T * (kDistCW / 4);
+      const int r = rem / (kDistCW / 4), c4 = rem - r * (kDistCW / 4);
+      const int grow = (tl ? bj : bi) * T + r;
+      const int64_t col = c0 + 4 * c4;
+      const bool ok = grow < n && col < c_end;
+      const float* src = theta + (ok ? (int64_t)grow * ld + col : 0);
+      cp_async16(sbase + 4 * (((buf * 2 + tl) * T + r) * RS + 4 * c4), src, ok ? 16 : 0);
+    }
+  };
   float acc[RT][RT];
 #pragma unroll
   for (int r = 0; r < RT; ++r)
 #pragma unroll
     for (int c = 0; c < RT; ++c) acc[r][c] = 0.f;
-  const int64_t c_begin = s * cols, c_end = min(ld, c_begin + cols);
-  for (int64_t c0 = c_begin; c0 < c_end; c0 += 32) {
-    for (int idx = threadIdx.x; idx < T * 32; idx += 256) {
-      const int r = idx >> 5, k = idx & 31;
-      const int gi = bi * T + r, gj = bj * T + r;
-      si[r][k] = gi < n ? theta[(int64_t)gi * ld + c0 + k] : 0.f;
-      sj[r][k] = gj < n ? theta[(int64_t)gj * ld + c0 + k] : 0.f;
-    }
+  stage(0);
+  cp_async_commit();
+  for (int sub = 0; sub < nsub; ++sub) {
+    if (sub + 1 < nsub) stage(sub + 1);
+    cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
+    const float* si = dsm + (size_t)((sub & 1) * 2) * T * RS;
+    const float* sj = diag ? si : si + T * RS;
 #pragma unroll 4
-    for (int k = 0; k < 32; ++k) {
+    for (int k = g; k < kDistCW; k += G) {
       float a[RT], b[RT];
 #pragma unroll
-      for (int r = 0; r < RT; ++r) a[r] = si[ty * RT + r][k];
+      for (int r = 0; r < RT; ++r) a[r] = si[(ty + TP * r) * RS + k];
 #pragma unroll
-      for (int c = 0; c < RT; ++c) b[c] = sj[tx * RT + c][k];
+      for (int c = 0; c < RT; ++c) b[c] = sj[(tx + TP * c) * RS + k];
 #pragma unroll
       for (int r = 0; r < RT; ++r)
 #pragma unroll
@@ -102,26 +134,51 @@ __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restri
     }
     __syncthreads();
   }
+  if constexpr (G > 1) {  // combine the column groups in ascending g
+    float* red = dsm + 4 * T * RS;
+#pragma unroll
+    for (int r = 0; r < RT; ++r)
+#pragma unroll
+      for (int c = 0; c < RT; ++c) red[(g * PT + pt) * RT * RT + r * RT + c] = acc[r][c];
+    __syncthreads();
+    if (g != 0) return;
+#pragma unroll
+    for (int r = 0; r < RT; ++r)
+#pragma unroll
+      for (int c = 0; c < RT; ++c) {
+        float v = red[pt * RT * RT + r * RT + c];
+        for (int gg = 1; gg < G; ++gg) v += red[(gg * PT + pt) * RT * RT + r * RT + c];
+        acc[r][c] = v;
+      }
+  }
   float* P = part + (int64_t)s * n * n;
 #pragma unroll
   for (int r = 0; r < RT; ++r)
 #pragma unroll
     for (int c = 0; c < RT; ++c) {
-      const int gi = bi * T + ty * RT + r, gj = bj * T + tx * RT + c;
+      const int gi = bi * T + ty + TP * r, gj = bj * T + tx + TP * c;
       if (gi < n && gj < n) {
         P[(int64_t)gi * n + gj] = acc[r][c];
         P[(int64_t)gj * n + gi] = acc[r][c];  // (a-b)^2 == (b-a)^2 bit-exactly
       }
     }
 }
+template <int T, int RT>
+static void dist_launch(const float* theta, int64_t ld, int n, const DistPlan& pl, float* part, cudaStream_t s) {
+  constexpr int TP = T / RT, PT = TP * TP, G = 256 / PT;
+  const size_t smem = sizeof(float) * (4 * T * (kDistCW + kDistPad) + (G > 1 ? G * PT * RT * RT : 0));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dist_partial_kernel<T, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dist_partial_kernel<T, RT><<<dim3(pl.npairs, pl.splits), 256, smem, s>>>(theta, ld, n, pl.ntile, pl.cols, part);
+}
 void dist_partial(const float* theta, int64_t ld, int n, const DistPlan& pl, float* part, cudaStream_t s) {
-  dim3 grid(pl.npairs, pl.splits);
-  if (pl.T == 16)
-    dist_partial_kernel<16><<<grid, 256, 0, s>>>(theta, ld, n, pl.ntile, pl.cols, part);
-  else if (pl.T == 32)
-    dist_partial_kernel<32><<<grid, 256, 0, s>>>(theta, ld, n, pl.ntile, pl.cols, part);
-  else
-    dist_partial_kernel<64><<<grid, 256, 0, s>>>(theta, ld, n, pl.ntile, pl.cols, part);
+  if (pl.T == 8) dist_launch<8, 1>(theta, ld, n, pl, part, s);
+  else if (pl.T == 16) dist_launch<16, 2>(theta, ld, n, pl, part, s);
+  else if (pl.T == 32) dist_launch<32, 2>(theta, ld, n, pl, part, s);
+  else dist_launch<64, 4>(theta, ld, n, pl, part, s);
 }
 
 // One warp per D entry: lane l sums splits s = l, l+32, ... ascending, then a fixed xor tree
@@ -235,72 +292,107 @@ void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c
 }
 
 // ---------------------------------------------------------------- a10 fused update
-constexpr int UPD_RB = 16;  // own rows per CTA (register accumulators: 16 x float4)
+// Thread = CT consecutive columns x RB own rows (RB*CT register accumulators); the CTA keeps
+// K^T[j][i] for its RB rows in smem (read as float4 broadcasts), so per j a thread loads CT values
+// of theta_j and g_j, RB/4 LDS.128 and issues RB*CT + CT FMAs.  Theta_all / G_all are streamed
+// ceil(n_local / RB) times.
+//   acc_i = sum_j K_ij (g_jk - r theta_jk)   (ascending j),   theta'_ik = theta_ik + (eps/n)(acc_i + r s_i theta_ik)
+// Each (i, k) sum runs over j in ascending order whatever (RB, CT), so results do not depend on them.
+template <int CT>
+struct VecT;
+template <>
+struct VecT<1> { using T = float; };
+template <>
+struct VecT<2> { using T = float2; };
+template <>
+struct VecT<4> { using T = float4; };
+__device__ __forceinline__ float vget(const float& v, int) { return v; }
+__device__ __forceinline__ float vget(const float2& v, int e) { return e == 0 ? v.x : v.y; }
+__device__ __forceinline__ float vget(const float4& v, int e) { return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w)); }
 
-__global__ void __launch_bounds__(256) svgd_update_kernel(const float* __restrict__ theta,
+template <int RB, int CT>
+__global__ void __launch_bounds__(128) svgd_update_kernel(const float* __restrict__ theta,
                                                           const float* __restrict__ grad, int64_t ld, int n, int row0,
                                                           int nl, const float* __restrict__ K,
                                                           const float* __restrict__ srow,
                                                           const float* __restrict__ hptr, float eps_n,
                                                           float* __restrict__ theta_next) {
-  extern __shared__ float sK[];  // [UPD_RB][n]
-  const int rb0 = blockIdx.y * UPD_RB;
-  const int rows = min(UPD_RB, nl - rb0);
-  for (int idx = threadIdx.x; idx < UPD_RB * n; idx += blockDim.x) {
-    const int r = idx / n;
-    sK[idx] = r < rows ? K[(int64_t)(rb0 + r) * n + (idx % n)] : 0.f;
+  using V = typename VecT<CT>::T;
+  extern __shared__ __align__(16) float sKT[];  // [n][RB]: K_(rb0+i),j at sKT[j*RB + i]
+  const int rb0 = blockIdx.y * RB;
+  const int rows = min(RB, nl - rb0);
+  for (int idx = threadIdx.x; idx < RB * n; idx += blockDim.x) {
+    const int j = idx / RB, i = idx - j * RB;
+    sKT[idx] = i < rows ? K[(int64_t)(rb0 + i) * n + j] : 0.f;
   }
   __syncthreads();
   const float r2 = 2.0f / *hptr;
-  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * CT;
   if (c >= ld) return;
-  float4 acc[UPD_RB];
+  float acc[RB][CT];
 #pragma unroll
-  for (int r = 0; r < UPD_RB; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 2
+  for (int r = 0; r < RB; ++r)
+#pragma unroll
+    for (int e = 0; e < CT; ++e) acc[r][e] = 0.f;
+#pragma unroll 4
   for (int j = 0; j < n; ++j) {
-    const float4 tj = __ldg(reinterpret_cast<const float4*>(theta + (int64_t)j * ld + c));
-    const float4 gj = __ldg(reinterpret_cast<const float4*>(grad + (int64_t)j * ld + c));
-    float4 m;
-    m.x = fmaf(-r2, tj.x, gj.x);
-    m.y = fmaf(-r2, tj.y, gj.y);
-    m.z = fmaf(-r2, tj.z, gj.z);
-    m.w = fmaf(-r2, tj.w, gj.w);
+    const V tv = __ldg(reinterpret_cast<const V*>(theta + (int64_t)j * ld + c));
+    const V gv = __ldg(reinterpret_cast<const V*>(grad + (int64_t)j * ld + c));
+    float m[CT];
 #pragma unroll
-    for (int r = 0; r < UPD_RB; ++r) {
-      const float k = sK[r * n + j];
-      acc[r].x = fmaf(k, m.x, acc[r].x);
-      acc[r].y = fmaf(k, m.y, acc[r].y);
-      acc[r].z = fmaf(k, m.z, acc[r].z);
-      acc[r].w = fmaf(k, m.w, acc[r].w);
+    for (int e = 0; e < CT; ++e) m[e] = fmaf(-r2, vget(tv, e), vget(gv, e));
+    const float4* kj = reinterpret_cast<const float4*>(sKT + j * RB);
+#pragma unroll
+    for (int r4 = 0; r4 < RB / 4; ++r4) {
+      const float4 k4 = kj[r4];
+      const float kk[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int e = 0; e < CT; ++e) acc[4 * r4 + u][e] = fmaf(kk[u], m[e], acc[4 * r4 + u][e]);
     }
   }
 #pragma unroll
-  for (int r = 0; r < UPD_RB; ++r) {
+  for (int r = 0; r < RB; ++r) {
     if (r < rows) {
       const int64_t i = row0 + rb0 + r;
-      const float4 ti = *reinterpret_cast<const float4*>(theta + i * ld + c);
       const float rs = r2 * srow[rb0 + r];
-      float4 o;
-      o.x = fmaf(eps_n, fmaf(rs, ti.x, acc[r].x), ti.x);
-      o.y = fmaf(eps_n, fmaf(rs, ti.y, acc[r].y), ti.y);
-      o.z = fmaf(eps_n, fmaf(rs, ti.z, acc[r].z), ti.z);
-      o.w = fmaf(eps_n, fmaf(rs, ti.w, acc[r].w), ti.w);
-      *reinterpret_cast<float4*>(theta_next + i * ld + c) = o;
+#pragma unroll
+      for (int e = 0; e < CT; ++e) {
+        const float ti = theta[i * ld + c + e];
+        theta_next[i * ld + c + e] = fmaf(eps_n, fmaf(rs, ti, acc[r][e]), ti);
+      }
     }
   }
 }
-void svgd_update(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl, const float* K,
-                 const float* srow, const float* h, float eps_over_n, float* theta_next, cudaStream_t s) {
-  const int64_t vec = ld / 4;
-  dim3 grid((unsigned)((vec + 255) / 256), (nl + UPD_RB - 1) / UPD_RB);
-  const size_t smem = sizeof(float) * UPD_RB * n;
+constexpr int kUpdThreads = 128;
+template <int RB, int CT>
+static void update_launch(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl, const float* K,
+                          const float* srow, const float* h, float eps_over_n, float* theta_next, cudaStream_t s) {
+  const size_t smem = sizeof(float) * RB * n;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(svgd_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(svgd_update_kernel<RB, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  svgd_update_kernel<<<grid, 256, smem, s>>>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next);
+  const dim3 grid((unsigned)((ld / CT + kUpdThreads - 1) / kUpdThreads), (unsigned)((nl + RB - 1) / RB));
+  svgd_update_kernel<RB, CT><<<grid, kUpdThreads, smem, s>>>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n,
+                                                             theta_next);
+}
+// (RB, CT) = (16, 4): measured fastest on every config (C3 1.7 ms vs 2.2 ms for 32 x 2 and 2.5 ms for
+// 64 x 1, whose lower re-read factor does not pay for the smaller loads); kept as a query so the
+// launch accounting stays in one place.
+int update_row_block(int n, int nl, int64_t ld) {
+  (void)n; (void)nl; (void)ld;
+  return 16;
+}
+int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl, const float* K,
+                const float* srow, const float* h, float eps_over_n, float* theta_next, cudaStream_t s) {
+  if (update_row_block(n, nl, ld) == 32)
+    update_launch<32, 2>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next, s);
+  else
+    update_launch<16, 4>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next, s);
+  return 1;
 }
 
 }  // namespace kern
