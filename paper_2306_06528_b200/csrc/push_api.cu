@@ -897,8 +897,16 @@ static push_status dbg_gemm(int passes, int32_t a_mn, int32_t b_mn, int32_t b_sp
     pb.B = gemm::Operand{buf, buf + batch * nb, false, b_mn != 0, b_mn ? N : K, nb};
   pb.epi = gemm::EPI_STORE;
   pb.out = C; pb.ldo = N; pb.out_pstride = (int64_t)M * N; pb.out_sstride = 0;
+  float* zb = nullptr;
+  if ((passes >> 8) & 32) {  // experiment: the forward epilogue (bias 0, tanh) instead of a plain store
+    PUSH_CUDA_TRY(cudaMallocAsync(&zb, sizeof(float) * N, s));
+    PUSH_CUDA_TRY(cudaMemsetAsync(zb, 0, sizeof(float) * N, s));
+    pb.epi = gemm::EPI_FWD; pb.act = PUSH_ACT_TANH; pb.bias = zb; pb.bias_pstride = 0;
+    pb.passes = passes & ~(32 << 8);
+  }
   push_status st = gemm::run(pb, s);
   if (buf) cudaFreeAsync(buf, s);
+  if (zb) cudaFreeAsync(zb, s);
   return st;
 }
 
