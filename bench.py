@@ -208,9 +208,15 @@ def run_ours(args, w):
     def maxall(v):
         return pdist.max_over_ranks(v, ws, dev)
 
+    def step(s):
+        if args.no_graph:
+            ctx.particle_grads(xs[s], ys[s])
+            ctx.svgd_step()
+        else:
+            ctx.step_graph(xs[s], ys[s])
+
     for s in range(args.warmup):
-        ctx.particle_grads(xs[s], ys[s])
-        ctx.svgd_step()
+        step(s)
     barrier()
     clocks = ClockSampler(local)
     time.sleep(0.3)
@@ -219,8 +225,7 @@ def run_ours(args, w):
     barrier()
     e0.record(stream)
     for s in range(args.warmup, nsteps):
-        ctx.particle_grads(xs[s], ys[s])
-        ctx.svgd_step()
+        step(s)
     e1.record(stream)
     barrier()
     ms = maxall(e0.elapsed_time(e1))
@@ -291,7 +296,8 @@ def run_ours(args, w):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": w.name + ": " + w.note, "n_particles": w.n_particles, "dims": dims,
                        "d": w.d, "batch": w.batch, "parallelism": f"particles sharded n/{ws} per GPU",
-                       "l2": "per-step working set > 126 MB L2 (no flush)"},
+                       "l2": "per-step working set > 126 MB L2 (no flush)",
+                       "launch": "eager" if args.no_graph else "cuda-graph (batch staged D2D into the context each step)"},
             "param_updates_per_s": value * w.d, "clocks": clk, "e2e": e2e,
             "gpu_launches": int(launches), "roofline": roof, "phases": phases}
     if ws == 1 and not args.no_cpu_baseline:
@@ -309,6 +315,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of the captured CUDA graph")
     args = ap.parse_args()
     w = WORKLOADS[args.config]
     if args.impl == "reference":

@@ -163,10 +163,21 @@ push_status push_set_grads(push_ctx* ctx, const float* g_dev, void* stream);
  * Errors: PUSH_E_STATE (no fresh grads), PUSH_E_CUDA, PUSH_E_NCCL. */
 push_status push_svgd_step(push_ctx* ctx, void* stream);
 
+/* ASYNC.  One whole step (push_particle_grads + push_svgd_step) replayed from a CUDA graph: the batch
+ * is first copied (device to device, on `stream`) into the context's own batch buffers, which the
+ * captured step reads; one executable graph per Theta buffer parity is captured on first use and
+ * re-captured when B or loss_dev changes.  The first call on a context runs eagerly (it also
+ * initialises every kernel's one-time attributes).  Results are identical to the eager calls.
+ * PUSH_NO_GRAPH=1 in the environment, or profiling (push_profile_enable), selects the eager path.
+ *   x_dev, y_dev, B, loss_dev: as in push_particle_grads.   State: READY or GRADS_READY -> READY.
+ * Errors: PUSH_E_INVALID, PUSH_E_SHAPE, PUSH_E_CUDA, PUSH_E_NCCL. */
+push_status push_step_graph(push_ctx* ctx, const float* x_dev, const float* y_dev, int32_t B, float* loss_dev,
+                            void* stream);
+
 /* SYNC.  End-to-end convenience through host memory: copies x_host (B x d_in)
- * and y_host (B x d_out) to the device, runs push_particle_grads +
- * push_svgd_step, copies the n_local per-particle losses to loss_host (may be
- * NULL) and synchronises `stream`.  State: READY -> READY. */
+ * and y_host (B x d_out) to the device, runs the step (push_step_graph), copies
+ * the n_local per-particle losses to loss_host (may be NULL) and synchronises
+ * `stream`.  State: READY -> READY. */
 push_status push_step_host(push_ctx* ctx, const float* x_host, const float* y_host, int32_t B,
                            float* loss_host, void* stream);
 

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -226,6 +227,20 @@ struct push_ctx {
   // exchange
   push::nccl::Comm comm = nullptr;
   std::shared_ptr<push::LocalGroup> group;
+  // comm stream: the Theta all-gather (a6/C1) runs beside the gradient kernels (P > 1)
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_theta = nullptr;
+  bool theta_pending = false;
+  // CUDA-graph replay of a whole step (push_step_graph): one executable per Theta buffer parity
+  struct GraphEntry {
+    int B = 0;
+    float* loss = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0;
+  };
+  GraphEntry graphs[2];
+  cudaStream_t cap_stream = nullptr;
+  bool graph_warm = false;
   // profiling
   bool prof_on = false;
   std::vector<push::ProfRec> recs;
@@ -351,8 +366,16 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
     return r;
   };
 
-  // C1: Theta rows of every rank (needed by a7/a10; unchanged during the gradient phase)
-  if ((st = exchange(c, BUF_THETA, s)) != PUSH_OK) return st;
+  // C1: Theta rows of every rank (needed by a7/a10; unchanged during the gradient phase, whose kernels
+  // only read the own rows, which the in-place all-gather only reads): on the comm stream, joined in
+  // push_svgd_step
+  if (c->world > 1) {
+    PUSH_CUDA_TRY(cudaEventRecord(c->ev_fork, s));
+    PUSH_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
+    if ((st = exchange(c, BUF_THETA, c->comm_stream)) != PUSH_OK) return st;
+    PUSH_CUDA_TRY(cudaEventRecord(c->ev_theta, c->comm_stream));
+    c->theta_pending = true;
+  }
 
   // a0: tf32 hi/lo copies of tensor-core weights that are not 16-B aligned in Theta (the others, and all
   // activations, are split on the staged tile inside the GEMM)
@@ -513,6 +536,10 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
 static push_status do_step(push_ctx* c, cudaStream_t s) {
   const Plan& P = c->P;
   push_status st;
+  if (c->theta_pending) {  // join the Theta all-gather started by the gradient call
+    PUSH_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_theta, 0));
+    c->theta_pending = false;
+  }
   // C2: g rows of every rank
   if ((st = exchange(c, BUF_GRAD, s)) != PUSH_OK) return st;
   const float* th = c->theta[c->cur];
@@ -598,6 +625,10 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   else if (cfg->bw_rule == PUSH_BW_MEDIAN_LN_N1)
     c->c_ln = (float)(1.0 / std::log((double)P.n + 1.0));
 
+  PUSH_CUDA_TRY(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+  PUSH_CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_theta, cudaEventDisableTiming));
   cudaStream_t s = nullptr;
   const size_t nld = (size_t)P.n * P.ld;
   PUSH_CUDA_TRY(cudaMemsetAsync(c->theta[0], 0, nld * 4, s));
@@ -749,6 +780,79 @@ push_status push_svgd_step(push_ctx* c, void* stream) {
   return PUSH_OK;
 }
 
+static bool graphs_disabled() {
+  static const int v = [] {
+    const char* e = getenv("PUSH_NO_GRAPH");
+    return e && *e && *e != '0' ? 1 : 0;
+  }();
+  return v != 0;
+}
+
+push_status push_step_graph(push_ctx* c, const float* x_dev, const float* y_dev, int32_t B, float* loss_dev,
+                            void* stream) {
+  push_status st = check_ctx(c);
+  if (st != PUSH_OK) return st;
+  if (!x_dev || !y_dev) return fail(PUSH_E_INVALID, "x_dev / y_dev is NULL");
+  if (B < 1 || B > c->P.Bmax) return fail(PUSH_E_SHAPE, "B must be in [1, max_batch] (SPEC.md:55)");
+  if (c->group && c->world > 1)
+    return fail(PUSH_E_STATE, "whole-step calls need every rank's gradients first: use the lockstep calls in a local group");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int din = c->P.layers[0].in, dout = c->P.layers[c->P.L - 1].out;
+  // the captured step always reads the context's fixed batch buffers
+  auto stage = [&]() -> push_status {
+    if (x_dev != c->xbuf) PUSH_CUDA_TRY(cudaMemcpyAsync(c->xbuf, x_dev, (size_t)B * din * 4, cudaMemcpyDeviceToDevice, s));
+    if (y_dev != c->ybuf) PUSH_CUDA_TRY(cudaMemcpyAsync(c->ybuf, y_dev, (size_t)B * dout * 4, cudaMemcpyDeviceToDevice, s));
+    return PUSH_OK;
+  };
+  if ((st = stage()) != PUSH_OK) return sticky(c, st);
+  if (c->prof_on || graphs_disabled() || !c->graph_warm) {
+    // eager path (profiling, PUSH_NO_GRAPH=1, or the first call, which also initialises every
+    // kernel's one-time attributes so that the capture below records stream work only)
+    if ((st = push_particle_grads(c, c->xbuf, c->ybuf, B, loss_dev, stream)) != PUSH_OK) return st;
+    if ((st = push_svgd_step(c, stream)) != PUSH_OK) return st;
+    c->graph_warm = true;
+    return PUSH_OK;
+  }
+  push_ctx::GraphEntry& g = c->graphs[c->cur];
+  if (!g.exec || g.B != B || g.loss != loss_dev) {
+    if (g.exec) {
+      cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+    }
+    const int cur0 = c->cur;
+    const int64_t l0 = c->launches;
+    cudaGraph_t graph = nullptr;
+    PUSH_CUDA_TRY(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    st = do_grads(c, c->xbuf, c->ybuf, B, c->cap_stream);
+    if (st == PUSH_OK && loss_dev) {
+      cudaError_t e = cudaMemcpyAsync(loss_dev, c->loss, 4 * c->P.nl, cudaMemcpyDeviceToDevice, c->cap_stream);
+      if (e != cudaSuccess) st = fail(PUSH_E_CUDA, cudaGetErrorString(e));
+    }
+    if (st == PUSH_OK) st = do_step(c, c->cap_stream);
+    cudaError_t e = cudaStreamEndCapture(c->cap_stream, &graph);
+    c->cur = cur0;  // capturing executed nothing
+    c->theta_pending = false;
+    if (st != PUSH_OK || e != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      return sticky(c, st != PUSH_OK ? st : fail(PUSH_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e)));
+    }
+    e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e)));
+    g.kernels = c->launches - l0;
+    c->launches = l0;
+    g.B = B;
+    g.loss = loss_dev;
+  }
+  cudaError_t e = cudaGraphLaunch(g.exec, s);
+  if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, std::string("graph launch: ") + cudaGetErrorString(e)));
+  c->launches += g.kernels;
+  c->cur ^= 1;
+  c->state = 0;
+  c->has_grads = c->has_step = true;
+  return PUSH_OK;
+}
+
 push_status push_step_host(push_ctx* c, const float* x_host, const float* y_host, int32_t B, float* loss_host,
                            void* stream) {
   push_status st = check_ctx(c);
@@ -763,8 +867,7 @@ push_status push_step_host(push_ctx* c, const float* x_host, const float* y_host
     return PUSH_OK;
   };
   if ((st = copy_in()) != PUSH_OK) return sticky(c, st);
-  if ((st = push_particle_grads(c, c->xbuf, c->ybuf, B, nullptr, stream)) != PUSH_OK) return st;
-  if ((st = push_svgd_step(c, stream)) != PUSH_OK) return st;
+  if ((st = push_step_graph(c, c->xbuf, c->ybuf, B, nullptr, stream)) != PUSH_OK) return st;
   if (loss_host) {
     cudaError_t e = cudaMemcpyAsync(loss_host, c->loss, 4 * c->P.nl, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
@@ -868,6 +971,12 @@ push_status push_destroy(push_ctx* c) {
     cudaEventDestroy(r.e1);
   }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (auto& gph : c->graphs)
+    if (gph.exec) cudaGraphExecDestroy(gph.exec);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_theta) cudaEventDestroy(c->ev_theta);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
   return PUSH_OK;
 }

@@ -29,7 +29,8 @@ MAX_LAYERS = 15
 
 # Every symbol include/push.h and include/push_debug.h declare (checked by tests/test_abi.py).
 EXPORTS = ["push_version", "push_last_error", "push_get_unique_id", "push_workspace_size", "push_init",
-           "push_init_local_group", "push_particle_grads", "push_set_grads", "push_svgd_step", "push_step_host",
+           "push_init_local_group", "push_particle_grads", "push_set_grads", "push_svgd_step", "push_step_graph",
+           "push_step_host",
            "push_gather", "push_profile_enable", "push_profile_read", "push_launch_count", "push_destroy",
            "pushdbg_gemm3xtf32", "pushdbg_gemm1xtf32", "pushdbg_gemm"]
 
@@ -74,6 +75,7 @@ def lib():
         "push_particle_grads": ([P, P, P, c_int32, P, P], c_int32),
         "push_set_grads": ([P, P, P], c_int32),
         "push_svgd_step": ([P, P], c_int32),
+        "push_step_graph": ([P, P, P, c_int32, P, P], c_int32),
         "push_step_host": ([P, P, P, c_int32, P, P], c_int32),
         "push_gather": ([P, c_int32, P, P], c_int32),
         "push_profile_enable": ([P, c_int32], c_int32),
@@ -183,6 +185,10 @@ class Context:
 
     def svgd_step(self, stream=None):
         check(lib().push_svgd_step(self._h, _stream(stream)))
+
+    def step_graph(self, x, y, loss=None, stream=None):
+        """push_particle_grads + push_svgd_step replayed from a captured CUDA graph."""
+        check(lib().push_step_graph(self._h, _ptr(x), _ptr(y), int(x.shape[0]), _ptr(loss), _stream(stream)))
 
     def step_host(self, x: np.ndarray, y: np.ndarray, stream=None) -> np.ndarray:
         loss = np.empty(self.n_local, dtype=np.float32)

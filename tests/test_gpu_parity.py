@@ -194,6 +194,27 @@ def test_step_host_equals_device_path():
     assert np.array_equal(a.gather("theta"), b.gather("theta"))
 
 
+@pytest.mark.parametrize("cfgname", ["C1", "C2"])
+def test_step_graph_equals_eager(cfgname):
+    """push_step_graph (captured CUDA graph, batch staged into the context's buffers) reproduces the
+    eager calls bit for bit over several steps with changing batches."""
+    w = WORKLOADS[cfgname]
+    dims = list(w.dims)
+    a = push.Context(push.make_config(w.n_particles, dims, max_batch=w.batch, seed=6, step_size=1e-2))
+    b = push.Context(push.make_config(w.n_particles, dims, max_batch=w.batch, seed=6, step_size=1e-2))
+    la = torch.empty(w.n_particles, device="cuda")
+    lb = torch.empty(w.n_particles, device="cuda")
+    for t in range(5):
+        x, y = synth.workload_batch(w, t)
+        xd, yd = _dev(x), _dev(y)
+        a.particle_grads(xd, yd, la)
+        a.svgd_step()
+        b.step_graph(xd, yd, lb)
+        assert torch.equal(la, lb), t
+    assert np.array_equal(a.gather("theta"), b.gather("theta"))
+    assert np.array_equal(a.gather("dist"), b.gather("dist"))
+
+
 def test_state_machine_errors():
     ctx = push.Context(push.make_config(2, [1, 32, 1], max_batch=8))
     with pytest.raises(push.PushError) as e:
