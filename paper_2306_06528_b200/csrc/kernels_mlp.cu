@@ -319,26 +319,30 @@ __device__ __forceinline__ void finalize_range(const PartView& W, const PartView
   finalize_store(theta, grad, p * ld + off_w + t, v, lambda, prior, inv_sigma2);
 }
 __global__ void finalize_kernel(PartView W, PartView Bv, const float* __restrict__ theta, float* __restrict__ grad,
-                                int64_t ld, int64_t off_w, int nin, int nout, int nb_w, float lambda, int prior,
-                                float inv_sigma2) {
+                                int64_t ld, int64_t off_w, int nin, int nout, int nb_w, bool w_warp, bool b_warp,
+                                float lambda, int prior, float inv_sigma2) {
   const int p = blockIdx.y;
   const int64_t nw = (int64_t)nin * nout;
   if ((int)blockIdx.x < nb_w)
-    finalize_range(W, Bv, theta, grad, ld, off_w, nin, nout, 0, nw, W.splits > kThreadSplits, blockIdx.x, lambda,
-                   prior, inv_sigma2, p);
+    finalize_range(W, Bv, theta, grad, ld, off_w, nin, nout, 0, nw, w_warp, blockIdx.x, lambda, prior, inv_sigma2, p);
   else
-    finalize_range(W, Bv, theta, grad, ld, off_w, nin, nout, nw, nw + nout, Bv.splits > kThreadSplits,
-                   blockIdx.x - nb_w, lambda, prior, inv_sigma2, p);
+    finalize_range(W, Bv, theta, grad, ld, off_w, nin, nout, nw, nw + nout, b_warp, blockIdx.x - nb_w, lambda, prior,
+                   inv_sigma2, p);
 }
 int finalize_layer(PartView W, PartView Bv, const float* theta, float* grad, int64_t ld, int64_t off_w, int in,
                    int out, float lambda, int prior, float inv_sigma2, int batch, cudaStream_t s) {
   const int64_t nw = (int64_t)in * out;
-  auto blocks = [](int64_t elems, int splits) {
-    return (unsigned)(splits > kThreadSplits ? (elems + 7) / 8 : (elems + 255) / 256);
+  // warp-per-element only pays off for few elements: it reads each partial row strided (uncoalesced);
+  // thread-per-element reads one contiguous row of elements per partial
+  auto warp_mode = [](int64_t elems, int splits) { return splits > kThreadSplits && elems < 32768; };
+  const int Wsp = warp_mode(nw, W.splits) ? W.splits : 1, Bsp = warp_mode(out, Bv.splits) ? Bv.splits : 1;
+  auto blocks = [](int64_t elems, int wsplits) {
+    return (unsigned)(wsplits > kThreadSplits ? (elems + 7) / 8 : (elems + 255) / 256);
   };
-  const unsigned nb_w = blocks(nw, W.splits), nb_b = blocks(out, Bv.splits);
-  finalize_kernel<<<dim3(nb_w + nb_b, batch), 256, 0, s>>>(W, Bv, theta, grad, ld, off_w, in, out, (int)nb_w, lambda,
-                                                           prior, inv_sigma2);
+  const unsigned nb_w = blocks(nw, Wsp), nb_b = blocks(out, Bsp);
+  finalize_kernel<<<dim3(nb_w + nb_b, batch), 256, 0, s>>>(W, Bv, theta, grad, ld, off_w, in, out, (int)nb_w,
+                                                           Wsp > kThreadSplits, Bsp > kThreadSplits, lambda, prior,
+                                                           inv_sigma2);
   return 1;
 }
 

@@ -2,7 +2,7 @@
 //
 //   a7  D_ij = sum_k (theta_ik - theta_jk)^2        split over d, fixed chunk order
 //   a8  h = median(D) * c_n  (radix select on the fp32 bit patterns: bit-exact)
-//   a9  K_ij = exp(-D_ij / h),  s_i = sum_j K_ij    (ascending j)
+//   a9  K_ij = exp(-D_ij / h),  s_i = sum_j K_ij    (lane-strided + fixed xor tree)
 //   a10 theta_i <- theta_i + (eps/n) [ sum_j K_ij (g_j - r theta_j) + r s_i theta_i ],  r = 2/h
 //
 // a10 is phi(theta_i) = (1/n) sum_j [K_ij grad log p(theta_j) + grad_{theta_j} K_ij] with
@@ -253,9 +253,17 @@ __device__ uint32_t block_select(const float* __restrict__ D, int64_t N, uint32_
   return prefix;
 }
 
+// Median of all n^2 entries of D without touching the redundant ones: D has a +0 diagonal and
+// D_ij = D_ji >= 0, so the ascending list of all n^2 entries is n zeros followed by every strictly-
+// upper-triangle value u twice, and the two middle order statistics are
+//   n = 2: (0, u[0]);  n odd: u[(n-1)^2/4 - 1] (twice);  n even >= 4: u[n(n-2)/4 - 1], u[n(n-2)/4].
+// For n(n-1)/2 <= kTriKeys the u values are staged in shared memory and selected there.
+constexpr int kTriKeys = 40 * 1024;  // 160 KB of keys
 __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(const float* __restrict__ D, int n, int row0, int nl,
                                                               int rule, float c_ln, float bw_h, float* __restrict__ h_out,
-                                                              float* __restrict__ K, float* __restrict__ srow) {
+                                                              float* __restrict__ K, float* __restrict__ srow,
+                                                              int use_tri) {
+  extern __shared__ float skeys[];
   __shared__ uint32_t hist[256];
   __shared__ uint32_t sh[2];
   __shared__ float s_h;
@@ -265,8 +273,28 @@ __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(const float* __res
   } else if (n == 1) {
     if (threadIdx.x == 0) s_h = 1.0f;
   } else {
-    const float v0 = __uint_as_float(block_select(D, N, (uint32_t)((N - 1) / 2), hist, sh));
-    const float v1 = __uint_as_float(block_select(D, N, (uint32_t)(N / 2), hist, sh));
+    float v0, v1;
+    if (use_tri) {
+      const int64_t m = (int64_t)n * (n - 1) / 2;
+      for (int64_t idx = threadIdx.x; idx < N; idx += blockDim.x) {
+        const int i = (int)(idx / n), j = (int)(idx - (int64_t)i * n);
+        if (j > i) skeys[(int64_t)i * n - (int64_t)i * (i + 1) / 2 + (j - i - 1)] = D[idx];
+      }
+      __syncthreads();
+      if (n == 2) {
+        v0 = 0.f;
+        v1 = skeys[0];
+      } else if (n & 1) {
+        v0 = v1 = __uint_as_float(block_select(skeys, m, (uint32_t)((int64_t)(n - 1) * (n - 1) / 4 - 1), hist, sh));
+      } else {
+        const uint32_t k0 = (uint32_t)((int64_t)n * (n - 2) / 4 - 1);
+        v0 = __uint_as_float(block_select(skeys, m, k0, hist, sh));
+        v1 = __uint_as_float(block_select(skeys, m, k0 + 1, hist, sh));
+      }
+    } else {
+      v0 = __uint_as_float(block_select(D, N, (uint32_t)((N - 1) / 2), hist, sh));
+      v1 = __uint_as_float(block_select(D, N, (uint32_t)(N / 2), hist, sh));
+    }
     if (threadIdx.x == 0) {
       const float med = (v0 + v1) * 0.5f;
       s_h = med > 0.f ? med * c_ln : 1.0f;
@@ -275,20 +303,34 @@ __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(const float* __res
   __syncthreads();
   const float h = s_h;
   if (threadIdx.x == 0) *h_out = h;
-  for (int64_t idx = threadIdx.x; idx < (int64_t)nl * n; idx += blockDim.x) {
-    const int i = (int)(idx / n), j = (int)(idx % n);
-    K[idx] = expf(-D[(int64_t)(row0 + i) * n + j] / h);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+  // K rows and s_i = sum_j K_ij: one warp per own row; lane l sums j = l, l+32, ... ascending, then a
+  // fixed xor tree (the order depends only on n)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int i = warp; i < nl; i += nwarps) {
+    const float* drow = D + (int64_t)(row0 + i) * n;
+    float* krow = K + (int64_t)i * n;
     float acc = 0.f;
-    for (int j = 0; j < n; ++j) acc += K[(int64_t)i * n + j];
-    srow[i] = acc;
+    for (int j = lane; j < n; j += 32) {
+      const float kv = expf(-drow[j] / h);
+      krow[j] = kv;
+      acc += kv;
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if (lane == 0) srow[i] = acc;
   }
 }
 void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c_ln, float bw_h, float* h, float* K,
                       float* srow, cudaStream_t s) {
-  bandwidth_kernel_impl<<<1, 1024, 0, s>>>(D, n, row0, nl, rule, c_ln, bw_h, h, K, srow);
+  const int64_t m = (int64_t)n * (n - 1) / 2;
+  const int use_tri = rule != PUSH_BW_FIXED && n > 1 && m <= kTriKeys;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(bandwidth_kernel_impl, cudaFuncAttributeMaxDynamicSharedMemorySize, kTriKeys * 4);
+    attr = true;
+  }
+  bandwidth_kernel_impl<<<1, 1024, use_tri ? (size_t)m * 4 : 0, s>>>(D, n, row0, nl, rule, c_ln, bw_h, h, K, srow,
+                                                                    use_tri);
 }
 
 // ---------------------------------------------------------------- a10 fused update

@@ -90,7 +90,14 @@ static push_status validate(const push_config* c, int world) {
   return PUSH_OK;
 }
 
-static int wgrad_splits(int B) { return gemm::effective_splits(B, std::min(8, std::max(1, B / 1024))); }
+// Split-K count of a weight-gradient GEMM (K = B): enough splits that one particle's layer has >= 32
+// 128x128 output tiles, at most 8 and at most one per 1024 rows.  It depends only on (B, layer shape),
+// never on the number of particles per rank, so the dW summation order is the same for every P.
+static int wgrad_splits(int B, int out, int in) {
+  const int tiles = ((out + 127) / 128) * ((in + 127) / 128);
+  const int want = std::min({8, std::max(1, B / 1024), std::max(1, (32 + tiles - 1) / tiles)});
+  return gemm::effective_splits(B, want);
+}
 
 static push_status make_plan(const push_config* c, int world, Plan* p) {
   push_status st = validate(c, world);
@@ -456,7 +463,7 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
     const float* dl = c->dlt[xb];
     const ActView ap = layer_input(c, l, x);
     if (lp.gemm) {
-      const int S = wgrad_splits(B);
+      const int S = wgrad_splits(B, lp.out, lp.in);
       gemm::Problem pb;
       pb.M = lp.out; pb.N = lp.in; pb.K = B; pb.batch = nl; pb.splits = S; pb.passes = 3;
       pb.A = gemm::Operand{dl, nullptr, true, true, lp.out, P.dlt_pst};

@@ -74,7 +74,8 @@ def test_grads_match_oracle(n, dims, B, act, prior, sigma, lam, data):
 
 
 # ------------------------------------------------------------------ kernel phase a7-a10
-@pytest.mark.parametrize("n,d", [(1, 100), (2, 37), (3, 1000), (16, 5000), (33, 777), (64, 2048), (100, 96)])
+@pytest.mark.parametrize("n,d", [(1, 100), (2, 37), (3, 1000), (16, 5000), (33, 777), (64, 2048), (100, 96),
+                                 (300, 64), (8, 70001)])
 def test_step_from_set_grads_matches_oracle(n, d):
     Th = synth.random_theta(n, d, seed=n + d, scale=0.2)
     G = synth.random_grads(n, d, seed=n * d)
@@ -99,7 +100,7 @@ def cfg_dims(cfg):
     return [cfg.dims[i] for i in range(cfg.n_layers + 1)]
 
 
-@pytest.mark.parametrize("n", [2, 9, 16, 25])
+@pytest.mark.parametrize("n", [2, 3, 4, 9, 16, 25, 300])
 def test_bandwidth_bit_exact_on_dyadic_lattice(n):
     """Dyadic Theta: every D_ij is exact in fp32 and fp64, so the GPU median equals the
     oracle's bit for bit and h = fp32(med) * fp32(1/ln n) (R4)."""
