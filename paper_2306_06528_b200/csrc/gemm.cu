@@ -511,29 +511,34 @@ __global__ void __launch_bounds__(kThreads, 1)
 // aempty and tfull barriers.
 constexpr int k2Warps = 16, k2Threads = 32 * k2Warps;
 constexpr int k2XfWarp0 = 4, k2EpiWarp0 = 8;
-constexpr int k2BN = 256, k2CW = 128;
-
+// PBN = pair tile width: 256 (one TMEM accumulator of 256 columns, 128 columns per epilogue thread)
+// or 128 (two rotating accumulators of 128 columns, so the fused epilogue overlaps the next tile, and
+// 32-KB stages, so 6 of them fit).
+template <int PBN>
 struct Cfg2 {
   static constexpr int A_BYTES = BM * BK * 4;
-  static constexpr int B_BYTES = (k2BN / 2) * BK * 4;
+  static constexpr int B_BYTES = (PBN / 2) * BK * 4;
   static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;
   static constexpr int EPI_BYTES = kEpiWarps * kEpiBox;
   static constexpr int BAR_BYTES = 512;
   static constexpr int STAGES_RAW = (kMaxSmem - 1024 - EPI_BYTES - BAR_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
   static constexpr int NSLOT = 4;
-  static constexpr int ASLOT0 = k2BN;  // accumulator: columns [0, 256); A slots: [256, 512)
+  static constexpr int NACC = PBN == 256 ? 1 : 2;
+  static constexpr int CW = PBN / 2;          // accumulator columns per epilogue thread
+  static constexpr int ASLOT0 = NACC * PBN;   // accumulators: [0, 256); A slots: [256, 512)
   static constexpr int TMEM_COLS = 512;
   static constexpr int SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
   static_assert(STAGES >= 2 && SMEM_BYTES <= kMaxSmem, "smem");
 };
 
-template <bool AMN, bool BMN, bool BSPLIT>
+template <int PBN, bool AMN, bool BMN, bool BSPLIT>
 __global__ void __launch_bounds__(k2Threads, 1)
     gemm3xtf32_2sm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tBhi,
                           const __grid_constant__ CUtensorMap tBlo, const __grid_constant__ CUtensorMap tOut,
                           const __grid_constant__ CUtensorMap tAux, const KParams prm) {
-  using C = Cfg2;
+  using C = Cfg2<PBN>;
+  constexpr int k2BN = PBN, k2CW = C::CW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ebuf_all = smem + C::STAGES * C::STAGE_BYTES;
@@ -541,9 +546,9 @@ __global__ void __launch_bounds__(k2Threads, 1)
   uint64_t* ready = full + C::STAGES;     // leader: both CTAs' transforms done with stage s
   uint64_t* empty = ready + C::STAGES;    // the pair's MMAs reading stage s have completed
   uint64_t* aempty = empty + C::STAGES;   // [NSLOT] the MMAs reading TMEM A slot j have completed
-  uint64_t* tfull = aempty + C::NSLOT;    // the accumulator holds a finished K-chunk
-  uint64_t* tempty = tfull + 1;           // leader: both CTAs have drained the accumulator
-  uint64_t* auxbar = tempty + 1;          // [kEpiWarps]
+  uint64_t* tfull = aempty + C::NSLOT;    // [NACC] accumulator b holds a finished K-chunk
+  uint64_t* tempty = tfull + C::NACC;     // [NACC] leader: both CTAs have drained accumulator b
+  uint64_t* auxbar = tempty + C::NACC;    // [kEpiWarps]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -557,8 +562,10 @@ __global__ void __launch_bounds__(k2Threads, 1)
       ptx::mbar_init(&empty[s], 1);
     }
     for (int j = 0; j < C::NSLOT; ++j) ptx::mbar_init(&aempty[j], 1);
-    ptx::mbar_init(tfull, 1);
-    ptx::mbar_init(tempty, 2 * kEpiWarps);  // one arrival per epilogue warp of each CTA
+    for (int b = 0; b < C::NACC; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], 2 * kEpiWarps);  // one arrival per epilogue warp of each CTA
+    }
     for (int e = 0; e < kEpiWarps; ++e) ptx::mbar_init(&auxbar[e], 1);
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tA);
@@ -634,7 +641,8 @@ __global__ void __launch_bounds__(k2Threads, 1)
         for (int i = 0; i < nkb; ++i, ++it) {
           const bool first = (i % kChunkKB) == 0;
           const bool last = (i % kChunkKB) == kChunkKB - 1 || i == nkb - 1;
-          if (first) ptx::mbar_wait(tempty, (ch & 1) ^ 1);
+          const int b = ch % C::NACC;
+          if (first) ptx::mbar_wait(&tempty[b], ((ch / C::NACC) & 1) ^ 1);
           const int s = it % C::STAGES;
           const int slot = it % C::NSLOT;
           ptx::mbar_wait(&ready[s], (it / C::STAGES) & 1);
@@ -642,23 +650,24 @@ __global__ void __launch_bounds__(k2Threads, 1)
           const uint32_t b_hi = ptx::smem_u32(smem + s * C::STAGE_BYTES) + C::A_BYTES;
           const uint32_t b_lo = b_hi + C::B_BYTES;
           const uint32_t ta_hi = tmem_base + C::ASLOT0 + slot * 64, ta_lo = ta_hi + 32;
+          const uint32_t d = tmem_base + b * PBN;
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {
             const uint64_t dbh = op_desc<BMN>(b_hi, ks), dbl = op_desc<BMN>(b_lo, ks);
             const uint32_t acc = (first && ks == 0) ? 0u : 1u;
             if (prm.dbg & 4) {
             } else if (prm.passes == 3) {
-              ptx::mma2_tf32_ts(tmem_base, ta_lo + ks * 8, dbh, idesc, acc);
-              ptx::mma2_tf32_ts(tmem_base, ta_hi + ks * 8, dbl, idesc, 1u);
-              ptx::mma2_tf32_ts(tmem_base, ta_hi + ks * 8, dbh, idesc, 1u);
+              ptx::mma2_tf32_ts(d, ta_lo + ks * 8, dbh, idesc, acc);
+              ptx::mma2_tf32_ts(d, ta_hi + ks * 8, dbl, idesc, 1u);
+              ptx::mma2_tf32_ts(d, ta_hi + ks * 8, dbh, idesc, 1u);
             } else {
-              ptx::mma2_tf32_ts(tmem_base, ta_hi + ks * 8, dbh, idesc, acc);
+              ptx::mma2_tf32_ts(d, ta_hi + ks * 8, dbh, idesc, acc);
             }
           }
           ptx::mma2_commit_mc(&empty[s], 3);
           ptx::mma2_commit_mc(&aempty[slot], 3);
           if (last) {
-            ptx::mma2_commit_mc(tfull, 3);
+            ptx::mma2_commit_mc(&tfull[b], 3);
             ++ch;
           }
         }
@@ -721,13 +730,13 @@ __global__ void __launch_bounds__(k2Threads, 1)
     }
   } else {
     // ---------------- epilogue warps (warpgroups 2-3): quarter q, column half h of the 256 columns
-    ptx::setmaxnreg_inc<184>();  // the 128-column fp32 running sum lives in registers
+    ptx::setmaxnreg_inc<184>();  // the fp32 running sum (up to 128 columns) lives in registers
     const int e = warp - k2EpiWarp0;
     const int q = warp & 3;
     const int h = e >> 2;
     const uint32_t ebuf_s = ptx::smem_u32(ebuf_all + e * kEpiBox);
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-    const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(tempty), 0);
+    const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(tempty), 0);  // + 8 * b for accumulator b
     uint32_t ch = 0, aux_ph = 0;
     const bool bwd = prm.epi == EPI_BWD;
     for (int t = cid; t < prm.ntiles; t += ncl) {
@@ -748,19 +757,20 @@ __global__ void __launch_bounds__(k2Threads, 1)
 #pragma unroll
       for (int j = 0; j < k2CW; ++j) acc[j] = 0.f;
       for (int c = 0; c < nchunks; ++c, ++ch) {
-        ptx::mbar_wait(tfull, ch & 1);
+        const int b = ch % C::NACC;
+        ptx::mbar_wait(&tfull[b], (ch / C::NACC) & 1);
         ptx::tc_fence_after();
 #pragma unroll
         for (int c0 = 0; c0 < k2CW; c0 += 16) {
           uint32_t r[16];
-          ptx::tmem_ld_32x32b_x16(lane_base + h * k2CW + c0, r);
+          ptx::tmem_ld_32x32b_x16(lane_base + b * PBN + h * k2CW + c0, r);
           ptx::tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 16; ++j) acc[c0 + j] += __uint_as_float(r[j]);
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader, 1);
+        if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * b, 1);
       }
       if (!live || (prm.dbg & 2)) continue;
       const int pz = prm.epi == EPI_STORE ? split * prm.batch + p : p;
@@ -855,10 +865,10 @@ push_status launch_bn(bool amn, bool bmn, bool bs, const CUtensorMap* maps, cons
     default: return launch_t<BN, true, true, true>(maps, kp, s);
   }
 }
-template <bool AMN, bool BMN, bool BS>
+template <int PBN, bool AMN, bool BMN, bool BS>
 push_status launch2_t(const CUtensorMap* maps, const KParams& kp, cudaStream_t stream) {
   static int max_pairs = 0;
-  auto kern = gemm3xtf32_2sm_kernel<AMN, BMN, BS>;
+  auto kern = gemm3xtf32_2sm_kernel<PBN, AMN, BMN, BS>;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -866,12 +876,12 @@ push_status launch2_t(const CUtensorMap* maps, const KParams& kp, cudaStream_t s
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.blockDim = dim3(k2Threads);
-  cfg.dynamicSmemBytes = Cfg2::SMEM_BYTES;
+  cfg.dynamicSmemBytes = Cfg2<PBN>::SMEM_BYTES;
   cfg.stream = stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (!max_pairs) {
-    PUSH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM_BYTES));
+    PUSH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<PBN>::SMEM_BYTES));
     cfg.gridDim = dim3(g_sms);
     int n = 0;
     PUSH_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
@@ -883,17 +893,18 @@ push_status launch2_t(const CUtensorMap* maps, const KParams& kp, cudaStream_t s
   return PUSH_OK;
 }
 
+template <int PBN>
 push_status launch2(bool amn, bool bmn, bool bs, const CUtensorMap* maps, const KParams& kp, cudaStream_t s) {
   const int key = (amn ? 4 : 0) | (bmn ? 2 : 0) | (bs ? 1 : 0);
   switch (key) {
-    case 0: return launch2_t<false, false, false>(maps, kp, s);
-    case 1: return launch2_t<false, false, true>(maps, kp, s);
-    case 2: return launch2_t<false, true, false>(maps, kp, s);
-    case 3: return launch2_t<false, true, true>(maps, kp, s);
-    case 4: return launch2_t<true, false, false>(maps, kp, s);
-    case 5: return launch2_t<true, false, true>(maps, kp, s);
-    case 6: return launch2_t<true, true, false>(maps, kp, s);
-    default: return launch2_t<true, true, true>(maps, kp, s);
+    case 0: return launch2_t<PBN, false, false, false>(maps, kp, s);
+    case 1: return launch2_t<PBN, false, false, true>(maps, kp, s);
+    case 2: return launch2_t<PBN, false, true, false>(maps, kp, s);
+    case 3: return launch2_t<PBN, false, true, true>(maps, kp, s);
+    case 4: return launch2_t<PBN, true, false, false>(maps, kp, s);
+    case 5: return launch2_t<PBN, true, false, true>(maps, kp, s);
+    case 6: return launch2_t<PBN, true, true, false>(maps, kp, s);
+    default: return launch2_t<PBN, true, true, true>(maps, kp, s);
   }
 }
 
@@ -904,9 +915,17 @@ bool force_1sm() {
   }();
   return v != 0;
 }
-bool force_pair() {
+// PUSH_GEMM_PAIR=1: 256-wide pair tiles wherever N % 256 == 0; =2: 128-wide pair tiles for the rest
+int force_pair() {
   static const int v = [] {
     const char* e = getenv("PUSH_GEMM_PAIR");
+    return e && *e ? atoi(e) : 0;
+  }();
+  return v;
+}
+bool pair128_default() {
+  static const int v = [] {
+    const char* e = getenv("PUSH_GEMM_PAIR128");
     return e && *e && *e != '0' ? 1 : 0;
   }();
   return v != 0;
@@ -939,10 +958,12 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   // forward); at K = 256 the 1-CTA kernel's two TMEM accumulators overlap the fused epilogue better
   // (C2 forward 129 vs 150 us) (profiles/r01_gemm.md).  PUSH_GEMM_1SM=1
   // forces the 1-CTA kernel, PUSH_GEMM_PAIR=1 the pair kernel wherever N % 256 == 0 (A/B comparisons).
-  const bool pair = pb.N % k2BN == 0 && !(pb.passes >> 8 & (1 | 8)) && !force_1sm() &&
-                    (pb.epi == EPI_STORE || pb.K >= 512 || force_pair());
-  const int BN = pair ? k2BN : choose_bn(pb.N);
-  const int box_b = pair ? k2BN / 2 : BN;
+  const bool dbg_ok = !(pb.passes >> 8 & (1 | 8)) && !force_1sm();
+  const bool pair256 = dbg_ok && pb.N % 256 == 0 && (pb.epi == EPI_STORE || pb.K >= 512 || force_pair() == 1);
+  const bool pair128 = dbg_ok && !pair256 && pb.N % 128 == 0 && (force_pair() == 2 || pair128_default());
+  const bool pair = pair256 || pair128;
+  const int BN = pair256 ? 256 : (pair128 ? 128 : choose_bn(pb.N));
+  const int box_b = pair ? BN / 2 : BN;
   const int nkb = (pb.K + BK - 1) / BK;
   const int kbps = (nkb + pb.splits - 1) / pb.splits;
   if ((nkb + kbps - 1) / kbps != pb.splits) return fail(PUSH_E_SHAPE, "gemm: split count leaves an empty split");
@@ -976,7 +997,8 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   kp.bpart = pb.bpart; kp.bp_sstride = pb.bp_sstride; kp.bp_pstride = pb.bp_pstride;
   kp.x = pb.x; kp.din = pb.xpart ? pb.din : 0; kp.xpart = pb.xpart;
   kp.xp_sstride = pb.xp_sstride; kp.xp_pstride = pb.xp_pstride;
-  if (pair) return launch2(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
+  if (pair256) return launch2<256>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
+  if (pair128) return launch2<128>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
   if (BN == 128) return launch_bn<128>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
   if (BN == 64) return launch_bn<64>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
   return launch_bn<32>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);

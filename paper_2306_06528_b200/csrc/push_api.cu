@@ -322,7 +322,7 @@ static push_status exchange(push_ctx* c, int kind, cudaStream_t s) {
   float* buf = buf_of(c, kind, &cnt);
   if (kind == BUF_LOSS)
     PUSH_CUDA_TRY(cudaMemcpyAsync(buf + c->rank * cnt, c->loss, cnt * 4, cudaMemcpyDeviceToDevice, s));
-  if (c->world == 1) return PUSH_OK;
+  if (c->world == 1 && !c->comm) return PUSH_OK;
   const double bytes = 4.0 * cnt * (c->world - 1);
   if (c->group) {
     return run_k(c, PC_EXCHANGE, 0, bytes, 0, s, [&]() -> push_status {
@@ -376,7 +376,7 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
   // C1: Theta rows of every rank (needed by a7/a10; unchanged during the gradient phase, whose kernels
   // only read the own rows, which the in-place all-gather only reads): on the comm stream, joined in
   // push_svgd_step
-  if (c->world > 1) {
+  if (c->world > 1 || c->comm) {
     PUSH_CUDA_TRY(cudaEventRecord(c->ev_fork, s));
     PUSH_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
     if ((st = exchange(c, BUF_THETA, c->comm_stream)) != PUSH_OK) return st;
@@ -664,6 +664,14 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
 
 }  // namespace push
 
+static bool force_nccl() {
+  static const int v = [] {
+    const char* e = getenv("PUSH_FORCE_NCCL");
+    return e && *e && *e != '0' ? 1 : 0;
+  }();
+  return v != 0;
+}
+
 using namespace push;
 
 // ================================================================== C ABI
@@ -705,6 +713,12 @@ push_status push_init(const push_config* cfg, int32_t rank, int32_t world_size, 
     nccl::UniqueId u;
     std::memcpy(u.internal, nccl_id, 128);
     st = nccl::comm_init_rank(&c->comm, world_size, u, rank);
+  } else if (st == PUSH_OK && force_nccl()) {
+    // test hook (PUSH_FORCE_NCCL=1): a single-rank NCCL communicator, so that one GPU exercises the
+    // NCCL exchange path (comm stream, in-place all-gathers, graph capture of NCCL calls)
+    nccl::UniqueId u;
+    st = nccl::get_unique_id(&u);
+    if (st == PUSH_OK) st = nccl::comm_init_rank(&c->comm, 1, u, 0);
   }
   if (st != PUSH_OK) {
     delete c;
