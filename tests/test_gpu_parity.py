@@ -292,3 +292,32 @@ def test_c2_full_size_sampled_parity():
     ref, info = osvgd.svgd_step(th0, g.astype(np.float64), 1e-3)
     assert rel_err(ctx.gather("theta"), ref) <= 1e-4
     assert float(ctx.gather("h")[0]) == pytest.approx(info["h"], rel=1e-5)
+
+
+@pytest.mark.parametrize("cfgname", ["S1"])
+def test_full_size_sampled_parity_graph_path(cfgname):
+    """North-star point S1 (64 particles x 1,053,185 params, B = 8192) through the bench's launch path
+    (push_step_graph after an eager warm-up step): g of sampled particles against the oracle one by one;
+    D, h bit-compatible with the oracle's definition; theta' on sampled columns against the oracle's
+    phi (column-separable) with the oracle's own K and h computed from the full Theta."""
+    w = WORKLOADS[cfgname]
+    dims = list(w.dims)
+    ctx = push.Context(push.make_config(w.n_particles, dims, max_batch=w.batch, step_size=1e-3, seed=0))
+    x0, y0 = synth.workload_batch(w, 0)
+    ctx.step_graph(_dev(x0), _dev(y0))          # eager warm-up step (first call)
+    x, y = synth.workload_batch(w, 1)
+    th0 = ctx.gather("theta").astype(np.float64)
+    ctx.step_graph(_dev(x), _dev(y))            # captured graph
+    g = ctx.gather("grad")
+    for i in (0, w.n_particles - 1):
+        gref, _ = omlp.grad_log_post(th0[i], dims, x, y)
+        assert inf_rel(g[i:i + 1], gref[None]) <= 1e-5, i
+    D = osvgd.sq_dists(th0)
+    h = osvgd.bandwidth(D)
+    assert float(ctx.gather("h")[0]) == pytest.approx(h, rel=1e-5)
+    K = osvgd.kernel_matrix(D, h)
+    rng = np.random.default_rng(0)
+    cols = np.sort(rng.choice(th0.shape[1], 4096, replace=False))
+    ref = th0[:, cols] + 1e-3 * osvgd.phi(th0[:, cols], g[:, cols].astype(np.float64), K, h)
+    th1 = ctx.gather("theta")[:, cols]
+    assert rel_err(th1, ref) <= 1e-4
