@@ -65,9 +65,20 @@ struct PartView {
 };
 // G_p[off_w + o*in + i] = -lambda * sum_s W(s,p,o,i) + prior(theta)   (o < out, i < in)
 // G_p[off_b + o]        = -lambda * sum_s Bv(s,p,o,0) + prior(theta)
-// Returns the number of kernels launched (1 or 2).
-int finalize_layer(PartView W, PartView Bv, const float* theta, float* grad, int64_t ld, int64_t off_w, int in,
-                   int out, float lambda, int prior, float inv_sigma2, int batch, cudaStream_t s);
+// G_p[off_w + o*in + i] = -lambda * sum_s W(s,p,o,i) + prior(theta), G_p[off_b + o] likewise from Bv, for every
+// layer job in ONE launch (issued after the backward pass; the partial buffers are per layer).
+struct FinalizeJob {
+  PartView W, Bv;
+  int64_t off_w;
+  int in, out;
+  int nb_w, nb_b;        // blocks for the weight / bias parts
+  int w_warp, b_warp;    // 0 thread per element, 1 warp per element, 2 thread per 4 elements (weights)
+  int blk0;              // first block of this job (set by finalize_all)
+};
+constexpr int kMaxFinalizeJobs = 16;
+FinalizeJob make_finalize_job(const PartView& W, const PartView& Bv, int64_t off_w, int in, int out);
+void finalize_all(const FinalizeJob* jobs, int njobs, const float* theta, float* grad, int64_t ld, float lambda,
+                  int prior, float inv_sigma2, int batch, cudaStream_t s);
 
 // ---------------------------------------------------------------- K0 init (R14)
 struct InitTable {

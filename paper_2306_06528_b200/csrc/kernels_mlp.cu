@@ -294,56 +294,128 @@ __device__ __forceinline__ void finalize_store(const float* theta, float* grad, 
   const float pr = (prior == PUSH_PRIOR_GAUSSIAN) ? -theta[idx] * inv_sigma2 : 0.f;
   grad[idx] = fmaf(-lambda, v, pr);
 }
-// One launch per layer: blocks [0, nb_w) reduce the weight partials, blocks [nb_w, ...) the bias
-// partials, each part with the thread- or warp-per-element scheme its partial count calls for.
+// Sum of `splits` partials at stride ss in a fixed order that depends only on `splits`: ascending for
+// splits <= 8, else 8 interleaved ascending chains (s = u mod 8) combined by a fixed tree (loads in flight).
+template <typename V>
+__device__ __forceinline__ V vadd(V a, V b);
+template <>
+__device__ __forceinline__ float vadd(float a, float b) { return a + b; }
+template <>
+__device__ __forceinline__ float4 vadd(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+template <typename V>
+__device__ __forceinline__ V sum_partials(const V* src, int splits, int64_t ss_v) {
+  V zero;
+  memset(&zero, 0, sizeof(V));
+  if (splits <= 8) {
+    V v = zero;
+    for (int s = 0; s < splits; ++s) v = vadd(v, __ldg(src + s * ss_v));
+    return v;
+  }
+  V a[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) a[u] = zero;
+  int s = 0;
+  for (; s + 8 <= splits; s += 8)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = vadd(a[u], __ldg(src + (s + u) * ss_v));
+  for (int u = 0; s + u < splits; ++u) a[u] = vadd(a[u], __ldg(src + (s + u) * ss_v));
+  return vadd(vadd(vadd(a[0], a[1]), vadd(a[2], a[3])), vadd(vadd(a[4], a[5]), vadd(a[6], a[7])));
+}
+// mode 0: thread per element, 1: warp per element, 2: thread per 4 consecutive elements (float4)
 __device__ __forceinline__ void finalize_range(const PartView& W, const PartView& Bv, const float* theta,
                                                float* grad, int64_t ld, int64_t off_w, int nin, int nout,
-                                               int64_t t0, int64_t t1, bool warp_mode, int64_t blk, float lambda,
+                                               int64_t t0, int64_t t1, int mode, int64_t blk, float lambda,
                                                int prior, float inv_sigma2, int p) {
   const int64_t nw = (int64_t)nin * nout;
   const int lane = threadIdx.x & 31;
-  const int64_t t = warp_mode ? t0 + (blk * blockDim.x + threadIdx.x) / 32 : t0 + blk * blockDim.x + threadIdx.x;
+  if (mode == 2) {
+    const int64_t t = t0 + 4 * (blk * blockDim.x + threadIdx.x);
+    if (t >= t1) return;
+    int splits;
+    int64_t ss;
+    const float* src = part_ptr(W, Bv, p, t, nin, nw, &splits, &ss);
+    const float4 v = sum_partials(reinterpret_cast<const float4*>(src), splits, ss / 4);
+    const int64_t idx = p * ld + off_w + t;
+    float4 pr = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (prior == PUSH_PRIOR_GAUSSIAN) {
+      const float4 th = *reinterpret_cast<const float4*>(theta + idx);
+      pr = make_float4(-th.x * inv_sigma2, -th.y * inv_sigma2, -th.z * inv_sigma2, -th.w * inv_sigma2);
+    }
+    *reinterpret_cast<float4*>(grad + idx) = make_float4(fmaf(-lambda, v.x, pr.x), fmaf(-lambda, v.y, pr.y),
+                                                         fmaf(-lambda, v.z, pr.z), fmaf(-lambda, v.w, pr.w));
+    return;
+  }
+  const int64_t t = mode == 1 ? t0 + (blk * blockDim.x + threadIdx.x) / 32 : t0 + blk * blockDim.x + threadIdx.x;
   if (t >= t1) return;
   int splits;
   int64_t ss;
   const float* src = part_ptr(W, Bv, p, t, nin, nw, &splits, &ss);
   float v = 0.f;
-  if (warp_mode) {
+  if (mode == 1) {
     for (int s = lane; s < splits; s += 32) v += src[s * ss];
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
     if (lane != 0) return;
   } else {
-    for (int s = 0; s < splits; ++s) v += src[s * ss];
+    v = sum_partials(src, splits, ss);
   }
   finalize_store(theta, grad, p * ld + off_w + t, v, lambda, prior, inv_sigma2);
 }
-__global__ void finalize_kernel(PartView W, PartView Bv, const float* __restrict__ theta, float* __restrict__ grad,
-                                int64_t ld, int64_t off_w, int nin, int nout, int nb_w, bool w_warp, bool b_warp,
-                                float lambda, int prior, float inv_sigma2) {
+// All layers in one launch: block b of the grid belongs to the job whose [blk0, blk0 + nb_w + nb_b)
+// range contains it; within a job, blocks [0, nb_w) reduce the weight partials and the rest the bias
+// partials, each part with the thread- or warp-per-element scheme its partial count calls for.
+struct FinalizeTable {
+  FinalizeJob j[kMaxFinalizeJobs];
+  int n;
+};
+__global__ void finalize_all_kernel(const FinalizeTable t, const float* __restrict__ theta, float* __restrict__ grad,
+                                    int64_t ld, float lambda, int prior, float inv_sigma2) {
   const int p = blockIdx.y;
-  const int64_t nw = (int64_t)nin * nout;
-  if ((int)blockIdx.x < nb_w)
-    finalize_range(W, Bv, theta, grad, ld, off_w, nin, nout, 0, nw, w_warp, blockIdx.x, lambda, prior, inv_sigma2, p);
+  int k = 0;
+  while (k + 1 < t.n && (int)blockIdx.x >= t.j[k + 1].blk0) ++k;
+  const FinalizeJob& J = t.j[k];
+  const int b = blockIdx.x - J.blk0;
+  const int64_t nw = (int64_t)J.in * J.out;
+  if (b < J.nb_w)
+    finalize_range(J.W, J.Bv, theta, grad, ld, J.off_w, J.in, J.out, 0, nw, J.w_warp, b, lambda, prior, inv_sigma2,
+                   p);
   else
-    finalize_range(W, Bv, theta, grad, ld, off_w, nin, nout, nw, nw + nout, b_warp, blockIdx.x - nb_w, lambda, prior,
-                   inv_sigma2, p);
+    finalize_range(J.W, J.Bv, theta, grad, ld, J.off_w, J.in, J.out, nw, nw + J.out, J.b_warp, b - J.nb_w, lambda,
+                   prior, inv_sigma2, p);
 }
-int finalize_layer(PartView W, PartView Bv, const float* theta, float* grad, int64_t ld, int64_t off_w, int in,
-                   int out, float lambda, int prior, float inv_sigma2, int batch, cudaStream_t s) {
-  const int64_t nw = (int64_t)in * out;
+FinalizeJob make_finalize_job(const PartView& W, const PartView& Bv, int64_t off_w, int in, int out) {
   // warp-per-element only pays off for few elements: it reads each partial row strided (uncoalesced);
-  // thread-per-element reads one contiguous row of elements per partial
+  // thread-per-element reads one contiguous row of elements per partial, float4-wide when aligned
   auto warp_mode = [](int64_t elems, int splits) { return splits > kThreadSplits && elems < 32768; };
-  const int Wsp = warp_mode(nw, W.splits) ? W.splits : 1, Bsp = warp_mode(out, Bv.splits) ? Bv.splits : 1;
-  auto blocks = [](int64_t elems, int wsplits) {
-    return (unsigned)(wsplits > kThreadSplits ? (elems + 7) / 8 : (elems + 255) / 256);
+  FinalizeJob j{};
+  j.W = W;
+  j.Bv = Bv;
+  j.off_w = off_w;
+  j.in = in;
+  j.out = out;
+  const int64_t nw = (int64_t)in * out;
+  const bool v4 = in % 4 == 0 && off_w % 4 == 0 && W.pstride % 4 == 0 && W.sstride % 4 == 0 && W.ostride % 4 == 0 &&
+                  (reinterpret_cast<uintptr_t>(W.base) & 15) == 0;
+  j.w_warp = warp_mode(nw, W.splits) ? 1 : (v4 ? 2 : 0);
+  j.b_warp = warp_mode(out, Bv.splits) ? 1 : 0;
+  auto blocks = [](int64_t elems, int mode) {
+    return (int)(mode == 1 ? (elems + 7) / 8 : (mode == 2 ? (elems / 4 + 255) / 256 : (elems + 255) / 256));
   };
-  const unsigned nb_w = blocks(nw, Wsp), nb_b = blocks(out, Bsp);
-  finalize_kernel<<<dim3(nb_w + nb_b, batch), 256, 0, s>>>(W, Bv, theta, grad, ld, off_w, in, out, (int)nb_w,
-                                                           Wsp > kThreadSplits, Bsp > kThreadSplits, lambda, prior,
-                                                           inv_sigma2);
-  return 1;
+  j.nb_w = blocks(nw, j.w_warp);
+  j.nb_b = blocks(out, j.b_warp);
+  return j;
+}
+void finalize_all(const FinalizeJob* jobs, int njobs, const float* theta, float* grad, int64_t ld, float lambda,
+                  int prior, float inv_sigma2, int batch, cudaStream_t s) {
+  FinalizeTable t{};
+  t.n = njobs;
+  int blk = 0;
+  for (int k = 0; k < njobs; ++k) {
+    t.j[k] = jobs[k];
+    t.j[k].blk0 = blk;
+    blk += jobs[k].nb_w + jobs[k].nb_b;
+  }
+  finalize_all_kernel<<<dim3(blk, batch), 256, 0, s>>>(t, theta, grad, ld, lambda, prior, inv_sigma2);
 }
 
 // ---------------------------------------------------------------- set_grads copy

@@ -55,13 +55,15 @@ struct Plan {
   int64_t wsplit_total = 0;                 // per particle elements of the hi/lo weight copies
   std::vector<int64_t> act_pst;             // per layer 0..L-2 activation particle stride
   int64_t dlt_pst = 0;                      // delta buffer particle stride
-  int64_t wpart_elems = 0, tpart_elems = 0;
+  int64_t wpart_elems = 0, tpart_elems = 0;  // (unused totals kept for reference)
   bool fuse_x0 = false;                     // layer 0 thin + layer 1 GEMM: dW_0 from layer 1's BWD epilogue
   kern::DistPlan dist{};
   // byte offsets into the workspace
-  size_t o_theta0, o_theta1, o_grad, o_whi, o_wlo, o_dlt0, o_dlt1, o_err2, o_loss, o_loss_all, o_wpart, o_tpart,
-      o_bpart0, o_bpart1, o_opw, o_opb, o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf;
+  size_t o_theta0, o_theta1, o_grad, o_whi, o_wlo, o_dlt0, o_dlt1, o_err2, o_loss, o_loss_all, o_opw, o_opb,
+      o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf;
   std::vector<size_t> o_act;
+  // per-layer partial buffers, all alive until the single finalize launch at the end of a5
+  std::vector<size_t> o_wpart, o_tpart, o_bpart;
   size_t total = 0;
 };
 
@@ -170,10 +172,16 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.o_err2 = take((int64_t)P.nl * P.Bmax);
   P.o_loss = take(P.nl);
   P.o_loss_all = take(P.n);
-  P.o_wpart = take(P.wpart_elems);
-  P.o_tpart = take(P.tpart_elems);
-  P.o_bpart0 = take((int64_t)P.RB * P.nl * P.Hmax);
-  P.o_bpart1 = take((int64_t)P.RB * P.nl * P.Hmax);
+  P.o_wpart.assign(P.L, 0);
+  P.o_tpart.assign(P.L, 0);
+  P.o_bpart.assign(P.L, 0);
+  for (int l = 0; l < P.L; ++l) {
+    const LayerPlan& lp = P.layers[l];
+    if (lp.gemm) P.o_wpart[l] = take((int64_t)wgrad_splits(P.Bmax, lp.out, lp.in) * P.nl * lp.in * lp.out);
+    // thin weight partials (thin hidden layers) or bias-only column sums (GEMM layers under a thin one)
+    if (l < P.L - 1) P.o_tpart[l] = take((int64_t)chunks_max * P.nl * lp.out * (lp.gemm ? 1 : lp.in + 1));
+    if (l < P.L - 1) P.o_bpart[l] = take((int64_t)P.RB * P.nl * lp.out);
+  }
   P.o_opw = take((int64_t)P.RB * P.nl * top.out * top.in);
   P.o_opb = take((int64_t)P.RB * P.nl * top.out);
   P.o_xpart = take(P.fuse_x0 ? (int64_t)P.RB * P.nl * P.layers[0].out * P.layers[0].in : 1);
@@ -223,8 +231,9 @@ struct push_ctx {
   float *whi = nullptr, *wlo = nullptr;
   std::vector<float*> act;             // activations A_0 .. A_{L-2}
   float* dlt[2] = {nullptr, nullptr};  // delta ping-pong
-  float *err2 = nullptr, *loss = nullptr, *loss_all = nullptr, *wpart = nullptr, *tpart = nullptr;
-  float *bpart[2] = {nullptr, nullptr}, *opw = nullptr, *opb = nullptr, *xpart = nullptr;
+  float *err2 = nullptr, *loss = nullptr, *loss_all = nullptr;
+  std::vector<float*> wpart, tpart, bpart;  // per layer
+  float *opw = nullptr, *opb = nullptr, *xpart = nullptr;
   float *dpart = nullptr, *D = nullptr, *K = nullptr, *srow = nullptr, *h = nullptr;
   float *xbuf = nullptr, *ybuf = nullptr;
   int state = 0;  // 0 READY, 1 GRADS_READY
@@ -362,15 +371,12 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
   const float lambda = c->cfg.lik_scale;
   const float inv_s2 = c->cfg.prior == PUSH_PRIOR_GAUSSIAN ? 1.0f / (c->cfg.prior_sigma * c->cfg.prior_sigma) : 0.f;
   push_status st;
+  // a5 epilogue: every layer's partials are reduced into G by ONE launch after the backward pass
+  std::vector<kern::FinalizeJob> jobs;
   auto finalize = [&](int l, const kern::PartView& W, const kern::PartView& Bv) {
     const LayerPlan& lp = P.layers[l];
-    int nk = 0;
-    push_status r = run_k(c, PC_FINALIZE, 0, 0, 0, s, [&] {
-      nk = kern::finalize_layer(W, Bv, th, g, ld, lp.off_w, lp.in, lp.out, lambda, c->cfg.prior, inv_s2, nl, s);
-      return PUSH_OK;
-    });
-    c->launches += nk;
-    return r;
+    jobs.push_back(kern::make_finalize_job(W, Bv, lp.off_w, lp.in, lp.out));
+    return PUSH_OK;
   };
 
   // C1: Theta rows of every rank (needed by a7/a10; unchanged during the gradient phase, whose kernels
@@ -437,7 +443,7 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
     oa.bpart_out = c->opb; oa.bo_sstride = (int64_t)nl * lp.out; oa.bo_pstride = lp.out;
     if (L >= 2) {
       oa.dprev = c->dlt[0]; oa.dp_pstride = P.dlt_pst;
-      oa.bpart_prev = c->bpart[(L - 2) & 1]; oa.bp_sstride = (int64_t)nl * lp.in; oa.bp_pstride = lp.in;
+      oa.bpart_prev = c->bpart[L - 2]; oa.bp_sstride = (int64_t)nl * lp.in; oa.bp_pstride = lp.in;
       bias_ready[L - 2] = 1;
     }
     const double bytes = 4.0 * B * lp.in * nl * (L >= 2 ? 2 : 1);
@@ -469,21 +475,21 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
       pb.A = gemm::Operand{dl, nullptr, true, true, lp.out, P.dlt_pst};
       pb.B = gemm::Operand{ap.p, nullptr, true, true, lp.in, ap.pst};
       pb.epi = gemm::EPI_STORE;
-      pb.out = c->wpart; pb.ldo = lp.in; pb.out_pstride = (int64_t)lp.out * lp.in;
+      pb.out = c->wpart[l]; pb.ldo = lp.in; pb.out_pstride = (int64_t)lp.out * lp.in;
       pb.out_sstride = (int64_t)nl * lp.out * lp.in;
       const double fl = 2.0 * B * lp.out * (double)lp.in * nl;
       st = run_k(c, PC_WGRAD_GEMM, 1, 0, fl, s, [&] { return gemm::run(pb, s); });
       if (st != PUSH_OK) return st;
-      kern::PartView W{c->wpart, S, (int64_t)nl * lp.out * lp.in, (int64_t)lp.out * lp.in, lp.in};
-      kern::PartView Bv{c->bpart[l & 1], RB, (int64_t)nl * lp.out, lp.out, 1};
+      kern::PartView W{c->wpart[l], S, (int64_t)nl * lp.out * lp.in, (int64_t)lp.out * lp.in, lp.in};
+      kern::PartView Bv{c->bpart[l], RB, (int64_t)nl * lp.out, lp.out, 1};
       if (!bias_ready[l]) {  // delta_l came from a generic thin backward: column sums here
         int chunks = 0;
         st = run_k(c, PC_WGRAD_THIN, 1, 4.0 * B * lp.out * nl, 0, s, [&] {
-          chunks = kern::thin_wgrad(dl, P.dlt_pst, nullptr, 0, 0, lp.out, c->tpart, B, nl, s);
+          chunks = kern::thin_wgrad(dl, P.dlt_pst, nullptr, 0, 0, lp.out, c->tpart[l], B, nl, s);
           return PUSH_OK;
         });
         if (st != PUSH_OK) return st;
-        Bv = kern::PartView{c->tpart, chunks, (int64_t)nl * lp.out, lp.out, 1};
+        Bv = kern::PartView{c->tpart[l], chunks, (int64_t)nl * lp.out, lp.out, 1};
       }
       if ((st = finalize(l, W, Bv)) != PUSH_OK) return st;
     } else if (l == 0 && x0_ready) {
@@ -494,13 +500,13 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
       int chunks = 0;
       st = run_k(c, PC_WGRAD_THIN, 1, 4.0 * B * (lp.in + lp.out) * nl, 2.0 * B * lp.out * (double)(lp.in + 1) * nl,
                  s, [&] {
-                   chunks = kern::thin_wgrad(dl, P.dlt_pst, ap.p, ap.pst, lp.in, lp.out, c->tpart, B, nl, s);
+                   chunks = kern::thin_wgrad(dl, P.dlt_pst, ap.p, ap.pst, lp.in, lp.out, c->tpart[l], B, nl, s);
                    return PUSH_OK;
                  });
       if (st != PUSH_OK) return st;
       const int64_t cols = lp.in + 1;
-      kern::PartView W{c->tpart, chunks, (int64_t)nl * lp.out * cols, (int64_t)lp.out * cols, cols};
-      kern::PartView Bv{c->tpart + lp.in, chunks, (int64_t)nl * lp.out * cols, (int64_t)lp.out * cols, cols};
+      kern::PartView W{c->tpart[l], chunks, (int64_t)nl * lp.out * cols, (int64_t)lp.out * cols, cols};
+      kern::PartView Bv{c->tpart[l] + lp.in, chunks, (int64_t)nl * lp.out * cols, (int64_t)lp.out * cols, cols};
       if ((st = finalize(l, W, Bv)) != PUSH_OK) return st;
     }
     if (l == 0) break;
@@ -517,7 +523,7 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
       pb.epi = gemm::EPI_BWD; pb.act = act;
       pb.out = o; pb.ldo = lp.in; pb.out_pstride = P.dlt_pst;
       pb.aprev = aprev.p; pb.ld_aprev = lp.in; pb.aprev_pstride = aprev.pst;
-      pb.bpart = c->bpart[(l - 1) & 1]; pb.bp_sstride = (int64_t)nl * lp.in; pb.bp_pstride = lp.in;
+      pb.bpart = c->bpart[l - 1]; pb.bp_sstride = (int64_t)nl * lp.in; pb.bp_pstride = lp.in;
       if (l == 1 && P.fuse_x0) {
         pb.x = x; pb.din = P.layers[0].in; pb.xpart = c->xpart;
         pb.xp_sstride = (int64_t)nl * lp.in * P.layers[0].in; pb.xp_pstride = (int64_t)lp.in * P.layers[0].in;
@@ -536,7 +542,10 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
     if (st != PUSH_OK) return st;
     xb ^= 1;
   }
-  return PUSH_OK;
+  return run_k(c, PC_FINALIZE, 1, 0, 0, s, [&] {
+    kern::finalize_all(jobs.data(), (int)jobs.size(), th, g, ld, lambda, c->cfg.prior, inv_s2, nl, s);
+    return PUSH_OK;
+  });
 }
 
 // ------------------------------------------------------------------ step (a6-a10)
@@ -609,16 +618,17 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   for (size_t l = 0; l < P.o_act.size(); ++l) c->act.push_back(F(P.o_act[l]));
   c->dlt[0] = F(P.o_dlt0);
   c->dlt[1] = F(P.o_dlt1);
-  c->bpart[0] = F(P.o_bpart0);
-  c->bpart[1] = F(P.o_bpart1);
+  for (int l = 0; l < P.L; ++l) {
+    c->wpart.push_back(F(P.o_wpart[l]));
+    c->tpart.push_back(F(P.o_tpart[l]));
+    c->bpart.push_back(F(P.o_bpart[l]));
+  }
   c->opw = F(P.o_opw);
   c->opb = F(P.o_opb);
   c->xpart = F(P.o_xpart);
   c->err2 = F(P.o_err2);
   c->loss = F(P.o_loss);
   c->loss_all = F(P.o_loss_all);
-  c->wpart = F(P.o_wpart);
-  c->tpart = F(P.o_tpart);
   c->dpart = F(P.o_dpart);
   c->D = F(P.o_D);
   c->K = F(P.o_K);
