@@ -266,21 +266,36 @@ def run_ours(args, w):
     peaks, peak_kind = load_peaks()
     tot = sum(r["ms"] for r in prof) or 1.0
     gemm_rows = [r for r in prof if r["name"].endswith("gemm")]
-    dom = max(prof, key=lambda r: r["ms"])
+    # dominant kernel class among those with a roofline (tensor: the GEMMs; HBM: distances, update)
+    roofable = [r for r in prof if r["ms"] and (r["name"].endswith("gemm") or r["name"] in ("distances", "svgd_update"))]
+    dom = max(roofable or prof, key=lambda r: r["ms"])
     phases = {r["name"]: {"ms_per_step": r["ms"] / args.steps, "share": r["ms"] / tot,
                           "launches_per_step": r["launches"] / args.steps} for r in prof if r["launches"] or r["ms"]}
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{w.name}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tj = json.load(f)
+        if dom["name"] in tj.get("classes", {}):
+            traffic = tj["classes"][dom["name"]]["dram_bytes_per_launch"]
+            traffic_src = f"profiles/traffic_{w.name}.json ({tj.get('how', '')})"
+    per_launch = max(dom["launches"], 1)
     if dom["name"].endswith("gemm"):
         peak = peaks["bf16_tflops_sustained"] * TF32_OVER_BF16 / 3.0
         ach = dom["alg_flops"] / (dom["ms"] / 1e3) / 1e12
         roof = {"bound": "tensor", "kernel": "gemm3xtf32 (" + dom["name"] + ")", "achieved": ach, "peak": peak,
-                "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
+                "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic,
+                "algorithmic_per_launch": dom["alg_flops"] / per_launch,
                 "peak_note": f"{peak_kind} bf16 sustained x {TF32_OVER_BF16:.3f} (tf32/bf16 nominal) / 3 passes "
                              "(3xTF32 useful flops)"}
     else:
         peak = peaks["hbm_gbs"]
         ach = dom["alg_bytes"] / (dom["ms"] / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": dom["name"], "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "traffic": None, "peak_note": f"{peak_kind} hbm_gbs"}
+                "frac": ach / peak, "traffic": traffic, "algorithmic_per_launch": dom["alg_bytes"] / per_launch,
+                "peak_note": f"{peak_kind} hbm_gbs"}
+    if traffic_src:
+        roof["traffic_note"] = "DRAM bytes per launch (read + write) from " + traffic_src
     all_gemm_ms = sum(r["ms"] for r in gemm_rows)
     all_gemm_fl = sum(r["alg_flops"] for r in gemm_rows)
     if all_gemm_ms:

@@ -203,6 +203,11 @@ typedef struct {
 push_status push_profile_enable(push_ctx* ctx, int32_t enable);
 push_status push_profile_read(push_ctx* ctx, push_profile_row* rows, int32_t max_rows, int32_t* n_rows);
 
+/* Kernel class (index into the push_profile_read rows) of every kernel launched since the last
+ * push_profile_enable(ctx, 1), in launch order: *n = total count, the first min(*n, max_n) are
+ * written to classes.  Lets an external profiler's per-launch list be attributed to classes. */
+push_status push_profile_trace(push_ctx* ctx, int32_t* classes, int32_t max_n, int32_t* n);
+
 /* Total number of kernels this context has launched since push_init (host
  * counter, no sync).  Used for the bench's gpu_launches figure. */
 push_status push_launch_count(push_ctx* ctx, int64_t* count);

@@ -260,6 +260,7 @@ struct push_ctx {
   // profiling
   bool prof_on = false;
   std::vector<push::ProfRec> recs;
+  std::vector<int32_t> trace;  // kernel class of every launch while profiling, in launch order
   std::vector<cudaEvent_t> ev_pool;
   int64_t launches = 0;
 };
@@ -303,6 +304,7 @@ static push_status run_k(push_ctx* c, int cls, int nlaunch, double bytes, double
   }
   c->launches += nlaunch;
   if (c->prof_on) {
+    for (int k = 0; k < nlaunch; ++k) c->trace.push_back(cls);
     cudaEventRecord(e1, s);
     c->recs.push_back(ProfRec{cls, e0, e1, bytes, flops, nlaunch});
   }
@@ -961,7 +963,15 @@ push_status push_profile_enable(push_ctx* c, int32_t enable) {
     c->ev_pool.push_back(r.e1);
   }
   c->recs.clear();
+  c->trace.clear();
   c->prof_on = enable != 0;
+  return PUSH_OK;
+}
+
+push_status push_profile_trace(push_ctx* c, int32_t* classes, int32_t max_n, int32_t* n) {
+  if (!c || !n || (max_n > 0 && !classes)) return fail(PUSH_E_INVALID, "NULL argument");
+  *n = (int32_t)c->trace.size();
+  for (int32_t i = 0; i < max_n && i < *n; ++i) classes[i] = c->trace[i];
   return PUSH_OK;
 }
 

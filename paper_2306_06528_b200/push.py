@@ -31,7 +31,8 @@ MAX_LAYERS = 15
 EXPORTS = ["push_version", "push_last_error", "push_get_unique_id", "push_workspace_size", "push_init",
            "push_init_local_group", "push_particle_grads", "push_set_grads", "push_svgd_step", "push_step_graph",
            "push_step_host",
-           "push_gather", "push_profile_enable", "push_profile_read", "push_launch_count", "push_destroy",
+           "push_gather", "push_profile_enable", "push_profile_read", "push_profile_trace", "push_launch_count",
+           "push_destroy",
            "pushdbg_gemm3xtf32", "pushdbg_gemm1xtf32", "pushdbg_gemm"]
 
 
@@ -80,6 +81,7 @@ def lib():
         "push_gather": ([P, c_int32, P, P], c_int32),
         "push_profile_enable": ([P, c_int32], c_int32),
         "push_profile_read": ([P, POINTER(ProfileRow), c_int32, POINTER(c_int32)], c_int32),
+        "push_profile_trace": ([P, POINTER(c_int32), c_int32, POINTER(c_int32)], c_int32),
         "push_launch_count": ([P, POINTER(c_int64)], c_int32),
         "push_destroy": ([P], c_int32),
         "pushdbg_gemm3xtf32": ([c_int32] * 6 + [P, P, P, P], c_int32),
@@ -213,6 +215,15 @@ class Context:
         check(lib().push_profile_read(self._h, rows, 16, ctypes.byref(n)))
         return [dict(name=r.name.decode(), ms=r.ms, launches=r.launches, alg_bytes=r.alg_bytes,
                      alg_flops=r.alg_flops) for r in rows[:n.value]]
+
+    def profile_trace(self):
+        """Class names of every kernel launched since profile_enable(True), in launch order."""
+        n = c_int32(0)
+        check(lib().push_profile_trace(self._h, None, 0, ctypes.byref(n)))
+        buf = (c_int32 * max(n.value, 1))()
+        check(lib().push_profile_trace(self._h, buf, n.value, ctypes.byref(n)))
+        names = [r["name"] for r in self.profile_read()]
+        return [names[buf[i]] for i in range(n.value)]
 
     def launch_count(self) -> int:
         c = c_int64(0)
