@@ -75,6 +75,7 @@ struct KParams {
   int M, N, K, batch, splits, kb_per_split, passes, epi, act;
   int mt, nt, ntiles;
   int a_pz, b_pz;  // 1: operand batched over particles; 0: shared (particle coordinate 0)
+  int store;       // 0: BWD output only feeds the fused partials (delta of a thin first layer): no store
   int dbg;         // debug experiments only (pushdbg_gemm): bit 0 raw fp32 operands (no hi/lo split),
                    // bit 1 skip the epilogue math/stores, bit 2 skip the MMAs (commits only),
                    // bit 3 accumulate the whole K in TMEM (no fp32 promotion)
@@ -242,8 +243,10 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            ptx::tma_store_3d(tOut, ptx_ptr(buf), col, row0, pz);
-            ptx::bulk_commit();
+            if (prm.store) {
+              ptx::tma_store_3d(tOut, ptx_ptr(buf), col, row0, pz);
+              ptx::bulk_commit();
+            }
             if (bwd && g + 1 < G) {  // prefetch aprev of group g + 1 once the store of group g - 1 has read it
               ptx::bulk_wait_read1();
               const uint32_t nb = ebuf_s + ((g + 1) & 1) * kHalfBox;
@@ -293,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::prefetch_tmap(&tA);
     ptx::prefetch_tmap(&tBhi);
     if (!BSPLIT) ptx::prefetch_tmap(&tBlo);
-    ptx::prefetch_tmap(&tOut);
+    if (prm.store) ptx::prefetch_tmap(&tOut);
     if (prm.epi == EPI_BWD) ptx::prefetch_tmap(&tAux);
   }
   if (warp == 1) {
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(k2Threads, 1)
     ptx::prefetch_tmap(&tA);
     ptx::prefetch_tmap(&tBhi);
     if (!BSPLIT) ptx::prefetch_tmap(&tBlo);
-    ptx::prefetch_tmap(&tOut);
+    if (prm.store) ptx::prefetch_tmap(&tOut);
     if (prm.epi == EPI_BWD) ptx::prefetch_tmap(&tAux);
   }
   if (warp == 1) {
@@ -976,8 +979,9 @@ push_status run(const Problem& pb, cudaStream_t stream) {
     if ((st = make_operand_map(pb.B.lo, pb.B, pb.N, pb.K, pb.batch, box_b, &maps[2], false)) != PUSH_OK) return st;
   }
   const int nout = pb.epi == EPI_STORE ? pb.splits * pb.batch : pb.batch;
-  if ((st = make_map(&maps[3], pb.out, pb.N, pb.M, nout, pb.ldo, pb.out_pstride, 32, CU_TENSOR_MAP_SWIZZLE_64B,
-                     16)) != PUSH_OK)
+  if (!pb.out && pb.epi != EPI_BWD) return fail(PUSH_E_INVALID, "gemm: only the BWD epilogue may skip its output");
+  if (pb.out && (st = make_map(&maps[3], pb.out, pb.N, pb.M, nout, pb.ldo, pb.out_pstride, 32,
+                               CU_TENSOR_MAP_SWIZZLE_64B, 16)) != PUSH_OK)
     return st;
   if (pb.epi == EPI_BWD &&
       (st = make_map(&maps[4], pb.aprev, pb.N, pb.M, pb.batch, pb.ld_aprev, pb.aprev_pstride, 32,
@@ -987,6 +991,7 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   std::memset(&kp, 0, sizeof(kp));
   kp.M = pb.M; kp.N = pb.N; kp.K = pb.K; kp.batch = pb.batch; kp.splits = pb.splits; kp.kb_per_split = kbps;
   kp.passes = pb.passes & 0xff; kp.epi = pb.epi; kp.act = pb.act;
+  kp.store = pb.out != nullptr;
   kp.dbg = pb.passes >> 8;
   kp.mt = (pb.M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM);
   kp.nt = pb.N / BN;

@@ -39,6 +39,7 @@ struct Problem {
   int epi = EPI_STORE;
   int act = PUSH_ACT_TANH;
   float* out = nullptr;     // [s][p][m][n]: element at s*out_sstride + p*out_pstride + m*ldo + n
+                            // (BWD only: nullptr = compute the fused partials, store nothing)
   int64_t ldo = 0, out_pstride = 0, out_sstride = 0;  // out_sstride must equal batch*out_pstride when splits > 1
   const float* bias = nullptr;  // FWD: bias of particle p at bias + p*bias_pstride
   int64_t bias_pstride = 0;

@@ -31,32 +31,48 @@ void split_hilo(const float* src, int64_t src_pstride, float* hi, float* lo, int
 }
 
 // ---------------------------------------------------------------- thin forward (narrow input)
-// Narrow input (in <= kThinIn): thread = output feature o, W_o and b_o held in registers, looping
-// over the rows of a 32-row block (x[b][:] is a broadcast load, the store of row b is coalesced).
+// Narrow input (in <= kThinIn): thread = 4 consecutive output features (float4 store), W and b of
+// those features held in registers, looping over the rows of a 32-row block (x[b][:] is a broadcast
+// load; the stores of row b are coalesced).  Requires out % 4 == 0 (else VEC = 1: one feature).
 constexpr int kThinIn = 8;
-template <int NIN>
+template <int NIN, int VEC>
 __global__ void __launch_bounds__(256) thin_forward_narrow_kernel(const float* __restrict__ in, int64_t in_pstride,
                                                                   const float* __restrict__ theta, int64_t ld,
                                                                   int64_t off_w, int64_t off_b, int nin, int nout,
                                                                   int act, float* __restrict__ out,
                                                                   int64_t out_pstride, int B) {
+  constexpr int NI = NIN > 0 ? NIN : kThinIn;
   const int p = blockIdx.y;
   const int b0 = blockIdx.x * 32, b1 = min(B, b0 + 32);
   const float* x = in + p * in_pstride;
   const float* W = theta + p * ld + off_w;
   const float* bias = theta + p * ld + off_b;
   float* o_ = out + p * out_pstride;
-  for (int o = threadIdx.x; o < nout; o += blockDim.x) {
-    float w[kThinIn];
+  for (int o = threadIdx.x * VEC; o < nout; o += blockDim.x * VEC) {
+    float w[VEC][NI], bo[VEC];
 #pragma unroll
-    for (int i = 0; i < kThinIn; ++i) w[i] = i < nin ? __ldg(W + (int64_t)o * nin + i) : 0.f;
-    const float bo = __ldg(bias + o);
+    for (int v = 0; v < VEC; ++v) {
+#pragma unroll
+      for (int i = 0; i < NI; ++i) w[v][i] = (NIN > 0 || i < nin) ? __ldg(W + (int64_t)(o + v) * nin + i) : 0.f;
+      bo[v] = __ldg(bias + o + v);
+    }
     for (int b = b0; b < b1; ++b) {
-      float z = 0.f;
+      float xv[NI];
 #pragma unroll
-      for (int i = 0; i < (NIN > 0 ? NIN : kThinIn); ++i)
-        if (NIN > 0 || i < nin) z = fmaf(__ldg(x + (int64_t)b * nin + i), w[i], z);
-      o_[(int64_t)b * nout + o] = act_fwd(z + bo, act);
+      for (int i = 0; i < NI; ++i) xv[i] = (NIN > 0 || i < nin) ? __ldg(x + (int64_t)b * nin + i) : 0.f;
+      float z[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < NI; ++i)
+          if (NIN > 0 || i < nin) acc = fmaf(xv[i], w[v][i], acc);
+        z[v] = act_fwd(acc + bo[v], act);
+      }
+      if constexpr (VEC == 4)
+        *reinterpret_cast<float4*>(o_ + (int64_t)b * nout + o) = make_float4(z[0], z[1], z[2], z[3]);
+      else
+        o_[(int64_t)b * nout + o] = z[0];
     }
   }
 }
@@ -79,14 +95,24 @@ void thin_forward(const float* in, int64_t in_pstride, const float* theta, int64
                   cudaStream_t s) {
   if (in_ <= kThinIn) {
     const dim3 grid((unsigned)((B + 31) / 32), batch);
-    const int threads = out >= 256 ? 256 : ((out + 31) / 32) * 32;
-#define PUSH_THIN_FWD(N)                                                                                         \
-  thin_forward_narrow_kernel<N><<<grid, threads, 0, s>>>(in, in_pstride, theta, ld_theta, off_w, off_b, in_, out, \
-                                                         act, dst, out_pstride, B)
-    if (in_ == 1) PUSH_THIN_FWD(1);
-    else if (in_ == 2) PUSH_THIN_FWD(2);
-    else if (in_ == 3) PUSH_THIN_FWD(3);
-    else PUSH_THIN_FWD(0);
+    const bool v4 = out % 4 == 0 && out_pstride % 4 == 0;
+    const int per = v4 ? 4 : 1;
+    const int want = (out / per + 31) / 32 * 32;
+    const int threads = want > 256 ? 256 : (want < 32 ? 32 : want);
+#define PUSH_THIN_FWD(N, V)                                                                                     \
+  thin_forward_narrow_kernel<N, V><<<grid, threads, 0, s>>>(in, in_pstride, theta, ld_theta, off_w, off_b, in_, \
+                                                            out, act, dst, out_pstride, B)
+    if (v4) {
+      if (in_ == 1) PUSH_THIN_FWD(1, 4);
+      else if (in_ == 2) PUSH_THIN_FWD(2, 4);
+      else if (in_ == 3) PUSH_THIN_FWD(3, 4);
+      else PUSH_THIN_FWD(0, 4);
+    } else {
+      if (in_ == 1) PUSH_THIN_FWD(1, 1);
+      else if (in_ == 2) PUSH_THIN_FWD(2, 1);
+      else if (in_ == 3) PUSH_THIN_FWD(3, 1);
+      else PUSH_THIN_FWD(0, 1);
+    }
 #undef PUSH_THIN_FWD
     return;
   }

@@ -528,6 +528,7 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
       pb.bpart = c->bpart[l - 1]; pb.bp_sstride = (int64_t)nl * lp.in; pb.bp_pstride = lp.in;
       if (l == 1 && P.fuse_x0) {
         pb.x = x; pb.din = P.layers[0].in; pb.xpart = c->xpart;
+        pb.out = nullptr;  // delta_0 only feeds the fused first-layer partials: never stored
         pb.xp_sstride = (int64_t)nl * lp.in * P.layers[0].in; pb.xp_pstride = (int64_t)lp.in * P.layers[0].in;
         x0_ready = true;
       }
