@@ -131,15 +131,28 @@ void thin_forward(const float* in, int64_t in_pstride, const float* theta, int64
 //        dprev[b][i]          = (sum_o dL_o(b) W_o[i]) sigma'(a_b[i])  (delta of the layer below)
 //        bprev[rb][p][i]      = sum_b dprev[b][i]                     (its bias-gradient partial)
 //   and bpart[rb][p][o] = sum_b dL_o(b).
-template <int DOUT>  // compile-time bound on d_out (loops below run to DOUT, masked by a.dout)
+// SMEM: the block's 32 x H slab of A is staged once in shared memory (float4 loads), so phases 1
+// and 2 read it on chip and A crosses HBM once (H <= kOutSmemH, H % 4 == 0); same arithmetic order.
+constexpr int kOutSmemH = 1024;
+template <int DOUT, bool SMEM>  // compile-time bound on d_out (loops below run to DOUT, masked by a.dout)
 __global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
   __shared__ float sdl[32][DOUT];
   __shared__ float serr[32][DOUT];
+  extern __shared__ __align__(16) float sA[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.y;
   const int rb = blockIdx.x;
   const int rows = min(32, a.B - rb * 32);
-  const float* __restrict__ A = a.A + p * a.a_pstride + (int64_t)rb * 32 * a.H;
+  const float* __restrict__ Ag = a.A + p * a.a_pstride + (int64_t)rb * 32 * a.H;
+  if constexpr (SMEM) {
+    const int n4 = rows * a.H / 4;
+    const float4* src = reinterpret_cast<const float4*>(Ag);
+    float4* dst = reinterpret_cast<float4*>(sA);
+#pragma unroll 4
+    for (int k = threadIdx.x; k < n4; k += 256) dst[k] = __ldg(src + k);
+    __syncthreads();
+  }
+  const float* __restrict__ A = SMEM ? sA : Ag;
   const float* __restrict__ W = a.theta + p * a.ld + a.off_w;
   const float* __restrict__ bias = a.theta + p * a.ld + a.off_b;
   const float scale = 2.0f / (float)((int64_t)a.B * a.dout);
@@ -154,7 +167,7 @@ __global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
       const float w = __ldg(wrow + i);
 #pragma unroll
       for (int rr = 0; rr < 4; ++rr)
-        if (r0 + rr < rows) part[rr] = fmaf(__ldg(A + (int64_t)(r0 + rr) * a.H + i), w, part[rr]);
+        if (r0 + rr < rows) part[rr] = fmaf(A[(int64_t)(r0 + rr) * a.H + i], w, part[rr]);
     }
 #pragma unroll
     for (int rr = 0; rr < 4; ++rr) {
@@ -197,7 +210,7 @@ __global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
     float bacc = 0.f;
 #pragma unroll 8
     for (int r = 0; r < rows; ++r) {
-      const float av = __ldg(A + (int64_t)r * a.H + i);
+      const float av = A[(int64_t)r * a.H + i];
       float d = 0.f;
 #pragma unroll
       for (int o = 0; o < DOUT; ++o) {
@@ -216,13 +229,28 @@ __global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
     if (dprev) a.bpart_prev[(int64_t)rb * a.bp_sstride + p * a.bp_pstride + i] = bacc;
   }
 }
+template <int DOUT>
+static void output_launch(const OutputArgs& a, int batch, cudaStream_t s) {
+  const dim3 grid((a.B + 31) / 32, batch);
+  const bool smem = a.H <= kOutSmemH && a.H % 4 == 0 && a.a_pstride % 4 == 0 &&
+                    (reinterpret_cast<uintptr_t>(a.A) & 15) == 0;
+  if (smem) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(output_fused_kernel<DOUT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           32 * kOutSmemH * 4);
+      attr = true;
+    }
+    output_fused_kernel<DOUT, true><<<grid, 256, (size_t)32 * a.H * 4, s>>>(a);
+  } else {
+    output_fused_kernel<DOUT, false><<<grid, 256, 0, s>>>(a);
+  }
+}
 void output_fused(const OutputArgs& a, int batch, cudaStream_t s) {
-  const int RB = (a.B + 31) / 32;
-  const dim3 grid(RB, batch);
-  if (a.dout == 1) output_fused_kernel<1><<<grid, 256, 0, s>>>(a);
-  else if (a.dout == 2) output_fused_kernel<2><<<grid, 256, 0, s>>>(a);
-  else if (a.dout <= 4) output_fused_kernel<4><<<grid, 256, 0, s>>>(a);
-  else output_fused_kernel<kMaxDout><<<grid, 256, 0, s>>>(a);
+  if (a.dout == 1) output_launch<1>(a, batch, s);
+  else if (a.dout == 2) output_launch<2>(a, batch, s);
+  else if (a.dout <= 4) output_launch<4>(a, batch, s);
+  else output_launch<kMaxDout>(a, batch, s);
 }
 
 __global__ void loss_reduce_kernel(const float* __restrict__ err2, int64_t err_pstride, float* __restrict__ loss,
