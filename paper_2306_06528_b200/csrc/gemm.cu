@@ -157,11 +157,11 @@ __device__ __forceinline__ TileCoord decode(int t, const KParams& prm) {
 // Fused epilogue of one 32-row x CW-column slab held in registers (acc), written through the
 // warp's double-buffered swizzled 32x16 smem half-boxes with TMA stores (see the v3 notes above).
 // aux_ph: parity of the warp's aprev barrier (BWD); the aprev box of group 0 must already be in flight.
-template <int CW>
+template <int CW, int EPI>
 __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& prm, const CUtensorMap* tOut,
                                          const CUtensorMap* tAux, uint64_t* auxbar, uint32_t& aux_ph,
                                          uint32_t ebuf_s, int lane, int row0, int colw, int p, int pz) {
-  const bool bwd = prm.epi == EPI_BWD;
+  constexpr bool bwd = EPI == EPI_BWD;
         // Output in 16-column groups g, double-buffered: group g is staged in half-box (g & 1)
         // (32 rows x 16 fp32, SWIZZLE_64B: 16-B chunk c of row r sits at chunk c ^ ((r >> 1) & 3)),
         // so the TMA store of group g overlaps the math of group g + 1.
@@ -172,14 +172,14 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
         for (int g = 0; g < G; ++g) {
           const int col = colw + g * 16;
           const uint32_t buf = ebuf_s + (g & 1) * kHalfBox;
-          if (bwd) {
+          if constexpr (bwd) {
             ptx::mbar_wait(auxbar, aux_ph);  // aprev of group g has landed in buf
             aux_ph ^= 1;
           } else {
             if (lane == 0) ptx::bulk_wait_read1();  // the store of group g - 2 has finished reading buf
             __syncwarp();
           }
-          if (prm.epi == EPI_FWD) {
+          if constexpr (EPI == EPI_FWD) {
             const float* bias = prm.bias + p * prm.bias_pstride + col;  // b_l need not be 16-B aligned
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) {
@@ -192,7 +192,7 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
               v.w = act_fwd(acc[g * 16 + 4 * c4 + 3] + bv.w, prm.act);
               ptx::sts_f4(buf + roff + ((c4 ^ swz) << 4), v);
             }
-          } else if (bwd) {
+          } else if constexpr (bwd) {
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) {
               const uint32_t pp = buf + roff + ((c4 ^ swz) << 4);
@@ -212,7 +212,7 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
                                       acc[g * 16 + 4 * c4 + 3]));
           }
           __syncwarp();
-          if (bwd && prm.bpart) {
+          if (bwd && prm.bpart) {  // (bwd is constexpr)
             // a5 of the layer below: column partial sums of delta over this warp's 32 rows (rows >= M are
             // zero: their A rows were zero-filled by TMA).  Lane l: column l & 15, rows 16*(l >> 4) + 0..15
             // ascending, then the two halves added (commutative, so both lanes get the same bits).
@@ -257,7 +257,7 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
         }
       }
 
-template <int BN, bool AMN, bool BMN, bool BSPLIT>
+template <int BN, bool AMN, bool BMN, bool BSPLIT, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tBhi,
                       const __grid_constant__ CUtensorMap tBlo, const __grid_constant__ CUtensorMap tOut,
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::prefetch_tmap(&tBhi);
     if (!BSPLIT) ptx::prefetch_tmap(&tBlo);
     if (prm.store) ptx::prefetch_tmap(&tOut);
-    if (prm.epi == EPI_BWD) ptx::prefetch_tmap(&tAux);
+    if (EPI == EPI_BWD) ptx::prefetch_tmap(&tAux);
   }
   if (warp == 1) {
     ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ebuf_s = ptx::smem_u32(ebuf);
       const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
       uint32_t ch = 0, aux_ph = 0;
-      const bool bwd = prm.epi == EPI_BWD;
+      constexpr bool bwd = EPI == EPI_BWD;
       for (int t = blockIdx.x; t < prm.ntiles; t += gridDim.x) {
         TileCoord tc = decode(t, prm);
         const int n0 = tc.nt * BN;
@@ -488,8 +488,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_arrive(&tempty[b]);
         }
         if (!live || (prm.dbg & 2)) continue;
-        const int pz = prm.epi == EPI_STORE ? tc.split * prm.batch + tc.p : tc.p;
-        epi_tile<C::CW>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, tc.p, pz);
+        const int pz = EPI == EPI_STORE ? tc.split * prm.batch + tc.p : tc.p;
+        epi_tile<C::CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, tc.p, pz);
       }
       if (lane == 0) ptx::bulk_wait0();
     }
@@ -535,7 +535,7 @@ struct Cfg2 {
   static_assert(STAGES >= 2 && SMEM_BYTES <= kMaxSmem, "smem");
 };
 
-template <int PBN, bool AMN, bool BMN, bool BSPLIT>
+template <int PBN, bool AMN, bool BMN, bool BSPLIT, int EPI>
 __global__ void __launch_bounds__(k2Threads, 1)
     gemm3xtf32_2sm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tBhi,
                           const __grid_constant__ CUtensorMap tBlo, const __grid_constant__ CUtensorMap tOut,
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(k2Threads, 1)
     ptx::prefetch_tmap(&tBhi);
     if (!BSPLIT) ptx::prefetch_tmap(&tBlo);
     if (prm.store) ptx::prefetch_tmap(&tOut);
-    if (prm.epi == EPI_BWD) ptx::prefetch_tmap(&tAux);
+    if (EPI == EPI_BWD) ptx::prefetch_tmap(&tAux);
   }
   if (warp == 1) {
     ptx::tmem_alloc2(tmem_slot, C::TMEM_COLS);
@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(k2Threads, 1)
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
     const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(tempty), 0);  // + 8 * b for accumulator b
     uint32_t ch = 0, aux_ph = 0;
-    const bool bwd = prm.epi == EPI_BWD;
+    constexpr bool bwd = EPI == EPI_BWD;
     for (int t = cid; t < prm.ntiles; t += ncl) {
       int p, split, mp, nt;
       decode2(t, &p, &split, &mp, &nt);
@@ -776,8 +776,8 @@ __global__ void __launch_bounds__(k2Threads, 1)
         if (lane == 0) ptx::mbar_arrive_cluster(tempty_leader + 8 * b, 1);
       }
       if (!live || (prm.dbg & 2)) continue;
-      const int pz = prm.epi == EPI_STORE ? split * prm.batch + p : p;
-      epi_tile<k2CW>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, p, pz);
+      const int pz = EPI == EPI_STORE ? split * prm.batch + p : p;
+      epi_tile<k2CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, p, pz);
     }
     if (lane == 0) ptx::bulk_wait0();
   }
@@ -838,40 +838,52 @@ push_status make_operand_map(const float* ptr, const Operand& op, int mn_extent,
                   is_a ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
-template <int BN, bool AMN, bool BMN, bool BS>
+template <int BN, bool AMN, bool BMN, bool BS, int EPI>
 push_status launch_t(const CUtensorMap* maps, const KParams& kp, cudaStream_t stream) {
   using C = Cfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    PUSH_CUDA_TRY(cudaFuncSetAttribute(gemm3xtf32_kernel<BN, AMN, BMN, BS>,
+    PUSH_CUDA_TRY(cudaFuncSetAttribute(gemm3xtf32_kernel<BN, AMN, BMN, BS, EPI>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
     attr_set = true;
   }
   const int grid = kp.ntiles < g_sms ? kp.ntiles : g_sms;
-  gemm3xtf32_kernel<BN, AMN, BMN, BS>
+  gemm3xtf32_kernel<BN, AMN, BMN, BS, EPI>
       <<<grid, kThreads, C::SMEM_BYTES, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], kp);
   PUSH_CUDA_TRY(cudaGetLastError());
   return PUSH_OK;
 }
 
+// Instantiated layouts: every (A, B) layout for the plain-store epilogue (debug GEMM entry, split-K
+// weight gradients), the product's layouts for the fused ones (forward: K-major A and B; backward:
+// K-major A, MN-major B).
 template <int BN>
-push_status launch_bn(bool amn, bool bmn, bool bs, const CUtensorMap* maps, const KParams& kp, cudaStream_t s) {
+push_status launch_bn(bool amn, bool bmn, bool bs, int epi, const CUtensorMap* maps, const KParams& kp,
+                      cudaStream_t s) {
+  if (epi == EPI_FWD && !amn && !bmn)
+    return bs ? launch_t<BN, false, false, true, EPI_FWD>(maps, kp, s)
+              : launch_t<BN, false, false, false, EPI_FWD>(maps, kp, s);
+  if (epi == EPI_BWD && !amn && bmn)
+    return bs ? launch_t<BN, false, true, true, EPI_BWD>(maps, kp, s)
+              : launch_t<BN, false, true, false, EPI_BWD>(maps, kp, s);
+  if (epi != EPI_STORE) return fail(PUSH_E_INVALID, "gemm: fused epilogue with an unsupported operand layout");
   const int key = (amn ? 4 : 0) | (bmn ? 2 : 0) | (bs ? 1 : 0);
   switch (key) {
-    case 0: return launch_t<BN, false, false, false>(maps, kp, s);
-    case 1: return launch_t<BN, false, false, true>(maps, kp, s);
-    case 2: return launch_t<BN, false, true, false>(maps, kp, s);
-    case 3: return launch_t<BN, false, true, true>(maps, kp, s);
-    case 4: return launch_t<BN, true, false, false>(maps, kp, s);
-    case 5: return launch_t<BN, true, false, true>(maps, kp, s);
-    case 6: return launch_t<BN, true, true, false>(maps, kp, s);
-    default: return launch_t<BN, true, true, true>(maps, kp, s);
+    case 0: return launch_t<BN, false, false, false, EPI_STORE>(maps, kp, s);
+    case 1: return launch_t<BN, false, false, true, EPI_STORE>(maps, kp, s);
+    case 2: return launch_t<BN, false, true, false, EPI_STORE>(maps, kp, s);
+    case 3: return launch_t<BN, false, true, true, EPI_STORE>(maps, kp, s);
+    case 4: return launch_t<BN, true, false, false, EPI_STORE>(maps, kp, s);
+    case 5: return launch_t<BN, true, false, true, EPI_STORE>(maps, kp, s);
+    case 6: return launch_t<BN, true, true, false, EPI_STORE>(maps, kp, s);
+    default: return launch_t<BN, true, true, true, EPI_STORE>(maps, kp, s);
   }
 }
-template <int PBN, bool AMN, bool BMN, bool BS>
+
+template <int PBN, bool AMN, bool BMN, bool BS, int EPI>
 push_status launch2_t(const CUtensorMap* maps, const KParams& kp, cudaStream_t stream) {
   static int max_pairs = 0;
-  auto kern = gemm3xtf32_2sm_kernel<PBN, AMN, BMN, BS>;
+  auto kern = gemm3xtf32_2sm_kernel<PBN, AMN, BMN, BS, EPI>;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -897,17 +909,25 @@ push_status launch2_t(const CUtensorMap* maps, const KParams& kp, cudaStream_t s
 }
 
 template <int PBN>
-push_status launch2(bool amn, bool bmn, bool bs, const CUtensorMap* maps, const KParams& kp, cudaStream_t s) {
+push_status launch2(bool amn, bool bmn, bool bs, int epi, const CUtensorMap* maps, const KParams& kp,
+                    cudaStream_t s) {
+  if (epi == EPI_FWD && !amn && !bmn)
+    return bs ? launch2_t<PBN, false, false, true, EPI_FWD>(maps, kp, s)
+              : launch2_t<PBN, false, false, false, EPI_FWD>(maps, kp, s);
+  if (epi == EPI_BWD && !amn && bmn)
+    return bs ? launch2_t<PBN, false, true, true, EPI_BWD>(maps, kp, s)
+              : launch2_t<PBN, false, true, false, EPI_BWD>(maps, kp, s);
+  if (epi != EPI_STORE) return fail(PUSH_E_INVALID, "gemm: fused epilogue with an unsupported operand layout");
   const int key = (amn ? 4 : 0) | (bmn ? 2 : 0) | (bs ? 1 : 0);
   switch (key) {
-    case 0: return launch2_t<PBN, false, false, false>(maps, kp, s);
-    case 1: return launch2_t<PBN, false, false, true>(maps, kp, s);
-    case 2: return launch2_t<PBN, false, true, false>(maps, kp, s);
-    case 3: return launch2_t<PBN, false, true, true>(maps, kp, s);
-    case 4: return launch2_t<PBN, true, false, false>(maps, kp, s);
-    case 5: return launch2_t<PBN, true, false, true>(maps, kp, s);
-    case 6: return launch2_t<PBN, true, true, false>(maps, kp, s);
-    default: return launch2_t<PBN, true, true, true>(maps, kp, s);
+    case 0: return launch2_t<PBN, false, false, false, EPI_STORE>(maps, kp, s);
+    case 1: return launch2_t<PBN, false, false, true, EPI_STORE>(maps, kp, s);
+    case 2: return launch2_t<PBN, false, true, false, EPI_STORE>(maps, kp, s);
+    case 3: return launch2_t<PBN, false, true, true, EPI_STORE>(maps, kp, s);
+    case 4: return launch2_t<PBN, true, false, false, EPI_STORE>(maps, kp, s);
+    case 5: return launch2_t<PBN, true, false, true, EPI_STORE>(maps, kp, s);
+    case 6: return launch2_t<PBN, true, true, false, EPI_STORE>(maps, kp, s);
+    default: return launch2_t<PBN, true, true, true, EPI_STORE>(maps, kp, s);
   }
 }
 
@@ -1002,11 +1022,11 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   kp.bpart = pb.bpart; kp.bp_sstride = pb.bp_sstride; kp.bp_pstride = pb.bp_pstride;
   kp.x = pb.x; kp.din = pb.xpart ? pb.din : 0; kp.xpart = pb.xpart;
   kp.xp_sstride = pb.xp_sstride; kp.xp_pstride = pb.xp_pstride;
-  if (pair256) return launch2<256>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
-  if (pair128) return launch2<128>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
-  if (BN == 128) return launch_bn<128>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
-  if (BN == 64) return launch_bn<64>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
-  return launch_bn<32>(pb.A.mn_major, pb.B.mn_major, pb.B.split, maps, kp, stream);
+  if (pair256) return launch2<256>(pb.A.mn_major, pb.B.mn_major, pb.B.split, pb.epi, maps, kp, stream);
+  if (pair128) return launch2<128>(pb.A.mn_major, pb.B.mn_major, pb.B.split, pb.epi, maps, kp, stream);
+  if (BN == 128) return launch_bn<128>(pb.A.mn_major, pb.B.mn_major, pb.B.split, pb.epi, maps, kp, stream);
+  if (BN == 64) return launch_bn<64>(pb.A.mn_major, pb.B.mn_major, pb.B.split, pb.epi, maps, kp, stream);
+  return launch_bn<32>(pb.A.mn_major, pb.B.mn_major, pb.B.split, pb.epi, maps, kp, stream);
 }
 
 int effective_splits(int K, int want) {

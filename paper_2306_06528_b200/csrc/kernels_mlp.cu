@@ -422,7 +422,8 @@ struct FinalizeTable {
   FinalizeJob j[kMaxFinalizeJobs];
   int n;
 };
-__global__ void finalize_all_kernel(const FinalizeTable t, const float* __restrict__ theta, float* __restrict__ grad,
+__global__ void finalize_all_kernel(const __grid_constant__ FinalizeTable t, const float* __restrict__ theta,
+                                    float* __restrict__ grad,
                                     int64_t ld, float lambda, int prior, float inv_sigma2) {
   const int p = blockIdx.y;
   int k = 0;

@@ -1052,8 +1052,9 @@ static push_status dbg_gemm(int passes, int32_t a_mn, int32_t b_mn, int32_t b_sp
   if ((passes >> 8) & 32) {  // experiment: the forward epilogue (bias 0, tanh) instead of a plain store
     PUSH_CUDA_TRY(cudaMallocAsync(&zb, sizeof(float) * N, s));
     PUSH_CUDA_TRY(cudaMemsetAsync(zb, 0, sizeof(float) * N, s));
-    pb.epi = gemm::EPI_FWD; pb.act = PUSH_ACT_TANH; pb.bias = zb; pb.bias_pstride = 0;
-    pb.passes = passes & ~(32 << 8);
+    pb.epi = gemm::EPI_FWD; pb.act = ((passes >> 8) & 64) ? PUSH_ACT_IDENTITY : PUSH_ACT_TANH;
+    pb.bias = zb; pb.bias_pstride = 0;
+    pb.passes = passes & ~(96 << 8);
   }
   push_status st = gemm::run(pb, s);
   if (buf) cudaFreeAsync(buf, s);
