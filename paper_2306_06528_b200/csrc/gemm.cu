@@ -946,10 +946,12 @@ int force_pair() {
   }();
   return v;
 }
+// 128-wide pair tiles for the forward/backward GEMMs not covered by the 256-wide rule (default on:
+// C2 1.172 -> 1.150 ms/step); PUSH_GEMM_PAIR128=0 falls back to the 1-CTA kernel there.
 bool pair128_default() {
   static const int v = [] {
     const char* e = getenv("PUSH_GEMM_PAIR128");
-    return e && *e && *e != '0' ? 1 : 0;
+    return e && *e ? (*e != '0' ? 1 : 0) : 1;
   }();
   return v != 0;
 }
@@ -976,10 +978,11 @@ push_status run(const Problem& pb, cudaStream_t stream) {
     return fail(PUSH_E_INVALID, "gemm: split partials must be [s][p] contiguous");
   push_status st;
   if ((st = get_encoder()) != PUSH_OK) return st;
-  // CTA-pair kernel for the weight-gradient GEMMs over 256-wide column blocks (measured faster there:
-  // 89 vs 113 us on the C2 shape) and for forward/backward GEMMs with K >= 512 (C3: 19.5 -> 15.4 ms
-  // forward); at K = 256 the 1-CTA kernel's two TMEM accumulators overlap the fused epilogue better
-  // (C2 forward 129 vs 150 us) (profiles/r01_gemm.md).  PUSH_GEMM_1SM=1
+  // CTA-pair kernel with 256-wide pair tiles for the weight-gradient GEMMs (C2 shape: 89 vs 113 us for
+  // the 1-CTA kernel) and for forward/backward GEMMs with K >= 512 (C3: 19.5 -> 15.4 ms forward); at
+  // K = 256 the 128-wide pair tiles (two rotating TMEM accumulators overlap the fused epilogue with
+  // the next tile) are fastest; the 1-CTA kernel covers the remaining (narrow) shapes
+  // (profiles/r01_gemm.md).  PUSH_GEMM_1SM=1
   // forces the 1-CTA kernel, PUSH_GEMM_PAIR=1 the pair kernel wherever N % 256 == 0 (A/B comparisons).
   const bool dbg_ok = !(pb.passes >> 8 & (1 | 8)) && !force_1sm();
   const bool pair256 = dbg_ok && pb.N % 256 == 0 && (pb.epi == EPI_STORE || pb.K >= 512 || force_pair() == 1);
