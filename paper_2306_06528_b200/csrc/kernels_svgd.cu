@@ -48,21 +48,25 @@ void init_theta(float* theta, int64_t ld, int row0, int rows, int64_t d, uint64_
 // Tile shapes (rows per tile side T, pairs per thread RT x RT, column groups G per CTA):
 //   n <= 8: T=8 RT=1 G=4 | n <= 16: T=16 RT=2 G=4 | n <= 32: T=32 RT=2 G=1 | else T=64 RT=4 G=1
 // Each CTA owns one upper-triangular tile pair (bi <= bj) and a fixed column range (split s);
-// sub-chunks of kDistCW columns of both row tiles are double-buffered in smem with cp.async.
+// sub-chunks of DistCW<T> columns of both row tiles are double-buffered in smem with cp.async.
 // Every accumulation order depends only on (n, ld), never on the number of ranks.
-constexpr int kDistCW = 64;
-constexpr int kDistPad = 4;  // row stride 68 floats: 16-B aligned rows, 2-way bank conflicts at most
+constexpr int kDistCW = 64;   // smallest staged sub-chunk width (columns)
+constexpr int kDistPad = 4;  // row stride CW+4 floats: 16-B aligned rows, 2-way bank conflicts at most
+// staged sub-chunk width per tile shape: small tiles stream wider sub-chunks (fewer syncs per byte)
+template <int T>
+struct DistCW { static constexpr int v = T == 8 ? 256 : (T == 16 ? 128 : 64); };
 
 DistPlan dist_plan(int n, int64_t ld) {
   DistPlan pl;
   pl.T = n <= 8 ? 8 : (n <= 16 ? 16 : (n <= 32 ? 32 : 64));
   pl.ntile = (n + pl.T - 1) / pl.T;
   pl.npairs = pl.ntile * (pl.ntile + 1) / 2;
-  const int64_t chunks = (ld + kDistCW - 1) / kDistCW;
+  const int cw = pl.T == 8 ? 256 : (pl.T == 16 ? 128 : kDistCW);  // = DistCW<T>::v: split ranges are whole sub-chunks
+  const int64_t chunks = (ld + cw - 1) / cw;
   int64_t want = (4 * 148 + pl.npairs - 1) / pl.npairs;
   if (want > chunks) want = chunks;
   if (want < 1) want = 1;
-  pl.cols = (((ld + want - 1) / want) + kDistCW - 1) / kDistCW * kDistCW;
+  pl.cols = (((ld + want - 1) / want) + cw - 1) / cw * cw;
   pl.splits = (int)((ld + pl.cols - 1) / pl.cols);
   return pl;
 }
@@ -77,7 +81,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 template <int T, int RT>
 __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restrict__ theta, int64_t ld, int n,
                                                            int ntile, int64_t cols, float* __restrict__ part) {
-  constexpr int TP = T / RT, PT = TP * TP, G = 256 / PT, RS = kDistCW + kDistPad;
+  constexpr int CW = DistCW<T>::v;
+  constexpr int TP = T / RT, PT = TP * TP, G = 256 / PT, RS = CW + kDistPad;
   extern __shared__ __align__(16) float dsm[];  // [2 bufs][2 tiles][T][RS], then G*PT*RT*RT reduction
   int q = blockIdx.x, bi = 0;  // decode upper-triangular tile pair (bi <= bj)
   while (q >= ntile - bi) { q -= ntile - bi; ++bi; }
@@ -86,16 +91,16 @@ __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restri
   const int s = blockIdx.y;
   const int tid = threadIdx.x, g = tid / PT, pt = tid % PT, ty = pt / TP, tx = pt % TP;
   const int64_t c_begin = s * cols, c_end = min(ld, c_begin + cols);
-  const int nsub = (int)((c_end - c_begin + kDistCW - 1) / kDistCW);
+  const int nsub = (int)((c_end - c_begin + CW - 1) / CW);
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));
   auto stage = [&](int sub) {
     const int buf = sub & 1;
-    const int64_t c0 = c_begin + (int64_t)sub * kDistCW;
+    const int64_t c0 = c_begin + (int64_t)sub * CW;
     const int ntiles_ld = diag ? 1 : 2;
-    for (int idx = tid; idx < ntiles_ld * T * (kDistCW / 4); idx += 256) {
-      const int tl = idx / (T * (kDistCW / 4));
-      const int rem = idx - tl * T * (kDistCW / 4);
-      const int r = rem / (kDistCW / 4), c4 = rem - r * (kDistCW / 4);
+    for (int idx = tid; idx < ntiles_ld * T * (CW / 4); idx += 256) {
+      const int tl = idx / (T * (CW / 4));
+      const int rem = idx - tl * T * (CW / 4);
+      const int r = rem / (CW / 4), c4 = rem - r * (CW / 4);
       const int grow = (tl ? bj : bi) * T + r;
       const int64_t col = c0 + 4 * c4;
       const bool ok = grow < n && col < c_end;
@@ -118,7 +123,7 @@ __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restri
     const float* si = dsm + (size_t)((sub & 1) * 2) * T * RS;
     const float* sj = diag ? si : si + T * RS;
 #pragma unroll 4
-    for (int k = g; k < kDistCW; k += G) {
+    for (int k = g; k < CW; k += G) {
       float a[RT], b[RT];
 #pragma unroll
       for (int r = 0; r < RT; ++r) a[r] = si[(ty + TP * r) * RS + k];
@@ -166,7 +171,7 @@ __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restri
 template <int T, int RT>
 static void dist_launch(const float* theta, int64_t ld, int n, const DistPlan& pl, float* part, cudaStream_t s) {
   constexpr int TP = T / RT, PT = TP * TP, G = 256 / PT;
-  const size_t smem = sizeof(float) * (4 * T * (kDistCW + kDistPad) + (G > 1 ? G * PT * RT * RT : 0));
+  const size_t smem = sizeof(float) * (4 * T * (DistCW<T>::v + kDistPad) + (G > 1 ? G * PT * RT * RT : 0));
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(dist_partial_kernel<T, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -421,17 +426,16 @@ static void update_launch(const float* theta, const float* grad, int64_t ld, int
   svgd_update_kernel<RB, CT><<<grid, kUpdThreads, smem, s>>>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n,
                                                              theta_next);
 }
-// (RB, CT) = (16, 4): measured fastest on every config (C3 1.7 ms vs 2.2 ms for 32 x 2 and 2.5 ms for
-// 64 x 1, whose lower re-read factor does not pay for the smaller loads); kept as a query so the
-// launch accounting stays in one place.
+// (RB, CT) = (16, 4) (8 x 4 when n_local <= 8): measured fastest (C3 1.7 ms vs 2.2 ms for 32 x 2 and
+// 2.5 ms for 64 x 1, whose lower re-read factor does not pay for the smaller loads).
 int update_row_block(int n, int nl, int64_t ld) {
-  (void)n; (void)nl; (void)ld;
-  return 16;
+  (void)n; (void)ld;
+  return nl <= 8 ? 8 : 16;
 }
 int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl, const float* K,
                 const float* srow, const float* h, float eps_over_n, float* theta_next, cudaStream_t s) {
-  if (update_row_block(n, nl, ld) == 32)
-    update_launch<32, 2>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next, s);
+  if (update_row_block(n, nl, ld) == 8)
+    update_launch<8, 4>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next, s);
   else
     update_launch<16, 4>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next, s);
   return 1;
