@@ -181,6 +181,17 @@ push_status push_step_graph(push_ctx* ctx, const float* x_dev, const float* y_de
 push_status push_step_host(push_ctx* ctx, const float* x_host, const float* y_host, int32_t B,
                            float* loss_host, void* stream);
 
+/* ASYNC (collective when world_size > 1).  Predictive pushforward ppush(mu)(g(x; .)) (
+ * SURVEY.md §8(f) NEXT-1): every particle's network evaluated on the same inputs, gathered to every rank.
+ *   x_dev    : B x d_in float32 row-major, 1 <= B <= cfg.max_batch.
+ *   pred_dev : NULL or n x B x d_out float32 (particle-major) receiving every particle's prediction.
+ *   mean_dev, std_dev : NULL or B x d_out float32 receiving the cross-particle mean and population
+ *              standard deviation (ascending particle order).
+ * Uses the context's activation buffers (the last training forward's activations are overwritten; the
+ * state machine is unchanged).  Errors: PUSH_E_INVALID, PUSH_E_SHAPE, PUSH_E_CUDA, PUSH_E_NCCL. */
+push_status push_predict(push_ctx* ctx, const float* x_dev, int32_t B, float* pred_dev, float* mean_dev,
+                         float* std_dev, void* stream);
+
 /* SYNC (collective for THETA / LOSS when world_size > 1).  Copies `what`
  * (PUSH_WHAT_*) to out_host; sizes in the PUSH_WHAT_* comments.
  * Errors: PUSH_E_INVALID, PUSH_E_STATE (GRAD/DIST/H/KERNEL/LOSS before they exist). */

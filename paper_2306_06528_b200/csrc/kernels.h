@@ -42,6 +42,11 @@ struct OutputArgs {
   int64_t bp_sstride, bp_pstride;
 };
 void output_fused(const OutputArgs& a, int batch, cudaStream_t s);
+// Predictive forward of the output layer: yhat[p][b][o] = A_b . W_o + b_o  (pred laid out [p][B][d_out])
+void output_forward(const float* A, int64_t a_pstride, const float* theta, int64_t ld, int64_t off_w, int64_t off_b,
+                    int H, int dout, float* pred, int B, int batch, cudaStream_t s);
+// Cross-particle mean and population std of pred [n][m] (ascending particle order); mean/std may be NULL.
+void predict_stats(const float* pred, int n, int64_t m, float* mean, float* stdev, cudaStream_t s);
 // loss[p] = sum_b err2[p][b] / (B d_out)   (fixed-order tree reduction)
 void loss_reduce(const float* err2, int64_t err_pstride, float* loss, int B, int d_out, int batch, cudaStream_t s);
 

@@ -253,6 +253,47 @@ void output_fused(const OutputArgs& a, int batch, cudaStream_t s) {
   else output_launch<kMaxDout>(a, batch, s);
 }
 
+// ---------------------------------------------------------------- predictive pushforward (NEXT-1)
+// warp per (particle, row): lanes split the features, fixed xor tree (same order as output_fused)
+__global__ void output_forward_kernel(const float* __restrict__ A, int64_t a_pstride, const float* __restrict__ theta,
+                                      int64_t ld, int64_t off_w, int64_t off_b, int H, int dout,
+                                      float* __restrict__ pred, int B) {
+  const int p = blockIdx.y, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= B) return;
+  const float* arow = A + p * a_pstride + (int64_t)b * H;
+  for (int o = 0; o < dout; ++o) {
+    const float* wrow = theta + p * ld + off_w + (int64_t)o * H;
+    float part = 0.f;
+    for (int i = lane; i < H; i += 32) part = fmaf(__ldg(arow + i), __ldg(wrow + i), part);
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) part += __shfl_xor_sync(0xffffffffu, part, m);
+    if (lane == 0) pred[((int64_t)p * B + b) * dout + o] = part + __ldg(theta + p * ld + off_b + o);
+  }
+}
+void output_forward(const float* A, int64_t a_pstride, const float* theta, int64_t ld, int64_t off_w, int64_t off_b,
+                    int H, int dout, float* pred, int B, int batch, cudaStream_t s) {
+  output_forward_kernel<<<dim3((B + 7) / 8, batch), 256, 0, s>>>(A, a_pstride, theta, ld, off_w, off_b, H, dout, pred, B);
+}
+__global__ void predict_stats_kernel(const float* __restrict__ pred, int n, int64_t m, float* __restrict__ mean,
+                                     float* __restrict__ stdev) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  float s1 = 0.f;
+  for (int p = 0; p < n; ++p) s1 += pred[(int64_t)p * m + t];
+  const float mu = s1 / (float)n;
+  float s2 = 0.f;
+  for (int p = 0; p < n; ++p) {
+    const float dv = pred[(int64_t)p * m + t] - mu;
+    s2 = fmaf(dv, dv, s2);
+  }
+  if (mean) mean[t] = mu;
+  if (stdev) stdev[t] = sqrtf(s2 / (float)n);
+}
+void predict_stats(const float* pred, int n, int64_t m, float* mean, float* stdev, cudaStream_t s) {
+  predict_stats_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(pred, n, m, mean, stdev);
+}
+
 __global__ void loss_reduce_kernel(const float* __restrict__ err2, int64_t err_pstride, float* __restrict__ loss,
                                    int B, float denom) {
   __shared__ float sh[256];

@@ -60,7 +60,7 @@ struct Plan {
   kern::DistPlan dist{};
   // byte offsets into the workspace
   size_t o_theta0, o_theta1, o_grad, o_whi, o_wlo, o_dlt0, o_dlt1, o_err2, o_loss, o_loss_all, o_opw, o_opb,
-      o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf;
+      o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf, o_pred;
   std::vector<size_t> o_act;
   // per-layer partial buffers, all alive until the single finalize launch at the end of a5
   std::vector<size_t> o_wpart, o_tpart, o_bpart;
@@ -192,6 +192,7 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.o_h = take(32);
   P.o_xbuf = take((int64_t)P.Bmax * P.layers[0].in);
   P.o_ybuf = take((int64_t)P.Bmax * top.out);
+  P.o_pred = take((int64_t)P.n * P.Bmax * top.out);
   P.total = cur;
   return PUSH_OK;
 }
@@ -236,6 +237,8 @@ struct push_ctx {
   float *opw = nullptr, *opb = nullptr, *xpart = nullptr;
   float *dpart = nullptr, *D = nullptr, *K = nullptr, *srow = nullptr, *h = nullptr;
   float *xbuf = nullptr, *ybuf = nullptr;
+  float* pred = nullptr;  // predictive pushforward: n x B x d_out (own rows, then all-gathered)
+  int pred_B = 0;
   int state = 0;  // 0 READY, 1 GRADS_READY
   bool broken = false;
   bool has_grads = false, has_step = false;
@@ -312,7 +315,7 @@ static push_status run_k(push_ctx* c, int cls, int nlaunch, double bytes, double
 }
 
 // ------------------------------------------------------------------ exchange
-enum BufKind { BUF_THETA = 0, BUF_GRAD = 1, BUF_LOSS = 2 };
+enum BufKind { BUF_THETA = 0, BUF_GRAD = 1, BUF_LOSS = 2, BUF_PRED = 3 };
 
 static float* buf_of(push_ctx* c, int kind, size_t* per_rank) {
   if (kind == BUF_THETA) {
@@ -322,6 +325,10 @@ static float* buf_of(push_ctx* c, int kind, size_t* per_rank) {
   if (kind == BUF_GRAD) {
     *per_rank = (size_t)c->P.nl * c->P.ld;
     return c->grad;
+  }
+  if (kind == BUF_PRED) {
+    *per_rank = (size_t)c->P.nl * c->pred_B * c->P.layers[c->P.L - 1].out;
+    return c->pred;
   }
   *per_rank = (size_t)c->P.nl;
   return c->loss_all;
@@ -585,6 +592,58 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   return PUSH_OK;
 }
 
+// ------------------------------------------------------------------ predictive pushforward (NEXT-1)
+// ppush(mu)(g(x; .)) = {g(x; theta_i)}: every particle's forward on x, all-gathered
+// to every rank, then the cross-particle mean and population standard deviation per output.
+static push_status do_predict(push_ctx* c, const float* x, int B, cudaStream_t s) {
+  const Plan& P = c->P;
+  const int nl = P.nl, L = P.L, act = c->cfg.activation;
+  const int64_t ld = P.ld;
+  const float* th = c->theta[c->cur] + (int64_t)c->row0 * ld;
+  push_status st;
+  for (int l = 0; l + 1 < L; ++l) {
+    const LayerPlan& lp = P.layers[l];
+    const ActView in = layer_input(c, l, x);
+    const double fl = 2.0 * B * lp.out * (double)lp.in * nl;
+    if (lp.gemm) {
+      gemm::Problem pb;
+      pb.M = B; pb.N = lp.out; pb.K = lp.in; pb.batch = nl; pb.splits = 1; pb.passes = 3;
+      pb.A = gemm::Operand{in.p, nullptr, true, false, lp.in, in.pst};
+      pb.B = lp.wraw ? gemm::Operand{th + lp.off_w, nullptr, true, false, lp.in, ld}
+                     : gemm::Operand{c->whi + lp.woff, c->wlo + lp.woff, false, false, lp.in, P.wsplit_total};
+      if (!lp.wraw) {
+        const int64_t cnt = (int64_t)lp.in * lp.out;
+        st = run_k(c, PC_SPLIT, 1, 12.0 * cnt * nl, 0, s, [&] {
+          kern::split_hilo(th + lp.off_w, ld, c->whi + lp.woff, c->wlo + lp.woff, P.wsplit_total, cnt, nl, s);
+          return PUSH_OK;
+        });
+        if (st != PUSH_OK) return st;
+      }
+      pb.epi = gemm::EPI_FWD; pb.act = act;
+      pb.out = c->act[l]; pb.ldo = lp.out; pb.out_pstride = P.act_pst[l];
+      pb.bias = th + lp.off_b; pb.bias_pstride = ld;
+      st = run_k(c, PC_FWD_GEMM, 1, 0, fl, s, [&] { return gemm::run(pb, s); });
+    } else {
+      st = run_k(c, PC_FWD_THIN, 1, 4.0 * B * lp.out * nl, fl, s, [&] {
+        kern::thin_forward(in.p, in.pst, th, ld, lp.off_w, lp.off_b, lp.in, lp.out, act, c->act[l], P.act_pst[l], B,
+                           nl, s);
+        return PUSH_OK;
+      });
+    }
+    if (st != PUSH_OK) return st;
+  }
+  const LayerPlan& top = P.layers[L - 1];
+  const ActView in = layer_input(c, L - 1, x);
+  c->pred_B = B;
+  float* own = c->pred + (size_t)c->row0 * B * top.out;
+  st = run_k(c, PC_OUTPUT, 1, 4.0 * B * top.in * nl, 2.0 * B * top.out * (double)top.in * nl, s, [&] {
+    kern::output_forward(in.p, in.pst, th, ld, top.off_w, top.off_b, top.in, top.out, own, B, nl, s);
+    return PUSH_OK;
+  });
+  if (st != PUSH_OK) return st;
+  return exchange(c, BUF_PRED, s);
+}
+
 static push_status check_ctx(push_ctx* c) {
   if (!c) return fail(PUSH_E_INVALID, "ctx is NULL");
   if (c->broken) return fail(PUSH_E_STATE, "context is in a failed state after an earlier CUDA/NCCL error");
@@ -639,6 +698,7 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   c->h = F(P.o_h);
   c->xbuf = F(P.o_xbuf);
   c->ybuf = F(P.o_ybuf);
+  c->pred = F(P.o_pred);
   // bandwidth constant c_n = fp32(1/ln n) or fp32(1/ln(n+1)), computed once in double (R4)
   if (cfg->bw_rule == PUSH_BW_MEDIAN_LN_N)
     c->c_ln = P.n > 1 ? (float)(1.0 / std::log((double)P.n)) : 1.f;
@@ -908,6 +968,32 @@ push_status push_step_host(push_ctx* c, const float* x_host, const float* y_host
   }
   cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
+  return PUSH_OK;
+}
+
+push_status push_predict(push_ctx* c, const float* x_dev, int32_t B, float* pred_dev, float* mean_dev, float* std_dev,
+                         void* stream) {
+  push_status st = check_ctx(c);
+  if (st != PUSH_OK) return st;
+  if (!x_dev) return fail(PUSH_E_INVALID, "x_dev is NULL");
+  if (B < 1 || B > c->P.Bmax) return fail(PUSH_E_SHAPE, "B must be in [1, max_batch] (SPEC.md:55)");
+  if (c->group && c->world > 1)
+    return fail(PUSH_E_STATE, "push_predict gathers every rank's predictions: not available in a loopback group");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = do_predict(c, x_dev, B, s)) != PUSH_OK) return sticky(c, st);
+  const int dout = c->P.layers[c->P.L - 1].out;
+  const size_t per = (size_t)B * dout;
+  if (mean_dev || std_dev) {
+    st = run_k(c, PC_OUTPUT, 1, 4.0 * c->P.n * per, 0, s, [&] {
+      kern::predict_stats(c->pred, c->P.n, (int64_t)per, mean_dev, std_dev, s);
+      return PUSH_OK;
+    });
+    if (st != PUSH_OK) return sticky(c, st);
+  }
+  if (pred_dev) {
+    cudaError_t e = cudaMemcpyAsync(pred_dev, c->pred, 4 * per * c->P.n, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
+  }
   return PUSH_OK;
 }
 

@@ -31,7 +31,7 @@ MAX_LAYERS = 15
 EXPORTS = ["push_version", "push_last_error", "push_get_unique_id", "push_workspace_size", "push_init",
            "push_init_local_group", "push_particle_grads", "push_set_grads", "push_svgd_step", "push_step_graph",
            "push_step_host",
-           "push_gather", "push_profile_enable", "push_profile_read", "push_profile_trace", "push_launch_count",
+           "push_gather", "push_predict", "push_profile_enable", "push_profile_read", "push_profile_trace", "push_launch_count",
            "push_destroy",
            "pushdbg_gemm3xtf32", "pushdbg_gemm1xtf32", "pushdbg_gemm"]
 
@@ -79,6 +79,7 @@ def lib():
         "push_step_graph": ([P, P, P, c_int32, P, P], c_int32),
         "push_step_host": ([P, P, P, c_int32, P, P], c_int32),
         "push_gather": ([P, c_int32, P, P], c_int32),
+        "push_predict": ([P, P, c_int32, P, P, P, P], c_int32),
         "push_profile_enable": ([P, c_int32], c_int32),
         "push_profile_read": ([P, POINTER(ProfileRow), c_int32, POINTER(c_int32)], c_int32),
         "push_profile_trace": ([P, POINTER(c_int32), c_int32, POINTER(c_int32)], c_int32),
@@ -204,6 +205,16 @@ class Context:
         out = np.empty(shape, dtype=np.float32)
         check(lib().push_gather(self._h, WHAT[what], out.ctypes.data_as(c_void_p), _stream(stream)))
         return out
+
+    def predict(self, x, stream=None):
+        """Predictive pushforward (push_predict): (pred [n, B, d_out], mean [B, d_out], std [B, d_out]) tensors."""
+        import torch
+        B, dout = int(x.shape[0]), self.dims[-1]
+        pred = torch.empty((self.n, B, dout), dtype=torch.float32, device=x.device)
+        mean = torch.empty((B, dout), dtype=torch.float32, device=x.device)
+        std = torch.empty((B, dout), dtype=torch.float32, device=x.device)
+        check(lib().push_predict(self._h, _ptr(x), B, _ptr(pred), _ptr(mean), _ptr(std), _stream(stream)))
+        return pred, mean, std
 
     # -- instrumentation
     def profile_enable(self, on: bool = True):

@@ -321,3 +321,26 @@ def test_full_size_sampled_parity_graph_path(cfgname):
     ref = th0[:, cols] + 1e-3 * osvgd.phi(th0[:, cols], g[:, cols].astype(np.float64), K, h)
     th1 = ctx.gather("theta")[:, cols]
     assert rel_err(th1, ref) <= 1e-4
+
+
+# ------------------------------------------------------------------ predictive pushforward (NEXT-1)
+@pytest.mark.parametrize("n,dims,B", [(4, [1, 32, 32, 1], 256), (16, [2, 256, 256, 256, 256, 1], 1000),
+                                      (3, [5, 7, 3], 77), (8, [3, 96, 32, 2], 300)])
+def test_predict_matches_oracle(n, dims, B):
+    from oracle import predict as opred
+    x, _ = synth.batch("gauss", B, dims[0], dims[-1], step=5)
+    ctx = push.Context(push.make_config(n, dims, max_batch=B, seed=4))
+    th = ctx.gather("theta")
+    pred, mean, std = ctx.predict(_dev(x))
+    rp, rm, rs = opred.predictive_summary(th, dims, x)
+    assert inf_rel(pred.cpu().numpy().reshape(n, -1), rp.reshape(n, -1)) <= 1e-5
+    scale = np.abs(rp).max()
+    np.testing.assert_allclose(mean.cpu().numpy(), rm, rtol=0, atol=1e-5 * scale)
+    np.testing.assert_allclose(std.cpu().numpy(), rs, rtol=0, atol=1e-5 * scale)
+    # the training state is untouched: a step after predict equals a step without it
+    x2, y2 = synth.batch("gauss", B, dims[0], dims[-1], step=6)
+    ctx2 = push.Context(push.make_config(n, dims, max_batch=B, seed=4))
+    for c in (ctx, ctx2):
+        c.particle_grads(_dev(x2), _dev(y2))
+        c.svgd_step()
+    assert np.array_equal(ctx.gather("theta"), ctx2.gather("theta"))
