@@ -76,6 +76,7 @@ struct KParams {
   int mt, nt, ntiles;
   int a_pz, b_pz;  // 1: operand batched over particles; 0: shared (particle coordinate 0)
   int store;       // 0: BWD output only feeds the fused partials (delta of a thin first layer): no store
+  int chunk_kb;    // k-blocks per TMEM accumulation chunk before the fp32 promotion (pair kernel)
   int dbg;         // debug experiments only (pushdbg_gemm): bit 0 raw fp32 operands (no hi/lo split),
                    // bit 1 skip the epilogue math/stores, bit 2 skip the MMAs (commits only),
                    // bit 3 accumulate the whole K in TMEM (no fp32 promotion)
@@ -476,13 +477,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int b = ch % C::NACC;
           ptx::mbar_wait(&tfull[b], (ch / C::NACC) & 1);
           ptx::tc_fence_after();
+          // two TMEM loads in flight per wait (each load-wait round trip costs ~200 cycles with 8 warps)
 #pragma unroll
-          for (int c0 = 0; c0 < C::CW; c0 += 16) {
-            uint32_t r[16];
-            ptx::tmem_ld_32x32b_x16(lane_base + b * BN + h * C::CW + c0, r);
+          for (int c0 = 0; c0 < C::CW; c0 += 32) {
+            uint32_t r0[16], r1[16];
+            ptx::tmem_ld_32x32b_x16(lane_base + b * BN + h * C::CW + c0, r0);
+            ptx::tmem_ld_32x32b_x16(lane_base + b * BN + h * C::CW + c0 + 16, r1);
             ptx::tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 16; ++j) acc[c0 + j] += __uint_as_float(r[j]);
+            for (int j = 0; j < 16; ++j) {
+              acc[c0 + j] += __uint_as_float(r0[j]);
+              acc[c0 + 16 + j] += __uint_as_float(r1[j]);
+            }
           }
           ptx::tc_fence_before();
           ptx::mbar_arrive(&tempty[b]);
@@ -642,8 +648,9 @@ __global__ void __launch_bounds__(k2Threads, 1)
         int kb0;
         const int nkb = tile_kb(split, &kb0);
         for (int i = 0; i < nkb; ++i, ++it) {
-          const bool first = (i % kChunkKB) == 0;
-          const bool last = (i % kChunkKB) == kChunkKB - 1 || i == nkb - 1;
+          const int ckb = prm.chunk_kb;
+          const bool first = (i % ckb) == 0;
+          const bool last = (i % ckb) == ckb - 1 || i == nkb - 1;
           const int b = ch % C::NACC;
           if (first) ptx::mbar_wait(&tempty[b], ((ch / C::NACC) & 1) ^ 1);
           const int s = it % C::STAGES;
@@ -747,7 +754,7 @@ __global__ void __launch_bounds__(k2Threads, 1)
       decode2(t, &p, &split, &mp, &nt);
       int kb0;
       const int nkb = tile_kb(split, &kb0);
-      const int nchunks = (nkb + kChunkKB - 1) / kChunkKB;
+      const int nchunks = (nkb + prm.chunk_kb - 1) / prm.chunk_kb;
       const int row0 = mp * 256 + (int)crank * 128 + q * 32;
       const bool live = row0 < prm.M;
       const int colw = nt * k2BN + h * k2CW;
@@ -763,13 +770,18 @@ __global__ void __launch_bounds__(k2Threads, 1)
         const int b = ch % C::NACC;
         ptx::mbar_wait(&tfull[b], (ch / C::NACC) & 1);
         ptx::tc_fence_after();
+        // two TMEM loads in flight per wait (each load-wait round trip costs ~200 cycles with 8 warps)
 #pragma unroll
-        for (int c0 = 0; c0 < k2CW; c0 += 16) {
-          uint32_t r[16];
-          ptx::tmem_ld_32x32b_x16(lane_base + b * PBN + h * k2CW + c0, r);
+        for (int c0 = 0; c0 < k2CW; c0 += 32) {
+          uint32_t r0[16], r1[16];
+          ptx::tmem_ld_32x32b_x16(lane_base + b * PBN + h * k2CW + c0, r0);
+          ptx::tmem_ld_32x32b_x16(lane_base + b * PBN + h * k2CW + c0 + 16, r1);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) acc[c0 + j] += __uint_as_float(r[j]);
+          for (int j = 0; j < 16; ++j) {
+            acc[c0 + j] += __uint_as_float(r0[j]);
+            acc[c0 + 16 + j] += __uint_as_float(r1[j]);
+          }
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -957,6 +969,15 @@ bool pair128_default() {
 }
 }  // namespace
 
+// experiment hook: PUSH_GEMM_CHUNK=<k-blocks per promotion chunk> (pair kernel; default kChunkKB)
+int chunk_kb_env() {
+  static const int v = [] {
+    const char* e = getenv("PUSH_GEMM_CHUNK");
+    return e && *e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 int choose_bn(int N) {
   if (N % 128 == 0) return 128;
   if (N % 64 == 0) return 64;
@@ -1015,6 +1036,7 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   kp.M = pb.M; kp.N = pb.N; kp.K = pb.K; kp.batch = pb.batch; kp.splits = pb.splits; kp.kb_per_split = kbps;
   kp.passes = pb.passes & 0xff; kp.epi = pb.epi; kp.act = pb.act;
   kp.store = pb.out != nullptr;
+  kp.chunk_kb = chunk_kb_env() > 0 ? chunk_kb_env() : kChunkKB;
   kp.dbg = pb.passes >> 8;
   kp.mt = (pb.M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM);
   kp.nt = pb.N / BN;
