@@ -331,8 +331,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of the captured CUDA graph")
+    ap.add_argument("--n-particles", type=int, default=0, help="override the workload's particle count (sweeps)")
     args = ap.parse_args()
     w = WORKLOADS[args.config]
+    if args.n_particles:
+        import dataclasses
+        w = dataclasses.replace(w, n_particles=args.n_particles,
+                                note=f"{w.note} [n overridden to {args.n_particles}]")
     if args.impl == "reference":
         run_reference(args, w)
     else:
