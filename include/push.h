@@ -83,7 +83,7 @@ enum {
   PUSH_WHAT_KERNEL = 5   /* n x n kernel matrix K of the last step                    */
 };
 
-/* Plain-old-data configuration (112 bytes; field order is ABI). */
+/* Plain-old-data configuration (120 bytes; field order is ABI). */
 typedef struct {
   int32_t n_particles;                 /* n >= 1, n % world_size == 0                        */
   int32_t n_layers;                    /* L in [1, 15] Linear layers                          */
@@ -97,6 +97,8 @@ typedef struct {
   float step_size;                     /* eps > 0                                             */
   int32_t max_batch;                   /* >= 1; sizes the workspace                           */
   uint64_t seed;                       /* K0 initialiser stream (R14)                         */
+  int32_t swag;                        /* 1: allocate SWAG moment buffers (push_swag_*)       */
+  int32_t reserved;                    /* must be 0                                           */
 } push_config;
 
 /* Library / build identification string (static storage). */
@@ -180,6 +182,25 @@ push_status push_step_graph(push_ctx* ctx, const float* x_dev, const float* y_de
  * `stream`.  State: READY -> READY. */
 push_status push_step_host(push_ctx* ctx, const float* x_host, const float* y_host, int32_t B,
                            float* loss_host, void* stream);
+
+/* ASYNC.  Deep-ensemble step (Fig. lang:de): every local
+ * particle takes an independent gradient-ascent step theta_i <- theta_i + eps * g_i on its own
+ * log posterior (no kernel, no exchange; SVGD with K = I and no repulsion).
+ * State: GRADS_READY -> READY.  Errors: PUSH_E_STATE (no fresh grads), PUSH_E_CUDA. */
+push_status push_ensemble_step(push_ctx* ctx, void* stream);
+
+/* ASYNC.  Diagonal SWAG moments (Fig. supp:swag): folds
+ * the current Theta of every local particle into its running first and second moments,
+ *   mean <- (mean * k + theta) / (k + 1),   sq <- (sq * k + theta^2) / (k + 1),   k <- k + 1.
+ * Requires cfg.swag = 1.  Errors: PUSH_E_STATE (no SWAG buffers), PUSH_E_CUDA. */
+push_status push_swag_collect(push_ctx* ctx, void* stream);
+
+/* ASYNC.  Draws one SWAG sample per local particle: out_dev[i][k] = mean_ik + sqrt(max(sq_ik - mean_ik^2, 0)) z,
+ * z = sqrt(-2 ln u1) cos(2 pi u2) with u1 = (m1 + 1) 2^-24, u2 = m2 2^-24 and m1, m2 the top 24 bits of
+ * mix64(seed ^ mix64(((i << 32) | k) * 2 + 0 / 1)) (i = global particle row, k = canonical index; the
+ * oracle implements the same counter-based generator).  out_dev: n_local x d canonical float32.
+ * Errors: PUSH_E_INVALID, PUSH_E_STATE (no SWAG buffers or no collected moments), PUSH_E_CUDA. */
+push_status push_swag_sample(push_ctx* ctx, uint64_t seed, float* out_dev, void* stream);
 
 /* ASYNC (collective when world_size > 1).  Predictive pushforward ppush(mu)(g(x; .)) (
  * SURVEY.md §8(f) NEXT-1): every particle's network evaluated on the same inputs, gathered to every rank.

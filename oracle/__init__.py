@@ -10,6 +10,7 @@ particle step (arXiv 2306.06528), written from the paper:
                      phi(theta_i) = (1/n) sum_j [K_ij grad log p(theta_j) + grad_{theta_j} K_ij]
                      and the Jacobi step (Fig. supp:svgd; north star).
 * ``oracle.init``  — the counter-based K0 initialiser (SplitMix64; R14).
+* ``oracle.swag``  — deep-ensemble step and diagonal SWAG moments / samples (NEXT-3).
 * ``oracle.predict`` — predictive pushforward: per-particle outputs, cross-particle mean and
                      population std.
 
@@ -22,4 +23,4 @@ against closed forms, finite differences, special cases and brute force.
 Functions without such a pin are marked "parity unpinned" (none at present;
 see DESIGN.md §Oracle).
 """
-from . import init, mlp, predict, svgd  # noqa: F401
+from . import init, mlp, predict, svgd, swag  # noqa: F401

@@ -119,6 +119,15 @@ int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int ro
                 const float* srow, const float* h, float eps_over_n, float* theta_next, cudaStream_t s);
 int update_row_block(int n, int nl, int64_t ld);
 
+// ---------------------------------------------------------------- NEXT-3: deep ensembles and diagonal SWAG
+// theta[p][k] += eps * g[p][k] for the own rows (in place)
+void ensemble_step(float* theta, const float* grad, int64_t ld, int rows, float eps, cudaStream_t s);
+// mean <- (mean k + x)/(k+1), sq <- (sq k + x^2)/(k+1) elementwise over count elements (k = snapshots so far)
+void swag_collect(const float* x, float* mean, float* sq, int64_t count, int64_t k, cudaStream_t s);
+// out[r][c] = mean + sqrt(max(sq - mean^2, 0)) * z(seed, row0 + r, c)   (counter-based Box-Muller, see push.h)
+void swag_sample(const float* mean, const float* sq, int64_t ld, int64_t d, int row0, int rows, uint64_t seed,
+                 float* out, cudaStream_t s);
+
 // copy rows (device, pitched) for set_grads: dst[p*ld + k] = src[p*d + k]
 void copy_rows(const float* src, int64_t d, float* dst, int64_t ld, int rows, cudaStream_t s);
 

@@ -441,5 +441,54 @@ int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int ro
   return 1;
 }
 
+// ---------------------------------------------------------------- NEXT-3: deep ensembles and diagonal SWAG
+__global__ void ensemble_step_kernel(float* __restrict__ theta, const float* __restrict__ grad, int64_t n4, float eps) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n4; t += (int64_t)gridDim.x * blockDim.x) {
+    float4 th = reinterpret_cast<float4*>(theta)[t];
+    const float4 g = __ldg(reinterpret_cast<const float4*>(grad) + t);
+    th.x = fmaf(eps, g.x, th.x);
+    th.y = fmaf(eps, g.y, th.y);
+    th.z = fmaf(eps, g.z, th.z);
+    th.w = fmaf(eps, g.w, th.w);
+    reinterpret_cast<float4*>(theta)[t] = th;
+  }
+}
+void ensemble_step(float* theta, const float* grad, int64_t ld, int rows, float eps, cudaStream_t s) {
+  const int64_t n4 = ld * rows / 4;  // ld % 32 == 0: whole float4s, padding stays 0 (g padding is 0)
+  ensemble_step_kernel<<<(unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 32), 256, 0, s>>>(theta, grad, n4, eps);
+}
+__global__ void swag_collect_kernel(const float* __restrict__ x, float* __restrict__ mean, float* __restrict__ sq,
+                                    int64_t count, float kf, float inv) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[t];
+    const float m = kf > 0.f ? mean[t] : 0.f, q = kf > 0.f ? sq[t] : 0.f;
+    mean[t] = fmaf(m, kf, v) * inv;
+    sq[t] = fmaf(q, kf, v * v) * inv;
+  }
+}
+void swag_collect(const float* x, float* mean, float* sq, int64_t count, int64_t k, cudaStream_t s) {
+  const float kf = (float)k, inv = 1.0f / (float)(k + 1);
+  swag_collect_kernel<<<(unsigned)std::min<int64_t>((count + 255) / 256, 148 * 32), 256, 0, s>>>(x, mean, sq, count,
+                                                                                              kf, inv);
+}
+__global__ void swag_sample_kernel(const float* __restrict__ mean, const float* __restrict__ sq, int64_t ld, int64_t d,
+                                   int row0, uint64_t seed, float* __restrict__ out) {
+  const int r = blockIdx.y;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < d; c += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t ctr = ((static_cast<uint64_t>(row0 + r) << 32) | static_cast<uint64_t>(c)) * 2ull;
+    const uint64_t m1 = mix64(seed ^ mix64(ctr)) >> 40, m2 = mix64(seed ^ mix64(ctr + 1)) >> 40;
+    const float u1 = (float)(m1 + 1) * 5.9604644775390625e-8f, u2 = (float)m2 * 5.9604644775390625e-8f;
+    const float z = sqrtf(-2.0f * logf(u1)) * cosf(6.283185307179586f * u2);
+    const float mu = mean[r * ld + c];
+    const float var = fmaxf(sq[r * ld + c] - mu * mu, 0.f);
+    out[r * d + c] = fmaf(sqrtf(var), z, mu);
+  }
+}
+void swag_sample(const float* mean, const float* sq, int64_t ld, int64_t d, int row0, int rows, uint64_t seed,
+                 float* out, cudaStream_t s) {
+  const int blocks = (int)std::min<int64_t>((d + 255) / 256, 1024);
+  swag_sample_kernel<<<dim3(blocks, rows), 256, 0, s>>>(mean, sq, ld, d, row0, seed, out);
+}
+
 }  // namespace kern
 }  // namespace push

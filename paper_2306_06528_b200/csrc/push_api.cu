@@ -60,7 +60,7 @@ struct Plan {
   kern::DistPlan dist{};
   // byte offsets into the workspace
   size_t o_theta0, o_theta1, o_grad, o_whi, o_wlo, o_dlt0, o_dlt1, o_err2, o_loss, o_loss_all, o_opw, o_opb,
-      o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf, o_pred;
+      o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf, o_pred, o_swag_mean, o_swag_sq;
   std::vector<size_t> o_act;
   // per-layer partial buffers, all alive until the single finalize launch at the end of a5
   std::vector<size_t> o_wpart, o_tpart, o_bpart;
@@ -89,6 +89,8 @@ static push_status validate(const push_config* c, int world) {
   if (c->bw_rule == PUSH_BW_FIXED && !(c->bw_h > 0.f)) return fail(PUSH_E_INVALID, "bw_h <= 0 (SPEC.md:100)");
   if (!(c->step_size > 0.f)) return fail(PUSH_E_INVALID, "step_size must be > 0");
   if (c->max_batch < 1) return fail(PUSH_E_SHAPE, "max_batch must be >= 1");
+  if (c->swag != 0 && c->swag != 1) return fail(PUSH_E_INVALID, "swag must be 0 or 1");
+  if (c->reserved != 0) return fail(PUSH_E_INVALID, "reserved must be 0");
   return PUSH_OK;
 }
 
@@ -193,6 +195,8 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.o_xbuf = take((int64_t)P.Bmax * P.layers[0].in);
   P.o_ybuf = take((int64_t)P.Bmax * top.out);
   P.o_pred = take((int64_t)P.n * P.Bmax * top.out);
+  P.o_swag_mean = take(c->swag ? (int64_t)P.nl * P.ld : 1);
+  P.o_swag_sq = take(c->swag ? (int64_t)P.nl * P.ld : 1);
   P.total = cur;
   return PUSH_OK;
 }
@@ -238,6 +242,8 @@ struct push_ctx {
   float *dpart = nullptr, *D = nullptr, *K = nullptr, *srow = nullptr, *h = nullptr;
   float *xbuf = nullptr, *ybuf = nullptr;
   float* pred = nullptr;  // predictive pushforward: n x B x d_out (own rows, then all-gathered)
+  float *swag_mean = nullptr, *swag_sq = nullptr;  // SWAG moments of the own rows (n_local x ld)
+  int64_t swag_count = 0;
   int pred_B = 0;
   int state = 0;  // 0 READY, 1 GRADS_READY
   bool broken = false;
@@ -699,6 +705,10 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   c->xbuf = F(P.o_xbuf);
   c->ybuf = F(P.o_ybuf);
   c->pred = F(P.o_pred);
+  if (cfg->swag) {
+    c->swag_mean = F(P.o_swag_mean);
+    c->swag_sq = F(P.o_swag_sq);
+  }
   // bandwidth constant c_n = fp32(1/ln n) or fp32(1/ln(n+1)), computed once in double (R4)
   if (cfg->bw_rule == PUSH_BW_MEDIAN_LN_N)
     c->c_ln = P.n > 1 ? (float)(1.0 / std::log((double)P.n)) : 1.f;
@@ -995,6 +1005,60 @@ push_status push_predict(push_ctx* c, const float* x_dev, int32_t B, float* pred
     if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
   }
   return PUSH_OK;
+}
+
+push_status push_ensemble_step(push_ctx* c, void* stream) {
+  push_status st = check_ctx(c);
+  if (st != PUSH_OK) return st;
+  if (c->state != 1) return fail(PUSH_E_STATE, "ensemble_step needs fresh gradients");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->theta_pending) {  // the Theta all-gather (started by the gradient call) must finish first
+    cudaError_t e = cudaStreamWaitEvent(s, c->ev_theta, 0);
+    if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
+    c->theta_pending = false;
+  }
+  const Plan& P = c->P;
+  float* th = c->theta[c->cur] + (int64_t)c->row0 * P.ld;
+  const float* g = c->grad + (int64_t)c->row0 * P.ld;
+  st = run_k(c, PC_UPDATE, 1, 12.0 * P.nl * (double)P.d, 2.0 * P.nl * (double)P.d, s, [&] {
+    kern::ensemble_step(th, g, P.ld, P.nl, c->cfg.step_size, s);
+    return PUSH_OK;
+  });
+  if (st != PUSH_OK) return sticky(c, st);
+  c->state = 0;
+  return PUSH_OK;
+}
+
+push_status push_swag_collect(push_ctx* c, void* stream) {
+  push_status st = check_ctx(c);
+  if (st != PUSH_OK) return st;
+  if (!c->swag_mean) return fail(PUSH_E_STATE, "SWAG buffers not allocated (cfg.swag = 0)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Plan& P = c->P;
+  const float* th = c->theta[c->cur] + (int64_t)c->row0 * P.ld;
+  const int64_t k = c->swag_count;
+  st = run_k(c, PC_UPDATE, 1, 20.0 * P.nl * (double)P.ld, 0, s, [&] {
+    kern::swag_collect(th, c->swag_mean, c->swag_sq, (int64_t)P.nl * P.ld, k, s);
+    return PUSH_OK;
+  });
+  if (st != PUSH_OK) return sticky(c, st);
+  c->swag_count = k + 1;
+  return PUSH_OK;
+}
+
+push_status push_swag_sample(push_ctx* c, uint64_t seed, float* out_dev, void* stream) {
+  push_status st = check_ctx(c);
+  if (st != PUSH_OK) return st;
+  if (!out_dev) return fail(PUSH_E_INVALID, "out_dev is NULL");
+  if (!c->swag_mean) return fail(PUSH_E_STATE, "SWAG buffers not allocated (cfg.swag = 0)");
+  if (c->swag_count < 1) return fail(PUSH_E_STATE, "no SWAG moments collected yet");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Plan& P = c->P;
+  st = run_k(c, PC_UPDATE, 1, 12.0 * P.nl * (double)P.d, 0, s, [&] {
+    kern::swag_sample(c->swag_mean, c->swag_sq, P.ld, P.d, c->row0, P.nl, seed, out_dev, s);
+    return PUSH_OK;
+  });
+  return st == PUSH_OK ? PUSH_OK : sticky(c, st);
 }
 
 push_status push_gather(push_ctx* c, int32_t what, float* out_host, void* stream) {

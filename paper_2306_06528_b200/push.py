@@ -31,7 +31,8 @@ MAX_LAYERS = 15
 EXPORTS = ["push_version", "push_last_error", "push_get_unique_id", "push_workspace_size", "push_init",
            "push_init_local_group", "push_particle_grads", "push_set_grads", "push_svgd_step", "push_step_graph",
            "push_step_host",
-           "push_gather", "push_predict", "push_profile_enable", "push_profile_read", "push_profile_trace", "push_launch_count",
+           "push_gather", "push_predict", "push_ensemble_step", "push_swag_collect", "push_swag_sample",
+           "push_profile_enable", "push_profile_read", "push_profile_trace", "push_launch_count",
            "push_destroy",
            "pushdbg_gemm3xtf32", "pushdbg_gemm1xtf32", "pushdbg_gemm"]
 
@@ -40,7 +41,7 @@ class PushConfig(Structure):
     _fields_ = [("n_particles", c_int32), ("n_layers", c_int32), ("dims", c_int32 * (MAX_LAYERS + 1)),
                 ("activation", c_int32), ("prior", c_int32), ("prior_sigma", c_float), ("lik_scale", c_float),
                 ("bw_rule", c_int32), ("bw_h", c_float), ("step_size", c_float), ("max_batch", c_int32),
-                ("seed", c_uint64)]
+                ("seed", c_uint64), ("swag", c_int32), ("reserved", c_int32)]
 
 
 class ProfileRow(Structure):
@@ -80,6 +81,9 @@ def lib():
         "push_step_host": ([P, P, P, c_int32, P, P], c_int32),
         "push_gather": ([P, c_int32, P, P], c_int32),
         "push_predict": ([P, P, c_int32, P, P, P, P], c_int32),
+        "push_ensemble_step": ([P, P], c_int32),
+        "push_swag_collect": ([P, P], c_int32),
+        "push_swag_sample": ([P, c_uint64, P, P], c_int32),
         "push_profile_enable": ([P, c_int32], c_int32),
         "push_profile_read": ([P, POINTER(ProfileRow), c_int32, POINTER(c_int32)], c_int32),
         "push_profile_trace": ([P, POINTER(c_int32), c_int32, POINTER(c_int32)], c_int32),
@@ -103,7 +107,7 @@ def check(status: int):
 
 
 def make_config(n_particles: int, dims, activation="tanh", prior="uniform", prior_sigma=1.0, lik_scale=1.0,
-                bw_rule="median", bw_h=1.0, step_size=1e-3, max_batch=1, seed=0) -> PushConfig:
+                bw_rule="median", bw_h=1.0, step_size=1e-3, max_batch=1, seed=0, swag=False) -> PushConfig:
     c = PushConfig()
     c.n_particles = n_particles
     c.n_layers = len(dims) - 1
@@ -118,6 +122,8 @@ def make_config(n_particles: int, dims, activation="tanh", prior="uniform", prio
     c.step_size = step_size
     c.max_batch = max_batch
     c.seed = seed
+    c.swag = 1 if swag else 0
+    c.reserved = 0
     return c
 
 
@@ -215,6 +221,18 @@ class Context:
         std = torch.empty((B, dout), dtype=torch.float32, device=x.device)
         check(lib().push_predict(self._h, _ptr(x), B, _ptr(pred), _ptr(mean), _ptr(std), _stream(stream)))
         return pred, mean, std
+
+    def ensemble_step(self, stream=None):
+        check(lib().push_ensemble_step(self._h, _stream(stream)))
+
+    def swag_collect(self, stream=None):
+        check(lib().push_swag_collect(self._h, _stream(stream)))
+
+    def swag_sample(self, seed: int, stream=None):
+        import torch
+        out = torch.empty((self.n_local, self.d), dtype=torch.float32, device="cuda")
+        check(lib().push_swag_sample(self._h, seed, _ptr(out), _stream(stream)))
+        return out
 
     # -- instrumentation
     def profile_enable(self, on: bool = True):

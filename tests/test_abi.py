@@ -37,8 +37,9 @@ def test_every_declared_symbol_is_exported(L):
 
 
 def test_config_struct_layout_matches_header():
-    assert ctypes.sizeof(push.PushConfig) == 112
+    assert ctypes.sizeof(push.PushConfig) == 120
     assert push.PushConfig.seed.offset == 104
+    assert push.PushConfig.swag.offset == 112
     assert ctypes.sizeof(push.ProfileRow) == 56
 
 

@@ -344,3 +344,34 @@ def test_predict_matches_oracle(n, dims, B):
         c.particle_grads(_dev(x2), _dev(y2))
         c.svgd_step()
     assert np.array_equal(ctx.gather("theta"), ctx2.gather("theta"))
+
+
+# ------------------------------------------------------------------ NEXT-3: deep ensembles, diagonal SWAG
+def test_ensemble_step_and_swag_match_oracle():
+    from oracle import swag as oswag
+    w = WORKLOADS["C1"]
+    dims = list(w.dims)
+    x, y = synth.workload_batch(w, 0)
+    ctx = push.Context(push.make_config(w.n_particles, dims, max_batch=w.batch, step_size=5e-2, seed=8, swag=True))
+    snaps = []
+    for t in range(4):
+        th = ctx.gather("theta")
+        ctx.particle_grads(_dev(x), _dev(y))
+        ctx.ensemble_step()
+        g = ctx.gather("grad")
+        assert rel_err(ctx.gather("theta"), oswag.ensemble_step(th, g, 5e-2)) <= 1e-6
+        ctx.swag_collect()
+        snaps.append(ctx.gather("theta"))
+    mean, mom2, _ = oswag.swag_moments(snaps)
+    z = oswag.swag_normal(99, 0, w.n_particles, ctx.d)
+    ref = oswag.swag_sample(mean, mom2, z)
+    smp = ctx.swag_sample(99).cpu().numpy()
+    sd = np.sqrt(np.maximum(mom2 - mean * mean, 0.0))
+    # fp32 moments: mom2 - mean^2 cancels, so the variance is only known to ~fp32 eps * (mom2 + mean^2);
+    # elementwise bound: |z| sqrt(that) + 1e-5 (|mean| + |z| sd)
+    var_err = 4.0 * np.finfo(np.float32).eps * (mom2 + mean * mean)
+    tol = np.abs(z) * np.sqrt(var_err) + 1e-5 * (np.abs(mean) + np.abs(z) * sd) + 1e-7
+    assert np.all(np.abs(smp - ref) <= tol)
+    assert np.array_equal(smp, ctx.swag_sample(99).cpu().numpy())      # same seed, same draw
+    with pytest.raises(push.PushError):
+        push.Context(push.make_config(2, [1, 4, 1], max_batch=4)).swag_collect()   # cfg.swag = 0
