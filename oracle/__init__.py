@@ -9,6 +9,8 @@ particle step (arXiv 2306.06528), written from the paper:
                      RBF kernel matrix, the SVGD direction
                      phi(theta_i) = (1/n) sum_j [K_ij grad log p(theta_j) + grad_{theta_j} K_ij]
                      and the Jacobi step (Fig. supp:svgd; north star).
+* ``oracle.svgd_paper`` — PusH's own update of the listing (per-tensor kernel, 1/n on the
+                     repulsion only, unweighted prior; NEXT-2).
 * ``oracle.init``  — the counter-based K0 initialiser (SplitMix64; R14).
 * ``oracle.swag``  — deep-ensemble step and diagonal SWAG moments / samples (NEXT-3).
 * ``oracle.predict`` — predictive pushforward: per-particle outputs, cross-particle mean and
@@ -23,4 +25,4 @@ against closed forms, finite differences, special cases and brute force.
 Functions without such a pin are marked "parity unpinned" (none at present;
 see DESIGN.md §Oracle).
 """
-from . import init, mlp, predict, svgd, swag  # noqa: F401
+from . import init, mlp, predict, svgd, svgd_paper, swag  # noqa: F401
