@@ -193,7 +193,11 @@ def run_ours(args, w):
     pdist.init("nccl", dev)
     nid = pdist.bootstrap_nccl_id(rank, ws)
     dims = list(w.dims)
-    cfg = push.make_config(w.n_particles, dims, max_batch=w.batch, step_size=1e-3, seed=0)
+    if args.variant == "paper":  # NEXT-2: PusH's own update, l = 1 (h = 2), its normal prior
+        cfg = push.make_config(w.n_particles, dims, max_batch=w.batch, step_size=1e-3, seed=0, bw_rule="fixed",
+                               bw_h=2.0, prior="gaussian", prior_sigma=1.0, variant=push.VARIANT_PAPER)
+    else:
+        cfg = push.make_config(w.n_particles, dims, max_batch=w.batch, step_size=1e-3, seed=0)
     ctx = push.Context(cfg, rank, ws, nid)
     nsteps = args.warmup + args.steps
     batches = [synth.workload_batch(w, s) for s in range(nsteps)]
@@ -310,6 +314,7 @@ def run_ours(args, w):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": w.name + ": " + w.note, "n_particles": w.n_particles, "dims": dims,
+                       "variant": args.variant,
                        "d": w.d, "batch": w.batch, "parallelism": f"particles sharded n/{ws} per GPU",
                        "l2": "per-step working set > 126 MB L2 (no flush)",
                        "launch": "eager" if args.no_graph else "cuda-graph (batch staged D2D into the context each step)"},
@@ -332,6 +337,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of the captured CUDA graph")
     ap.add_argument("--n-particles", type=int, default=0, help="override the workload's particle count (sweeps)")
+    ap.add_argument("--variant", default="canonical", choices=["canonical", "paper"],
+                    help="paper: PusH's own update (per-tensor kernel, 1/n on the repulsion, prior sum; NEXT-2)")
     args = ap.parse_args()
     w = WORKLOADS[args.config]
     if args.n_particles:

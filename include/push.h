@@ -76,12 +76,29 @@ enum { PUSH_PRIOR_UNIFORM = 0, PUSH_PRIOR_GAUSSIAN = 1 };               /* SPEC.
 enum { PUSH_BW_MEDIAN_LN_N = 0, PUSH_BW_MEDIAN_LN_N1 = 1, PUSH_BW_FIXED = 2 };
 enum {
   PUSH_WHAT_THETA = 0,   /* n x d canonical parameters (current Theta)            */
-  PUSH_WHAT_GRAD = 1,    /* n x d canonical g = grad log p of the last grads call   */
-  PUSH_WHAT_DIST = 2,    /* n x n squared distances D of the last step               */
-  PUSH_WHAT_H = 3,       /* 1 float: bandwidth h of the last step                     */
+  PUSH_WHAT_GRAD = 1,    /* n x d canonical g of the last grads call (likelihood term only under PRIOR_SUM) */
+  PUSH_WHAT_DIST = 2,    /* T x n x n squared distances D of the last step (T = 1 unless PER_TENSOR) */
+  PUSH_WHAT_H = 3,       /* T floats: bandwidth h of the last step                    */
   PUSH_WHAT_LOSS = 4,    /* n floats: per-particle MSE of the last grads call (pre-update) */
-  PUSH_WHAT_KERNEL = 5   /* n x n kernel matrix K of the last step                    */
+  PUSH_WHAT_KERNEL = 5   /* T x n_local x n kernel matrix K of the last step (own rows) */
 };
+
+/* Update variants: PusH's own `_svgd_update` differs
+ * from the canonical SVGD direction of the north star in three ways, each selectable alone:
+ *   PUSH_VAR_PER_TENSOR : the kernel is evaluated per parameter TENSOR (W_l and
+ *                         b_l of every layer, in module.parameters() order), T = 2L distance / kernel
+ *                         matrices, each with its own bandwidth under a median rule.
+ *   PUSH_VAR_PAPER_NORM : drive terms weighted 1 and the repulsion 1/n (A5)
+ *                         instead of 1/n on both.
+ *   PUSH_VAR_PRIOR_SUM  : G holds -lambda grad MSE only and the prior gradients of all n particles
+ *                         are added unweighted, sum_j grad log p0(theta_j) (A8),
+ *                         with the drive weight.
+ * PUSH_VARIANT_PAPER = all three; with bw_rule FIXED and bw_h = 2 it is the listing's
+ * kernel_bandwidth l = 1 (A1).  The update of particle i, element k of tensor t:
+ *   theta_ik += eps * ( w_d sum_j K^t_ij g_jk + w_r (2/h_t) sum_j K^t_ij (theta_ik - theta_jk)
+ *                       [+ w_d sum_j grad log p0(theta_j)_k] ),   w_d = 1 or 1/n, w_r = 1/n.
+ * With PER_TENSOR, PUSH_WHAT_DIST / KERNEL / H return T stacked matrices / values. */
+enum { PUSH_VAR_PER_TENSOR = 1, PUSH_VAR_PAPER_NORM = 2, PUSH_VAR_PRIOR_SUM = 4, PUSH_VARIANT_PAPER = 7 };
 
 /* Plain-old-data configuration (120 bytes; field order is ABI). */
 typedef struct {
@@ -98,7 +115,7 @@ typedef struct {
   int32_t max_batch;                   /* >= 1; sizes the workspace                           */
   uint64_t seed;                       /* K0 initialiser stream (R14)                         */
   int32_t swag;                        /* 1: allocate SWAG moment buffers (push_swag_*)       */
-  int32_t reserved;                    /* must be 0                                           */
+  int32_t variant;                     /* 0 = canonical SVGD; else an OR of PUSH_VAR_* (NEXT-2)  */
 } push_config;
 
 /* Library / build identification string (static storage). */

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 namespace push {
 namespace kern {
@@ -95,22 +96,34 @@ void init_theta(float* theta, int64_t ld, int row0, int rows, int64_t d, uint64_
                 cudaStream_t s);
 
 // ---------------------------------------------------------------- a7 distances
+// Column ranges ("tensors") over which separate distance matrices are summed: one range [0, ld) for
+// the canonical kernel over the whole theta, or W_l / b_l of every layer for PUSH_VAR_PER_TENSOR.
+constexpr int kMaxTensors = 2 * 15;
+struct TSplit { int s[kMaxTensors + 1]; };  // splits of tensor t are [s[t], s[t+1])
 struct DistPlan {
-  int T;        // tile side (16, 32 or 64)
+  int T;        // tile side (8, 16, 32 or 64)
   int ntile;    // ceil(n / T)
   int npairs;   // ntile*(ntile+1)/2 upper tile pairs
-  int splits;   // S_d
-  int64_t cols; // columns per split (multiple of 32)
+  int splits;   // S_d (all tensors)
+  int64_t cols; // columns per split (multiple of the staged sub-chunk width)
+  int tensors;  // T_k
+  TSplit tsplit;
+  std::vector<int64_t> ranges;  // [begin, end) column range of every split (uploaded to the device)
 };
-DistPlan dist_plan(int n, int64_t ld);
-void dist_partial(const float* theta, int64_t ld, int n, const DistPlan& pl, float* part, cudaStream_t s);
-// D[i][j] = sum_s part[s][i][j] (ascending s), D_ii = +0
-void dist_reduce(const float* part, int n, int splits, float* D, cudaStream_t s);
+// toff/tsize: the tensors' column ranges; `total` = the column count the split width is sized from.
+// The plan depends only on (n, tensor ranges), never on the number of ranks.
+DistPlan dist_plan(int n, int tensors, const int64_t* toff, const int64_t* tsize, int64_t total);
+// part[s][i][j] = sum_{c in range s} (theta_ic - theta_jc)^2; ranges_dev = pl.ranges on the device
+void dist_partial(const float* theta, int64_t ld, int n, const DistPlan& pl, const int64_t* ranges_dev, float* part,
+                  cudaStream_t s);
+// D[t][i][j] = sum_{s in tensor t} part[s][i][j] (ascending s), D_ii = +0
+void dist_reduce(const float* part, int n, const DistPlan& pl, float* D, cudaStream_t s);
 
 // ---------------------------------------------------------------- a8 + a9 bandwidth and kernel matrix
-// h from D (rule, c = fp32 1/ln n or 1/ln(n+1), or fixed bw_h); K[i][j] = exp(-D[row0+i][j]/h), srow[i] = sum_j K[i][j]
+// Per tensor t (one CTA each): h_t from D_t (rule, c = fp32 1/ln n or 1/ln(n+1), or fixed bw_h);
+// K[t][i][j] = exp(-D_t[row0+i][j]/h_t), srow[t][i] = sum_j K[t][i][j]
 void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c_ln, float bw_h, float* h, float* K,
-                      float* srow, cudaStream_t s);
+                      float* srow, int tensors, cudaStream_t s);
 
 // ---------------------------------------------------------------- a10 fused update
 // theta_next[row0+i][c] = theta_i[c] + (eps/n)[ sum_j K_ij (g_j[c] - r theta_j[c]) + r s_i theta_i[c] ], r = 2/h
@@ -118,6 +131,15 @@ void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c
 int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl, const float* K,
                 const float* srow, const float* h, float eps_over_n, float* theta_next, cudaStream_t s);
 int update_row_block(int n, int nl, int64_t ld);
+// NEXT-2 variants: column segments of <= kVarSegCols columns inside one tensor (x = begin, y = end, z = tensor)
+constexpr int kVarSegCols = 128;
+std::vector<int4> var_segments(int tensors, const int64_t* toff, const int64_t* tsize);
+// element c of tensor t (segment table segs_dev, nseg entries):
+//   theta_next_ic = theta_ic + eps_d [ sum_j K^t_ij (g_jc - r_t theta_jc) + r_t s^t_i theta_ic + pcoef sum_j theta_jc ]
+//   r_t = (2/h_t) alpha   (canonical weights: eps_d = eps/n, alpha = 1; paper: eps_d = eps, alpha = 1/n)
+int svgd_update_var(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl, const float* K,
+                    const float* srow, const float* h, const int4* segs_dev, int nseg, float alpha, float eps_d,
+                    float pcoef, float* theta_next, cudaStream_t s);
 
 // ---------------------------------------------------------------- NEXT-3: deep ensembles and diagonal SWAG
 // theta[p][k] += eps * g[p][k] for the own rows (in place)

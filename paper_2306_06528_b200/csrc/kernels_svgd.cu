@@ -8,6 +8,8 @@
 // a10 is phi(theta_i) = (1/n) sum_j [K_ij grad log p(theta_j) + grad_{theta_j} K_ij] with
 // grad_{theta_j} K_ij = (2/h)(theta_i - theta_j) K_ij regrouped as r (s_i theta_i - sum_j K_ij theta_j)
 // (north star).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -56,18 +58,29 @@ constexpr int kDistPad = 4;  // row stride CW+4 floats: 16-B aligned rows, 2-way
 template <int T>
 struct DistCW { static constexpr int v = T == 8 ? 256 : (T == 16 ? 128 : 64); };
 
-DistPlan dist_plan(int n, int64_t ld) {
+DistPlan dist_plan(int n, int tensors, const int64_t* toff, const int64_t* tsize, int64_t total) {
   DistPlan pl;
   pl.T = n <= 8 ? 8 : (n <= 16 ? 16 : (n <= 32 ? 32 : 64));
   pl.ntile = (n + pl.T - 1) / pl.T;
   pl.npairs = pl.ntile * (pl.ntile + 1) / 2;
   const int cw = pl.T == 8 ? 256 : (pl.T == 16 ? 128 : kDistCW);  // = DistCW<T>::v: split ranges are whole sub-chunks
-  const int64_t chunks = (ld + cw - 1) / cw;
+  const int64_t chunks = (total + cw - 1) / cw;
   int64_t want = (4 * 148 + pl.npairs - 1) / pl.npairs;
   if (want > chunks) want = chunks;
   if (want < 1) want = 1;
-  pl.cols = (((ld + want - 1) / want) + cw - 1) / cw * cw;
-  pl.splits = (int)((ld + pl.cols - 1) / pl.cols);
+  pl.cols = (((total + want - 1) / want) + cw - 1) / cw * cw;
+  pl.tensors = tensors;
+  pl.splits = 0;
+  for (int t = 0; t < tensors; ++t) {
+    pl.tsplit.s[t] = pl.splits;
+    const int64_t k = std::max<int64_t>(1, (tsize[t] + pl.cols - 1) / pl.cols);
+    for (int64_t q = 0; q < k; ++q) {
+      pl.ranges.push_back(toff[t] + q * pl.cols);
+      pl.ranges.push_back(std::min(toff[t] + tsize[t], toff[t] + (q + 1) * pl.cols));
+    }
+    pl.splits += (int)k;
+  }
+  pl.tsplit.s[tensors] = pl.splits;
   return pl;
 }
 
@@ -80,7 +93,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 template <int T, int RT>
 __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restrict__ theta, int64_t ld, int n,
-                                                           int ntile, int64_t cols, float* __restrict__ part) {
+                                                           int ntile, const int64_t* __restrict__ ranges,
+                                                           float* __restrict__ part) {
   constexpr int CW = DistCW<T>::v;
   constexpr int TP = T / RT, PT = TP * TP, G = 256 / PT, RS = CW + kDistPad;
   extern __shared__ __align__(16) float dsm[];  // [2 bufs][2 tiles][T][RS], then G*PT*RT*RT reduction
@@ -90,12 +104,15 @@ __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restri
   const bool diag = bi == bj;
   const int s = blockIdx.y;
   const int tid = threadIdx.x, g = tid / PT, pt = tid % PT, ty = pt / TP, tx = pt % TP;
-  const int64_t c_begin = s * cols, c_end = min(ld, c_begin + cols);
-  const int nsub = (int)((c_end - c_begin + CW - 1) / CW);
+  // split s covers columns [c_begin, c_end); staging starts at the 16-byte boundary below c_begin and
+  // 4-column groups that straddle either end are loaded element-wise with the outside columns zeroed
+  // (only per-tensor ranges have unaligned ends; the canonical ones are whole sub-chunks)
+  const int64_t c_begin = ranges[2 * s], c_end = ranges[2 * s + 1], c_al = c_begin & ~(int64_t)3;
+  const int nsub = (int)((c_end - c_al + CW - 1) / CW);
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));
   auto stage = [&](int sub) {
     const int buf = sub & 1;
-    const int64_t c0 = c_begin + (int64_t)sub * CW;
+    const int64_t c0 = c_al + (int64_t)sub * CW;
     const int ntiles_ld = diag ? 1 : 2;
     for (int idx = tid; idx < ntiles_ld * T * (CW / 4); idx += 256) {
       const int tl = idx / (T * (CW / 4));
@@ -103,9 +120,20 @@ __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restri
       const int r = rem / (CW / 4), c4 = rem - r * (CW / 4);
       const int grow = (tl ? bj : bi) * T + r;
       const int64_t col = c0 + 4 * c4;
-      const bool ok = grow < n && col < c_end;
-      const float* src = theta + (ok ? (int64_t)grow * ld + col : 0);
-      cp_async16(sbase + 4 * (((buf * 2 + tl) * T + r) * RS + 4 * c4), src, ok ? 16 : 0);
+      const bool ok = grow < n && col < c_end && col + 4 > c_begin;
+      const uint32_t dst = sbase + 4 * (((buf * 2 + tl) * T + r) * RS + 4 * c4);
+      if (ok && (col < c_begin || col + 4 > c_end)) {  // straddling group (per-tensor ranges only)
+        const float* src = theta + (int64_t)grow * ld;
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = (col + e >= c_begin && col + e < c_end) ? src[col + e] : 0.f;
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+                     "f"(v[3])
+                     : "memory");
+      } else {
+        const float* src = theta + (ok ? (int64_t)grow * ld + col : 0);
+        cp_async16(dst, src, ok ? 16 : 0);
+      }
     }
   };
   float acc[RT][RT];
@@ -169,7 +197,8 @@ __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restri
     }
 }
 template <int T, int RT>
-static void dist_launch(const float* theta, int64_t ld, int n, const DistPlan& pl, float* part, cudaStream_t s) {
+static void dist_launch(const float* theta, int64_t ld, int n, const DistPlan& pl, const int64_t* ranges, float* part,
+                        cudaStream_t s) {
   constexpr int TP = T / RT, PT = TP * TP, G = 256 / PT;
   const size_t smem = sizeof(float) * (4 * T * (DistCW<T>::v + kDistPad) + (G > 1 ? G * PT * RT * RT : 0));
   static bool attr = false;
@@ -177,33 +206,37 @@ static void dist_launch(const float* theta, int64_t ld, int n, const DistPlan& p
     cudaFuncSetAttribute(dist_partial_kernel<T, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  dist_partial_kernel<T, RT><<<dim3(pl.npairs, pl.splits), 256, smem, s>>>(theta, ld, n, pl.ntile, pl.cols, part);
+  dist_partial_kernel<T, RT><<<dim3(pl.npairs, pl.splits), 256, smem, s>>>(theta, ld, n, pl.ntile, ranges, part);
 }
-void dist_partial(const float* theta, int64_t ld, int n, const DistPlan& pl, float* part, cudaStream_t s) {
-  if (pl.T == 8) dist_launch<8, 1>(theta, ld, n, pl, part, s);
-  else if (pl.T == 16) dist_launch<16, 2>(theta, ld, n, pl, part, s);
-  else if (pl.T == 32) dist_launch<32, 2>(theta, ld, n, pl, part, s);
-  else dist_launch<64, 4>(theta, ld, n, pl, part, s);
+void dist_partial(const float* theta, int64_t ld, int n, const DistPlan& pl, const int64_t* ranges, float* part,
+                  cudaStream_t s) {
+  if (pl.T == 8) dist_launch<8, 1>(theta, ld, n, pl, ranges, part, s);
+  else if (pl.T == 16) dist_launch<16, 2>(theta, ld, n, pl, ranges, part, s);
+  else if (pl.T == 32) dist_launch<32, 2>(theta, ld, n, pl, ranges, part, s);
+  else dist_launch<64, 4>(theta, ld, n, pl, ranges, part, s);
 }
 
-// One warp per D entry: lane l sums splits s = l, l+32, ... ascending, then a fixed xor tree
-// (order depends only on the split count, which depends only on (n, ld)).
-__global__ void dist_reduce_kernel(const float* __restrict__ part, int n, int splits, float* __restrict__ D) {
+// One warp per D entry: lane l sums the tensor's splits s = s0 + l, s0 + l + 32, ... ascending, then a
+// fixed xor tree (order depends only on the split table, which depends only on n and the tensor ranges).
+__global__ void dist_reduce_kernel(const float* __restrict__ part, int n, int tensors, const TSplit ts,
+                                   float* __restrict__ D) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nn = (int64_t)n * n;
-  if (t >= nn) return;
-  const int i = (int)(t / n), j = (int)(t - (int64_t)i * n);
+  if (t >= nn * tensors) return;
+  const int tt = (int)(t / nn);
+  const int64_t e = t - tt * nn;
+  const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
   float v = 0.f;
   if (i != j)
-    for (int s = lane; s < splits; s += 32) v += part[s * nn + t];
+    for (int s = ts.s[tt] + lane; s < ts.s[tt + 1]; s += 32) v += part[s * nn + e];
 #pragma unroll
   for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
   if (lane == 0) D[t] = v;  // diagonal is exactly +0
 }
-void dist_reduce(const float* part, int n, int splits, float* D, cudaStream_t s) {
-  const int64_t nn = (int64_t)n * n;
-  dist_reduce_kernel<<<(unsigned)((nn * 32 + 255) / 256), 256, 0, s>>>(part, n, splits, D);
+void dist_reduce(const float* part, int n, const DistPlan& pl, float* D, cudaStream_t s) {
+  const int64_t nn = (int64_t)n * n * pl.tensors;
+  dist_reduce_kernel<<<(unsigned)((nn * 32 + 255) / 256), 256, 0, s>>>(part, n, pl.tensors, pl.tsplit, D);
 }
 
 // ---------------------------------------------------------------- a8 + a9
@@ -269,6 +302,11 @@ __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(const float* __res
                                                               float* __restrict__ K, float* __restrict__ srow,
                                                               int use_tri) {
   extern __shared__ float skeys[];
+  // CTA b: tensor b's distance matrix, bandwidth, kernel rows and row sums
+  D += (int64_t)blockIdx.x * n * n;
+  h_out += blockIdx.x;
+  K += (int64_t)blockIdx.x * nl * n;
+  srow += (int64_t)blockIdx.x * nl;
   __shared__ uint32_t hist[256];
   __shared__ uint32_t sh[2];
   __shared__ float s_h;
@@ -326,7 +364,7 @@ __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(const float* __res
   }
 }
 void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c_ln, float bw_h, float* h, float* K,
-                      float* srow, cudaStream_t s) {
+                      float* srow, int tensors, cudaStream_t s) {
   const int64_t m = (int64_t)n * (n - 1) / 2;
   const int use_tri = rule != PUSH_BW_FIXED && n > 1 && m <= kTriKeys;
   static bool attr = false;
@@ -334,7 +372,7 @@ void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c
     cudaFuncSetAttribute(bandwidth_kernel_impl, cudaFuncAttributeMaxDynamicSharedMemorySize, kTriKeys * 4);
     attr = true;
   }
-  bandwidth_kernel_impl<<<1, 1024, use_tri ? (size_t)m * 4 : 0, s>>>(D, n, row0, nl, rule, c_ln, bw_h, h, K, srow,
+  bandwidth_kernel_impl<<<tensors, 1024, use_tri ? (size_t)m * 4 : 0, s>>>(D, n, row0, nl, rule, c_ln, bw_h, h, K, srow,
                                                                     use_tri);
 }
 
@@ -438,6 +476,89 @@ int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int ro
     update_launch<8, 4>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next, s);
   else
     update_launch<16, 4>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next, s);
+  return 1;
+}
+
+// ---------------------------------------------------------------- NEXT-2: PusH's own update (variants)
+// One CTA = one segment of <= 128 columns inside a single tensor t x RB own rows; thread = one column.
+// The CTA keeps K^t's RB rows transposed in smem; per j a thread loads theta_jc and g_jc (coalesced
+// across the warp), issues RB/4 LDS.128 and RB + 2 FP32 ops.  Sums run over j ascending.
+std::vector<int4> var_segments(int tensors, const int64_t* toff, const int64_t* tsize) {
+  std::vector<int4> v;
+  for (int t = 0; t < tensors; ++t)
+    for (int64_t c = 0; c < tsize[t]; c += kVarSegCols)
+      v.push_back(make_int4((int)(toff[t] + c), (int)(toff[t] + std::min<int64_t>(tsize[t], c + kVarSegCols)), t, 0));
+  return v;
+}
+
+template <int RB>
+__global__ void __launch_bounds__(kVarSegCols) svgd_update_var_kernel(
+    const float* __restrict__ theta, const float* __restrict__ grad, int64_t ld, int n, int row0, int nl,
+    const float* __restrict__ K, const float* __restrict__ srow, const float* __restrict__ hptr,
+    const int4* __restrict__ segs, float alpha, float eps_d, float pcoef, float* __restrict__ theta_next) {
+  extern __shared__ __align__(16) float sKT[];  // [n][RB]: K^t_(rb0+i),j at sKT[j*RB + i]
+  const int4 seg = segs[blockIdx.x];
+  const int t = seg.z;
+  const int rb0 = blockIdx.y * RB;
+  const int rows = min(RB, nl - rb0);
+  const float* Kt = K + (int64_t)t * nl * n;
+  for (int idx = threadIdx.x; idx < RB * n; idx += blockDim.x) {
+    const int j = idx / RB, i = idx - j * RB;
+    sKT[idx] = i < rows ? Kt[(int64_t)(rb0 + i) * n + j] : 0.f;
+  }
+  __syncthreads();
+  const float r2 = 2.0f / hptr[t] * alpha;
+  const int64_t c = seg.x + threadIdx.x;
+  if (c >= seg.y) return;
+  float acc[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) acc[r] = 0.f;
+  float cs = 0.f;
+#pragma unroll 4
+  for (int j = 0; j < n; ++j) {
+    const float tv = __ldg(theta + (int64_t)j * ld + c);
+    const float m = fmaf(-r2, tv, __ldg(grad + (int64_t)j * ld + c));
+    cs += tv;
+    const float4* kj = reinterpret_cast<const float4*>(sKT + j * RB);
+#pragma unroll
+    for (int r4 = 0; r4 < RB / 4; ++r4) {
+      const float4 k4 = kj[r4];
+      acc[4 * r4 + 0] = fmaf(k4.x, m, acc[4 * r4 + 0]);
+      acc[4 * r4 + 1] = fmaf(k4.y, m, acc[4 * r4 + 1]);
+      acc[4 * r4 + 2] = fmaf(k4.z, m, acc[4 * r4 + 2]);
+      acc[4 * r4 + 3] = fmaf(k4.w, m, acc[4 * r4 + 3]);
+    }
+  }
+  const float* st = srow + (int64_t)t * nl;
+#pragma unroll
+  for (int r = 0; r < RB; ++r) {
+    if (r < rows) {
+      const int64_t i = row0 + rb0 + r;
+      const float ti = theta[i * ld + c];
+      theta_next[i * ld + c] = fmaf(eps_d, fmaf(pcoef, cs, fmaf(r2 * st[rb0 + r], ti, acc[r])), ti);
+    }
+  }
+}
+template <int RB>
+static void update_var_launch(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl,
+                              const float* K, const float* srow, const float* h, const int4* segs, int nseg,
+                              float alpha, float eps_d, float pcoef, float* theta_next, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(svgd_update_var_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const dim3 grid((unsigned)nseg, (unsigned)((nl + RB - 1) / RB));
+  svgd_update_var_kernel<RB><<<grid, kVarSegCols, sizeof(float) * RB * n, s>>>(
+      theta, grad, ld, n, row0, nl, K, srow, h, segs, alpha, eps_d, pcoef, theta_next);
+}
+int svgd_update_var(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl, const float* K,
+                    const float* srow, const float* h, const int4* segs, int nseg, float alpha, float eps_d,
+                    float pcoef, float* theta_next, cudaStream_t s) {
+  if (nl <= 8)
+    update_var_launch<8>(theta, grad, ld, n, row0, nl, K, srow, h, segs, nseg, alpha, eps_d, pcoef, theta_next, s);
+  else
+    update_var_launch<16>(theta, grad, ld, n, row0, nl, K, srow, h, segs, nseg, alpha, eps_d, pcoef, theta_next, s);
   return 1;
 }
 

@@ -58,9 +58,12 @@ struct Plan {
   int64_t wpart_elems = 0, tpart_elems = 0;  // (unused totals kept for reference)
   bool fuse_x0 = false;                     // layer 0 thin + layer 1 GEMM: dW_0 from layer 1's BWD epilogue
   kern::DistPlan dist{};
+  int tensors = 1;                          // distance / kernel matrices (2L under PUSH_VAR_PER_TENSOR)
+  std::vector<int64_t> toff, tsize;         // their column ranges
+  std::vector<int4> useg;                   // variant update segments (variant != 0)
   // byte offsets into the workspace
   size_t o_theta0, o_theta1, o_grad, o_whi, o_wlo, o_dlt0, o_dlt1, o_err2, o_loss, o_loss_all, o_opw, o_opb,
-      o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf, o_pred, o_swag_mean, o_swag_sq;
+      o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf, o_pred, o_swag_mean, o_swag_sq, o_dranges, o_useg;
   std::vector<size_t> o_act;
   // per-layer partial buffers, all alive until the single finalize launch at the end of a5
   std::vector<size_t> o_wpart, o_tpart, o_bpart;
@@ -90,7 +93,7 @@ static push_status validate(const push_config* c, int world) {
   if (!(c->step_size > 0.f)) return fail(PUSH_E_INVALID, "step_size must be > 0");
   if (c->max_batch < 1) return fail(PUSH_E_SHAPE, "max_batch must be >= 1");
   if (c->swag != 0 && c->swag != 1) return fail(PUSH_E_INVALID, "swag must be 0 or 1");
-  if (c->reserved != 0) return fail(PUSH_E_INVALID, "reserved must be 0");
+  if (c->variant < 0 || c->variant > PUSH_VARIANT_PAPER) return fail(PUSH_E_INVALID, "bad variant");
   return PUSH_OK;
 }
 
@@ -152,7 +155,21 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   const int chunks_max = (P.Bmax + kern::THIN_CHUNK - 1) / kern::THIN_CHUNK;
   P.wpart_elems = 8 * (int64_t)P.nl * max_w;
   P.tpart_elems = (int64_t)chunks_max * P.nl * max_t;
-  P.dist = kern::dist_plan(P.n, P.ld);
+  // distance tensors: the whole row [0, ld) (canonical), [0, d) (other variants) or every W_l / b_l
+  if (c->variant & PUSH_VAR_PER_TENSOR) {
+    for (const LayerPlan& lp : P.layers) {
+      P.toff.push_back(lp.off_w);
+      P.tsize.push_back((int64_t)lp.in * lp.out);
+      P.toff.push_back(lp.off_b);
+      P.tsize.push_back(lp.out);
+    }
+  } else {
+    P.toff.push_back(0);
+    P.tsize.push_back(c->variant ? P.d : P.ld);
+  }
+  P.tensors = (int)P.toff.size();
+  P.dist = kern::dist_plan(P.n, P.tensors, P.toff.data(), P.tsize.data(), c->variant ? P.d : P.ld);
+  if (c->variant) P.useg = kern::var_segments(P.tensors, P.toff.data(), P.tsize.data());
 
   size_t cur = 0;
   auto take = [&](int64_t elems) {
@@ -188,10 +205,12 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.o_opb = take((int64_t)P.RB * P.nl * top.out);
   P.o_xpart = take(P.fuse_x0 ? (int64_t)P.RB * P.nl * P.layers[0].out * P.layers[0].in : 1);
   P.o_dpart = take((int64_t)P.dist.splits * P.n * P.n);
-  P.o_D = take((int64_t)P.n * P.n);
-  P.o_K = take((int64_t)P.nl * P.n);
-  P.o_s = take(P.nl);
+  P.o_D = take((int64_t)P.tensors * P.n * P.n);
+  P.o_K = take((int64_t)P.tensors * P.nl * P.n);
+  P.o_s = take((int64_t)P.tensors * P.nl);
   P.o_h = take(32);
+  P.o_dranges = take(2 * (int64_t)P.dist.ranges.size());  // int64 pairs (2 floats' room each)
+  P.o_useg = take(4 * (int64_t)P.useg.size());
   P.o_xbuf = take((int64_t)P.Bmax * P.layers[0].in);
   P.o_ybuf = take((int64_t)P.Bmax * top.out);
   P.o_pred = take((int64_t)P.n * P.Bmax * top.out);
@@ -240,6 +259,8 @@ struct push_ctx {
   std::vector<float*> wpart, tpart, bpart;  // per layer
   float *opw = nullptr, *opb = nullptr, *xpart = nullptr;
   float *dpart = nullptr, *D = nullptr, *K = nullptr, *srow = nullptr, *h = nullptr;
+  int64_t* dranges = nullptr;  // distance split ranges (device copy of P.dist.ranges)
+  int4* useg = nullptr;        // variant update segments (device copy of P.useg)
   float *xbuf = nullptr, *ybuf = nullptr;
   float* pred = nullptr;  // predictive pushforward: n x B x d_out (own rows, then all-gathered)
   float *swag_mean = nullptr, *swag_sq = nullptr;  // SWAG moments of the own rows (n_local x ld)
@@ -559,7 +580,9 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
     xb ^= 1;
   }
   return run_k(c, PC_FINALIZE, 1, 0, 0, s, [&] {
-    kern::finalize_all(jobs.data(), (int)jobs.size(), th, g, ld, lambda, c->cfg.prior, inv_s2, nl, s);
+    // PUSH_VAR_PRIOR_SUM: G keeps the likelihood term only; a10 adds the unweighted prior sum
+    const int prior = (c->cfg.variant & PUSH_VAR_PRIOR_SUM) ? PUSH_PRIOR_UNIFORM : c->cfg.prior;
+    kern::finalize_all(jobs.data(), (int)jobs.size(), th, g, ld, lambda, prior, inv_s2, nl, s);
     return PUSH_OK;
   });
 }
@@ -577,20 +600,33 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   const float* th = c->theta[c->cur];
   const double nd4 = 4.0 * P.n * (double)P.d;
   st = run_k(c, PC_DIST, 2, nd4, 3.0 * P.n * (double)P.n * P.d / 2, s, [&] {
-    kern::dist_partial(th, P.ld, P.n, P.dist, c->dpart, s);
-    kern::dist_reduce(c->dpart, P.n, P.dist.splits, c->D, s);
+    kern::dist_partial(th, P.ld, P.n, P.dist, c->dranges, c->dpart, s);
+    kern::dist_reduce(c->dpart, P.n, P.dist, c->D, s);
     return PUSH_OK;
   });
   if (st != PUSH_OK) return st;
-  st = run_k(c, PC_BANDWIDTH, 1, 4.0 * P.n * P.n, 0, s, [&] {
-    kern::bandwidth_kernel(c->D, P.n, c->row0, P.nl, c->cfg.bw_rule, c->c_ln, c->cfg.bw_h, c->h, c->K, c->srow, s);
+  st = run_k(c, PC_BANDWIDTH, 1, 4.0 * P.tensors * P.n * P.n, 0, s, [&] {
+    kern::bandwidth_kernel(c->D, P.n, c->row0, P.nl, c->cfg.bw_rule, c->c_ln, c->cfg.bw_h, c->h, c->K, c->srow,
+                           P.tensors, s);
     return PUSH_OK;
   });
   if (st != PUSH_OK) return st;
   const float eps_n = c->cfg.step_size / (float)P.n;
   float* next = c->theta[c->cur ^ 1];
+  const int var = c->cfg.variant;
   st = run_k(c, PC_UPDATE, 1, 2.0 * nd4 + 4.0 * P.nl * (double)P.d, 2.0 * P.nl * (double)P.n * P.d, s, [&] {
-    kern::svgd_update(th, c->grad, P.ld, P.n, c->row0, P.nl, c->K, c->srow, c->h, eps_n, next, s);
+    if (var == 0) {
+      kern::svgd_update(th, c->grad, P.ld, P.n, c->row0, P.nl, c->K, c->srow, c->h, eps_n, next, s);
+    } else {  // NEXT-2 (include/push.h PUSH_VAR_*): weights w_d = eps or eps/n, repulsion eps/n
+      const bool pn = var & PUSH_VAR_PAPER_NORM;
+      const float eps_d = pn ? c->cfg.step_size : eps_n;
+      const float alpha = pn ? (float)(1.0 / P.n) : 1.0f;
+      const float pcoef = (var & PUSH_VAR_PRIOR_SUM) && c->cfg.prior == PUSH_PRIOR_GAUSSIAN
+                              ? (float)(-1.0 / ((double)c->cfg.prior_sigma * c->cfg.prior_sigma))
+                              : 0.f;
+      kern::svgd_update_var(th, c->grad, P.ld, P.n, c->row0, P.nl, c->K, c->srow, c->h, c->useg, (int)P.useg.size(),
+                            alpha, eps_d, pcoef, next, s);
+    }
     return PUSH_OK;
   });
   if (st != PUSH_OK) return st;
@@ -702,6 +738,8 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   c->K = F(P.o_K);
   c->srow = F(P.o_s);
   c->h = F(P.o_h);
+  c->dranges = reinterpret_cast<int64_t*>(c->ws + P.o_dranges);
+  c->useg = reinterpret_cast<int4*>(c->ws + P.o_useg);
   c->xbuf = F(P.o_xbuf);
   c->ybuf = F(P.o_ybuf);
   c->pred = F(P.o_pred);
@@ -724,6 +762,9 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   PUSH_CUDA_TRY(cudaMemsetAsync(c->theta[0], 0, nld * 4, s));
   PUSH_CUDA_TRY(cudaMemsetAsync(c->theta[1], 0, nld * 4, s));
   PUSH_CUDA_TRY(cudaMemsetAsync(c->grad, 0, nld * 4, s));
+  PUSH_CUDA_TRY(cudaMemcpyAsync(c->dranges, P.dist.ranges.data(), P.dist.ranges.size() * 8, cudaMemcpyHostToDevice, s));
+  if (!P.useg.empty())
+    PUSH_CUDA_TRY(cudaMemcpyAsync(c->useg, P.useg.data(), P.useg.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
   if (theta0_host) {
     PUSH_CUDA_TRY(cudaMemcpy2DAsync(c->theta[0], P.ld * 4, theta0_host, P.d * 4, P.d * 4, P.n,
                                     cudaMemcpyHostToDevice, s));
@@ -1087,7 +1128,8 @@ push_status push_gather(push_ctx* c, int32_t what, float* out_host, void* stream
     case PUSH_WHAT_KERNEL: {
       if (!c->has_step) return fail(PUSH_E_STATE, "no SVGD step yet");
       const float* src = what == PUSH_WHAT_DIST ? c->D : (what == PUSH_WHAT_H ? c->h : c->K);
-      const size_t cnt = what == PUSH_WHAT_DIST ? (size_t)P.n * P.n : (what == PUSH_WHAT_H ? 1 : (size_t)P.nl * P.n);
+      const size_t T = P.tensors;
+      const size_t cnt = what == PUSH_WHAT_DIST ? T * P.n * P.n : (what == PUSH_WHAT_H ? T : T * P.nl * P.n);
       cudaError_t e = cudaMemcpyAsync(out_host, src, cnt * 4, cudaMemcpyDeviceToHost, s);
       if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
       break;

@@ -22,6 +22,8 @@ PUSH_OK, PUSH_E_INVALID, PUSH_E_SHAPE, PUSH_E_STATE, PUSH_E_CUDA, PUSH_E_NCCL, P
 STATUS_NAMES = ["PUSH_OK", "PUSH_E_INVALID", "PUSH_E_SHAPE", "PUSH_E_STATE", "PUSH_E_CUDA", "PUSH_E_NCCL",
                 "PUSH_E_NOMEM", "PUSH_E_UNSUPPORTED"]
 ACT = {"tanh": 0, "relu": 1, "identity": 2}
+VAR_PER_TENSOR, VAR_PAPER_NORM, VAR_PRIOR_SUM = 1, 2, 4  # push_config.variant bits (NEXT-2)
+VARIANT_PAPER = 7
 PRIOR = {"uniform": 0, "gaussian": 1}
 BW = {"median": 0, "median_ln_n": 0, "median_ln_n1": 1, "fixed": 2}
 WHAT = {"theta": 0, "grad": 1, "dist": 2, "h": 3, "loss": 4, "kernel": 5}
@@ -41,7 +43,7 @@ class PushConfig(Structure):
     _fields_ = [("n_particles", c_int32), ("n_layers", c_int32), ("dims", c_int32 * (MAX_LAYERS + 1)),
                 ("activation", c_int32), ("prior", c_int32), ("prior_sigma", c_float), ("lik_scale", c_float),
                 ("bw_rule", c_int32), ("bw_h", c_float), ("step_size", c_float), ("max_batch", c_int32),
-                ("seed", c_uint64), ("swag", c_int32), ("reserved", c_int32)]
+                ("seed", c_uint64), ("swag", c_int32), ("variant", c_int32)]
 
 
 class ProfileRow(Structure):
@@ -107,7 +109,10 @@ def check(status: int):
 
 
 def make_config(n_particles: int, dims, activation="tanh", prior="uniform", prior_sigma=1.0, lik_scale=1.0,
-                bw_rule="median", bw_h=1.0, step_size=1e-3, max_batch=1, seed=0, swag=False) -> PushConfig:
+                bw_rule="median", bw_h=1.0, step_size=1e-3, max_batch=1, seed=0, swag=False,
+                variant=0) -> PushConfig:
+    """variant: 0 (canonical SVGD) or an OR of VAR_PER_TENSOR / VAR_PAPER_NORM / VAR_PRIOR_SUM
+    (VARIANT_PAPER = all three, include/push.h)."""
     c = PushConfig()
     c.n_particles = n_particles
     c.n_layers = len(dims) - 1
@@ -123,7 +128,7 @@ def make_config(n_particles: int, dims, activation="tanh", prior="uniform", prio
     c.max_batch = max_batch
     c.seed = seed
     c.swag = 1 if swag else 0
-    c.reserved = 0
+    c.variant = int(variant)
     return c
 
 
@@ -170,6 +175,8 @@ class Context:
         self.dims = [cfg.dims[i] for i in range(cfg.n_layers + 1)]
         self.d = int(sum(self.dims[l] * self.dims[l + 1] + self.dims[l + 1] for l in range(cfg.n_layers)))
         self.n_local = self.n // world_size
+        # distance / kernel matrices per step: one per W_l and b_l under VAR_PER_TENSOR, else one
+        self.n_tensors = 2 * cfg.n_layers if cfg.variant & VAR_PER_TENSOR else 1
         if _handle is not None:
             self._h, self._ws = _handle, _ws
             return
@@ -206,8 +213,10 @@ class Context:
         return loss
 
     def gather(self, what: str, stream=None) -> np.ndarray:
-        shape = {"theta": (self.n, self.d), "grad": (self.n, self.d), "dist": (self.n, self.n), "h": (1,),
-                 "loss": (self.n,), "kernel": (self.n_local, self.n)}[what]
+        T = self.n_tensors  # dist / kernel are stacked per tensor only under VAR_PER_TENSOR
+        lead = (T,) if T > 1 else ()
+        shape = {"theta": (self.n, self.d), "grad": (self.n, self.d), "dist": lead + (self.n, self.n), "h": (T,),
+                 "loss": (self.n,), "kernel": lead + (self.n_local, self.n)}[what]
         out = np.empty(shape, dtype=np.float32)
         check(lib().push_gather(self._h, WHAT[what], out.ctypes.data_as(c_void_p), _stream(stream)))
         return out

@@ -40,6 +40,7 @@ def test_config_struct_layout_matches_header():
     assert ctypes.sizeof(push.PushConfig) == 120
     assert push.PushConfig.seed.offset == 104
     assert push.PushConfig.swag.offset == 112
+    assert push.PushConfig.variant.offset == 116
     assert ctypes.sizeof(push.ProfileRow) == 56
 
 
@@ -77,3 +78,16 @@ def test_bad_dims_rejected(L):
     with pytest.raises(push.PushError) as e:
         push.workspace_size(cfg, 1)
     assert e.value.status == push.PUSH_E_SHAPE
+
+
+def test_variant_field_validated_on_host():
+    """push_config.variant: 0..7 accepted (OR of PUSH_VAR_*), anything else PUSH_E_INVALID; per-tensor
+    plans need workspace for T = 2L distance / kernel matrices."""
+    base = push.workspace_size(push.make_config(8, [2, 64, 64, 1], max_batch=64))
+    for v in range(8):
+        ws = push.workspace_size(push.make_config(8, [2, 64, 64, 1], max_batch=64, variant=v))
+        assert ws >= base if v & push.VAR_PER_TENSOR else ws > 0
+    for bad in (8, -1):
+        with pytest.raises(push.PushError) as e:
+            push.workspace_size(push.make_config(8, [2, 64, 64, 1], max_batch=64, variant=bad))
+        assert e.value.status == push.PUSH_E_INVALID
