@@ -100,7 +100,22 @@ enum {
  * With PER_TENSOR, PUSH_WHAT_DIST / KERNEL / H return T stacked matrices / values. */
 enum { PUSH_VAR_PER_TENSOR = 1, PUSH_VAR_PAPER_NORM = 2, PUSH_VAR_PRIOR_SUM = 4, PUSH_VARIANT_PAPER = 7 };
 
-/* Plain-old-data configuration (120 bytes; field order is ABI). */
+/* Kernel-phase exchange for world_size > 1:
+ *   PUSH_XCHG_ALLGATHER : every rank all-gathers Theta and G (n x ld each) and updates its own rows
+ *                         (NVLink bytes per rank per step 2 n ld (P-1)/P).
+ *   PUSH_XCHG_DSHARD    : the kernel phase is sharded over d: an all-to-all transposes the own rows'
+ *                         Theta and G into a column panel (all n rows x the rank's d-range, whole
+ *                         distance splits), each rank computes the distance partials of its splits,
+ *                         the partials are all-gathered (P x n^2 floats x splits per rank) and reduced
+ *                         in the fixed split order, every rank forms h and the full n x n K, updates
+ *                         all n rows of its panel, and a second all-to-all returns the updated columns
+ *                         to the row owners (NVLink bytes 3 n ld (P-1)/P^2 + partials).  Results are
+ *                         bit-identical to PUSH_XCHG_ALLGATHER for every P (same splits, same sums).
+ *                         Requires variant == 0.  With push_init_local_group the whole group's step
+ *                         runs in the call of the LAST rank (earlier ranks' calls only record it). */
+enum { PUSH_XCHG_ALLGATHER = 0, PUSH_XCHG_DSHARD = 1 };
+
+/* Plain-old-data configuration (128 bytes; field order is ABI). */
 typedef struct {
   int32_t n_particles;                 /* n >= 1, n % world_size == 0                        */
   int32_t n_layers;                    /* L in [1, 15] Linear layers                          */
@@ -116,6 +131,8 @@ typedef struct {
   uint64_t seed;                       /* K0 initialiser stream (R14)                         */
   int32_t swag;                        /* 1: allocate SWAG moment buffers (push_swag_*)       */
   int32_t variant;                     /* 0 = canonical SVGD; else an OR of PUSH_VAR_* (NEXT-2)  */
+  int32_t exchange;                    /* PUSH_XCHG_* (NEXT-4)                                 */
+  int32_t reserved;                    /* must be 0                                            */
 } push_config;
 
 /* Library / build identification string (static storage). */

@@ -116,8 +116,15 @@ DistPlan dist_plan(int n, int tensors, const int64_t* toff, const int64_t* tsize
 // part[s][i][j] = sum_{c in range s} (theta_ic - theta_jc)^2; ranges_dev = pl.ranges on the device
 void dist_partial(const float* theta, int64_t ld, int n, const DistPlan& pl, const int64_t* ranges_dev, float* part,
                   cudaStream_t s);
-// D[t][i][j] = sum_{s in tensor t} part[s][i][j] (ascending s), D_ii = +0
-void dist_reduce(const float* part, int n, const DistPlan& pl, float* D, cudaStream_t s);
+// Where split s's partial lives: rank q = the owner of s (s0[q] <= s < s0[q+1]) at slot q*smax + s - s0[q]
+// (NEXT-4: each rank's partials all-gathered in rank blocks of smax).  Identity: P = 1, s0 = {0, splits}.
+constexpr int kMaxRanks = 64;
+struct RankSlots {
+  int P, smax;
+  int s0[kMaxRanks + 1];
+};
+// D[t][i][j] = sum_{s in tensor t} part[slot(s)][i][j] (ascending s), D_ii = +0
+void dist_reduce(const float* part, int n, const DistPlan& pl, const RankSlots& rs, float* D, cudaStream_t s);
 
 // ---------------------------------------------------------------- a8 + a9 bandwidth and kernel matrix
 // Per tensor t (one CTA each): h_t from D_t (rule, c = fp32 1/ln n or 1/ln(n+1), or fixed bw_h);

@@ -219,7 +219,7 @@ void dist_partial(const float* theta, int64_t ld, int n, const DistPlan& pl, con
 // One warp per D entry: lane l sums the tensor's splits s = s0 + l, s0 + l + 32, ... ascending, then a
 // fixed xor tree (order depends only on the split table, which depends only on n and the tensor ranges).
 __global__ void dist_reduce_kernel(const float* __restrict__ part, int n, int tensors, const TSplit ts,
-                                   float* __restrict__ D) {
+                                   const RankSlots rs, float* __restrict__ D) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nn = (int64_t)n * n;
@@ -228,15 +228,20 @@ __global__ void dist_reduce_kernel(const float* __restrict__ part, int n, int te
   const int64_t e = t - tt * nn;
   const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
   float v = 0.f;
-  if (i != j)
-    for (int s = ts.s[tt] + lane; s < ts.s[tt + 1]; s += 32) v += part[s * nn + e];
+  if (i != j) {
+    int q = 0;  // owner rank of split s (monotone in s)
+    for (int s = ts.s[tt] + lane; s < ts.s[tt + 1]; s += 32) {
+      while (q + 1 < rs.P && s >= rs.s0[q + 1]) ++q;
+      v += part[(int64_t)(q * rs.smax + s - rs.s0[q]) * nn + e];
+    }
+  }
 #pragma unroll
   for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
   if (lane == 0) D[t] = v;  // diagonal is exactly +0
 }
-void dist_reduce(const float* part, int n, const DistPlan& pl, float* D, cudaStream_t s) {
+void dist_reduce(const float* part, int n, const DistPlan& pl, const RankSlots& rs, float* D, cudaStream_t s) {
   const int64_t nn = (int64_t)n * n * pl.tensors;
-  dist_reduce_kernel<<<(unsigned)((nn * 32 + 255) / 256), 256, 0, s>>>(part, n, pl.tensors, pl.tsplit, D);
+  dist_reduce_kernel<<<(unsigned)((nn * 32 + 255) / 256), 256, 0, s>>>(part, n, pl.tensors, pl.tsplit, rs, D);
 }
 
 // ---------------------------------------------------------------- a8 + a9

@@ -18,6 +18,9 @@ using FnGetUniqueId = Result (*)(UniqueId*);
 using FnCommInitRank = Result (*)(Comm*, int, UniqueId, int);
 using FnAllGather = Result (*)(const void*, void*, size_t, int, Comm, cudaStream_t);
 using FnCommDestroy = Result (*)(Comm);
+using FnSend = Result (*)(const void*, size_t, int, int, Comm, cudaStream_t);
+using FnRecv = Result (*)(void*, size_t, int, int, Comm, cudaStream_t);
+using FnGroup = Result (*)();
 using FnGetErrorString = const char* (*)(Result);
 
 struct Api {
@@ -27,6 +30,9 @@ struct Api {
   FnAllGather all_gather = nullptr;
   FnCommDestroy comm_destroy = nullptr;
   FnCommDestroy comm_abort = nullptr;
+  FnSend send = nullptr;
+  FnRecv recv = nullptr;
+  FnGroup group_start = nullptr, group_end = nullptr;
   FnGetErrorString err = nullptr;
   std::string why;
 };
@@ -58,7 +64,12 @@ push_status load() {
     g_api.comm_destroy = reinterpret_cast<FnCommDestroy>(dlsym(h, "ncclCommDestroy"));
     g_api.comm_abort = reinterpret_cast<FnCommDestroy>(dlsym(h, "ncclCommAbort"));
     g_api.err = reinterpret_cast<FnGetErrorString>(dlsym(h, "ncclGetErrorString"));
-    if (!g_api.get_unique_id || !g_api.comm_init_rank || !g_api.all_gather || !g_api.comm_destroy)
+    g_api.send = reinterpret_cast<FnSend>(dlsym(h, "ncclSend"));
+    g_api.recv = reinterpret_cast<FnRecv>(dlsym(h, "ncclRecv"));
+    g_api.group_start = reinterpret_cast<FnGroup>(dlsym(h, "ncclGroupStart"));
+    g_api.group_end = reinterpret_cast<FnGroup>(dlsym(h, "ncclGroupEnd"));
+    if (!g_api.get_unique_id || !g_api.comm_init_rank || !g_api.all_gather || !g_api.comm_destroy || !g_api.send ||
+        !g_api.recv || !g_api.group_start || !g_api.group_end)
       g_api.why = "libnccl.so.2 lacks required symbols";
   });
   if (!g_api.why.empty()) return fail(PUSH_E_NCCL, g_api.why);
@@ -82,6 +93,23 @@ push_status comm_init_rank(Comm* comm, int nranks, const UniqueId& id, int rank)
 push_status allgather_f32(const float* send, float* recv, size_t count, Comm comm, cudaStream_t s) {
   Result r = g_api.all_gather(send, recv, count, kNcclFloat32, comm, s);
   return r ? nfail("ncclAllGather", r) : PUSH_OK;
+}
+
+push_status group_start() {
+  Result r = g_api.group_start();
+  return r ? nfail("ncclGroupStart", r) : PUSH_OK;
+}
+push_status group_end() {
+  Result r = g_api.group_end();
+  return r ? nfail("ncclGroupEnd", r) : PUSH_OK;
+}
+push_status send_f32(const float* buf, size_t count, int peer, Comm comm, cudaStream_t s) {
+  Result r = g_api.send(buf, count, kNcclFloat32, peer, comm, s);
+  return r ? nfail("ncclSend", r) : PUSH_OK;
+}
+push_status recv_f32(float* buf, size_t count, int peer, Comm comm, cudaStream_t s) {
+  Result r = g_api.recv(buf, count, kNcclFloat32, peer, comm, s);
+  return r ? nfail("ncclRecv", r) : PUSH_OK;
 }
 
 void comm_release(Comm comm, bool abort) {

@@ -18,6 +18,11 @@ push_status get_unique_id(UniqueId* id);
 push_status comm_init_rank(Comm* comm, int nranks, const UniqueId& id, int rank);
 // in-place when send == recv + rank*count
 push_status allgather_f32(const float* send, float* recv, size_t count, Comm comm, cudaStream_t s);
+// grouped point-to-point (the NEXT-4 all-to-all transposes): group_start; send/recv ...; group_end
+push_status group_start();
+push_status group_end();
+push_status send_f32(const float* buf, size_t count, int peer, Comm comm, cudaStream_t s);
+push_status recv_f32(float* buf, size_t count, int peer, Comm comm, cudaStream_t s);
 void comm_release(Comm comm, bool abort);
 }  // namespace nccl
 }  // namespace push

@@ -61,9 +61,17 @@ struct Plan {
   int tensors = 1;                          // distance / kernel matrices (2L under PUSH_VAR_PER_TENSOR)
   std::vector<int64_t> toff, tsize;         // their column ranges
   std::vector<int4> useg;                   // variant update segments (variant != 0)
+  // NEXT-4 d-sharded kernel phase: rank q owns the distance splits [ds_s0[q], ds_s0[q+1]) = the columns
+  // [ds_c0[q], ds_c0[q+1]) (whole splits, so every sum keeps the order of the all-gather path)
+  bool ds = false;
+  std::vector<int> ds_s0;
+  std::vector<int64_t> ds_c0;
+  int64_t ds_wmax = 0;  // widest column panel
+  int ds_smax = 0;      // most splits on one rank (the all-gathered partial slots per rank)
   // byte offsets into the workspace
   size_t o_theta0, o_theta1, o_grad, o_whi, o_wlo, o_dlt0, o_dlt1, o_err2, o_loss, o_loss_all, o_opw, o_opb,
-      o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf, o_pred, o_swag_mean, o_swag_sq, o_dranges, o_useg;
+      o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf, o_pred, o_swag_mean, o_swag_sq, o_dranges, o_useg,
+      o_pth, o_pg, o_pth2, o_pack_th, o_pack_g;
   std::vector<size_t> o_act;
   // per-layer partial buffers, all alive until the single finalize launch at the end of a5
   std::vector<size_t> o_wpart, o_tpart, o_bpart;
@@ -94,6 +102,11 @@ static push_status validate(const push_config* c, int world) {
   if (c->max_batch < 1) return fail(PUSH_E_SHAPE, "max_batch must be >= 1");
   if (c->swag != 0 && c->swag != 1) return fail(PUSH_E_INVALID, "swag must be 0 or 1");
   if (c->variant < 0 || c->variant > PUSH_VARIANT_PAPER) return fail(PUSH_E_INVALID, "bad variant");
+  if (c->exchange != PUSH_XCHG_ALLGATHER && c->exchange != PUSH_XCHG_DSHARD) return fail(PUSH_E_INVALID, "bad exchange");
+  if (c->exchange == PUSH_XCHG_DSHARD && c->variant != 0)
+    return fail(PUSH_E_INVALID, "exchange DSHARD needs variant 0");
+  if (world > kern::kMaxRanks) return fail(PUSH_E_INVALID, "world_size > 64");
+  if (c->reserved != 0) return fail(PUSH_E_INVALID, "reserved must be 0");
   return PUSH_OK;
 }
 
@@ -170,6 +183,16 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.tensors = (int)P.toff.size();
   P.dist = kern::dist_plan(P.n, P.tensors, P.toff.data(), P.tsize.data(), c->variant ? P.d : P.ld);
   if (c->variant) P.useg = kern::var_segments(P.tensors, P.toff.data(), P.tsize.data());
+  P.ds = c->exchange == PUSH_XCHG_DSHARD;
+  if (P.ds) {
+    const int S = P.dist.splits;
+    for (int q = 0; q <= world; ++q) P.ds_s0.push_back((int)((int64_t)q * S / world));
+    for (int q = 0; q <= world; ++q) P.ds_c0.push_back(P.ds_s0[q] < S ? P.dist.ranges[2 * P.ds_s0[q]] : P.ld);
+    for (int q = 0; q < world; ++q) {
+      P.ds_wmax = std::max(P.ds_wmax, P.ds_c0[q + 1] - P.ds_c0[q]);
+      P.ds_smax = std::max(P.ds_smax, P.ds_s0[q + 1] - P.ds_s0[q]);
+    }
+  }
 
   size_t cur = 0;
   auto take = [&](int64_t elems) {
@@ -204,10 +227,16 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.o_opw = take((int64_t)P.RB * P.nl * top.out * top.in);
   P.o_opb = take((int64_t)P.RB * P.nl * top.out);
   P.o_xpart = take(P.fuse_x0 ? (int64_t)P.RB * P.nl * P.layers[0].out * P.layers[0].in : 1);
-  P.o_dpart = take((int64_t)P.dist.splits * P.n * P.n);
+  P.o_dpart = take((int64_t)(P.ds ? world * P.ds_smax : P.dist.splits) * P.n * P.n);
   P.o_D = take((int64_t)P.tensors * P.n * P.n);
-  P.o_K = take((int64_t)P.tensors * P.nl * P.n);
-  P.o_s = take((int64_t)P.tensors * P.nl);
+  P.o_K = take((int64_t)P.tensors * (P.ds ? P.n : P.nl) * P.n);  // d-sharded: K of all n rows
+  P.o_s = take((int64_t)P.tensors * (P.ds ? P.n : P.nl));
+  const int64_t pan = P.ds ? (int64_t)P.n * P.ds_wmax : 1;  // column panels (n x w) and send/recv staging
+  P.o_pth = take(pan);
+  P.o_pg = take(pan);
+  P.o_pth2 = take(pan);
+  P.o_pack_th = take(pan);
+  P.o_pack_g = take(pan);
   P.o_h = take(32);
   P.o_dranges = take(2 * (int64_t)P.dist.ranges.size());  // int64 pairs (2 floats' room each)
   P.o_useg = take(4 * (int64_t)P.useg.size());
@@ -261,6 +290,13 @@ struct push_ctx {
   float *dpart = nullptr, *D = nullptr, *K = nullptr, *srow = nullptr, *h = nullptr;
   int64_t* dranges = nullptr;  // distance split ranges (device copy of P.dist.ranges)
   int4* useg = nullptr;        // variant update segments (device copy of P.useg)
+  // NEXT-4 (d-sharded kernel phase): this rank's panel width, its splits (ranges relative to the panel),
+  // where every rank's partials live, and the panels / staging buffers
+  int64_t ds_w = 0, ds_c = 0;
+  push::kern::DistPlan dist_own;
+  push::kern::RankSlots slots{};
+  float *pth = nullptr, *pg = nullptr, *pth2 = nullptr, *pack_th = nullptr, *pack_g = nullptr;
+  bool ds_deferred = false;  // local group: this rank's step runs in the last rank's call
   float *xbuf = nullptr, *ybuf = nullptr;
   float* pred = nullptr;  // predictive pushforward: n x B x d_out (own rows, then all-gathered)
   float *swag_mean = nullptr, *swag_sq = nullptr;  // SWAG moments of the own rows (n_local x ld)
@@ -418,7 +454,7 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
   // C1: Theta rows of every rank (needed by a7/a10; unchanged during the gradient phase, whose kernels
   // only read the own rows, which the in-place all-gather only reads): on the comm stream, joined in
   // push_svgd_step
-  if (c->world > 1 || c->comm) {
+  if ((c->world > 1 || c->comm) && !P.ds) {
     PUSH_CUDA_TRY(cudaEventRecord(c->ev_fork, s));
     PUSH_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
     if ((st = exchange(c, BUF_THETA, c->comm_stream)) != PUSH_OK) return st;
@@ -588,9 +624,148 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
 }
 
 // ------------------------------------------------------------------ step (a6-a10)
+// ------------------------------------------------------------------ NEXT-4: d-sharded kernel phase
+// (include/push.h PUSH_XCHG_DSHARD).  Rank q owns the columns [c_q, c_q + w_q)
+// of every particle for a7-a10: three phases, each a collective step of the group.
+//   1  transpose: own rows' Theta / G columns of rank q -> rows [r n_l, (r+1) n_l) of q's panels
+//      (n x w_q, pitch w_q); the distance partials of q's whole splits over its panel
+//   2  all-gather of the partials (rank blocks of smax n^2), the fixed-order reduction into D, h and K
+//      of all n rows, the update of all n rows of the panel into pth2
+//   3  transpose back: panel rows of rank r -> r's next Theta buffer, columns of q
+// Every element sees the same splits, sums and update arithmetic as the all-gather path: results are
+// bit-identical for every P.
+static push_status ds_phase1(push_ctx* c, cudaStream_t s) {
+  const Plan& P = c->P;
+  const int W = c->world, nl = P.nl;
+  const int64_t ld = P.ld, wo = c->ds_w;
+  push_status st = run_k(c, PC_EXCHANGE, 0, 8.0 * P.n * wo, 0, s, [&]() -> push_status {
+    if (c->group || !c->comm) {  // loopback (or a single rank): pull the own columns from every row owner
+      for (int q = 0; q < W && wo > 0; ++q) {
+        push_ctx* pc = c->group ? c->group->members[q] : c;
+        const int64_t src = (int64_t)q * nl * ld + c->ds_c;
+        PUSH_CUDA_TRY(cudaMemcpy2DAsync(c->pth + (int64_t)q * nl * wo, wo * 4, pc->theta[c->cur] + src, ld * 4,
+                                        wo * 4, nl, cudaMemcpyDeviceToDevice, s));
+        PUSH_CUDA_TRY(cudaMemcpy2DAsync(c->pg + (int64_t)q * nl * wo, wo * 4, pc->grad + src, ld * 4, wo * 4, nl,
+                                        cudaMemcpyDeviceToDevice, s));
+      }
+      return PUSH_OK;
+    }
+    const float* th = c->theta[c->cur] + (int64_t)c->row0 * ld;
+    const float* g = c->grad + (int64_t)c->row0 * ld;
+    for (int q = 0; q < W; ++q) {  // pack the own rows' columns of rank q (contiguous n_l x w_q blocks)
+      const int64_t wq = P.ds_c0[q + 1] - P.ds_c0[q];
+      if (wq == 0) continue;
+      const int64_t dst = (int64_t)q * nl * P.ds_wmax;
+      PUSH_CUDA_TRY(cudaMemcpy2DAsync(c->pack_th + dst, wq * 4, th + P.ds_c0[q], ld * 4, wq * 4, nl,
+                                      cudaMemcpyDeviceToDevice, s));
+      PUSH_CUDA_TRY(cudaMemcpy2DAsync(c->pack_g + dst, wq * 4, g + P.ds_c0[q], ld * 4, wq * 4, nl,
+                                      cudaMemcpyDeviceToDevice, s));
+    }
+    push_status e = nccl::group_start();
+    for (int q = 0; q < W && e == PUSH_OK; ++q) {
+      const int64_t wq = P.ds_c0[q + 1] - P.ds_c0[q];
+      const int64_t dst = (int64_t)q * nl * P.ds_wmax;
+      if (wq > 0 && e == PUSH_OK) e = nccl::send_f32(c->pack_th + dst, nl * wq, q, c->comm, s);
+      if (wq > 0 && e == PUSH_OK) e = nccl::send_f32(c->pack_g + dst, nl * wq, q, c->comm, s);
+      if (wo > 0 && e == PUSH_OK) e = nccl::recv_f32(c->pth + (int64_t)q * nl * wo, nl * wo, q, c->comm, s);
+      if (wo > 0 && e == PUSH_OK) e = nccl::recv_f32(c->pg + (int64_t)q * nl * wo, nl * wo, q, c->comm, s);
+    }
+    const push_status e2 = nccl::group_end();
+    return e != PUSH_OK ? e : e2;
+  });
+  if (st != PUSH_OK || c->dist_own.splits == 0) return st;
+  float* part = c->dpart + (int64_t)c->rank * P.ds_smax * P.n * P.n;
+  return run_k(c, PC_DIST, 1, 4.0 * P.n * wo, 3.0 * P.n * (double)P.n * wo / 2, s, [&] {
+    kern::dist_partial(c->pth, wo, P.n, c->dist_own, c->dranges, part, s);
+    return PUSH_OK;
+  });
+}
+
+static push_status ds_phase2(push_ctx* c, cudaStream_t s) {
+  const Plan& P = c->P;
+  const int W = c->world;
+  const int64_t blk = (int64_t)P.ds_smax * P.n * P.n, wo = c->ds_w;
+  push_status st = PUSH_OK;
+  if (W > 1 || c->comm) {
+    st = run_k(c, PC_EXCHANGE, 0, 4.0 * blk * (W - 1), 0, s, [&]() -> push_status {
+      if (c->group) {
+        for (int q = 0; q < W; ++q)
+          if (q != c->rank)
+            PUSH_CUDA_TRY(cudaMemcpyAsync(c->dpart + q * blk, c->group->members[q]->dpart + q * blk, blk * 4,
+                                          cudaMemcpyDeviceToDevice, s));
+        return PUSH_OK;
+      }
+      return nccl::allgather_f32(c->dpart + c->rank * blk, c->dpart, blk, c->comm, s);
+    });
+    if (st != PUSH_OK) return st;
+  }
+  st = run_k(c, PC_DIST, 1, 4.0 * P.n * P.n * (double)P.dist.splits, 0, s, [&] {
+    kern::dist_reduce(c->dpart, P.n, P.dist, c->slots, c->D, s);
+    return PUSH_OK;
+  });
+  if (st != PUSH_OK) return st;
+  st = run_k(c, PC_BANDWIDTH, 1, 4.0 * P.n * P.n, 0, s, [&] {
+    kern::bandwidth_kernel(c->D, P.n, 0, P.n, c->cfg.bw_rule, c->c_ln, c->cfg.bw_h, c->h, c->K, c->srow, 1, s);
+    return PUSH_OK;
+  });
+  if (st != PUSH_OK || wo == 0) return st;
+  const float eps_n = c->cfg.step_size / (float)P.n;
+  return run_k(c, PC_UPDATE, 1, 12.0 * P.n * (double)wo, 2.0 * P.n * (double)P.n * wo, s, [&] {
+    kern::svgd_update(c->pth, c->pg, wo, P.n, 0, P.n, c->K, c->srow, c->h, eps_n, c->pth2, s);
+    return PUSH_OK;
+  });
+}
+
+static push_status ds_phase3(push_ctx* c, cudaStream_t s) {
+  const Plan& P = c->P;
+  const int W = c->world, nl = P.nl;
+  const int64_t ld = P.ld, wo = c->ds_w;
+  return run_k(c, PC_EXCHANGE, 0, 4.0 * P.n * wo, 0, s, [&]() -> push_status {
+    if (c->group || !c->comm) {  // loopback: push the updated columns into every row owner's next buffer
+      for (int q = 0; q < W && wo > 0; ++q) {
+        push_ctx* pc = c->group ? c->group->members[q] : c;
+        PUSH_CUDA_TRY(cudaMemcpy2DAsync(pc->theta[c->cur ^ 1] + (int64_t)q * nl * ld + c->ds_c, ld * 4,
+                                        c->pth2 + (int64_t)q * nl * wo, wo * 4, wo * 4, nl, cudaMemcpyDeviceToDevice,
+                                        s));
+      }
+      return PUSH_OK;
+    }
+    push_status e = nccl::group_start();
+    for (int q = 0; q < W && e == PUSH_OK; ++q) {
+      const int64_t wq = P.ds_c0[q + 1] - P.ds_c0[q];
+      if (wo > 0 && e == PUSH_OK) e = nccl::send_f32(c->pth2 + (int64_t)q * nl * wo, nl * wo, q, c->comm, s);
+      if (wq > 0 && e == PUSH_OK) e = nccl::recv_f32(c->pack_th + (int64_t)q * nl * P.ds_wmax, nl * wq, q, c->comm, s);
+    }
+    const push_status e2 = nccl::group_end();
+    if (e != PUSH_OK || e2 != PUSH_OK) return e != PUSH_OK ? e : e2;
+    float* nxt = c->theta[c->cur ^ 1] + (int64_t)c->row0 * ld;
+    for (int q = 0; q < W; ++q) {  // unpack rank q's columns into the own rows
+      const int64_t wq = P.ds_c0[q + 1] - P.ds_c0[q];
+      if (wq == 0) continue;
+      PUSH_CUDA_TRY(cudaMemcpy2DAsync(nxt + P.ds_c0[q], ld * 4, c->pack_th + (int64_t)q * nl * P.ds_wmax, wq * 4,
+                                      wq * 4, nl, cudaMemcpyDeviceToDevice, s));
+    }
+    return PUSH_OK;
+  });
+}
+
+// The whole group's d-sharded step on one stream (loopback groups: called by the last rank).
+static push_status ds_group_step(const std::vector<push_ctx*>& m, cudaStream_t s) {
+  push_status st;
+  for (push_ctx* c : m)
+    if ((st = ds_phase1(c, s)) != PUSH_OK) return st;
+  for (push_ctx* c : m)
+    if ((st = ds_phase2(c, s)) != PUSH_OK) return st;
+  for (push_ctx* c : m)
+    if ((st = ds_phase3(c, s)) != PUSH_OK) return st;
+  for (push_ctx* c : m) c->cur ^= 1;
+  return PUSH_OK;
+}
+
 static push_status do_step(push_ctx* c, cudaStream_t s) {
   const Plan& P = c->P;
   push_status st;
+  if (P.ds) return ds_group_step({c}, s);  // NCCL ranks (or one rank): three collective phases
   if (c->theta_pending) {  // join the Theta all-gather started by the gradient call
     PUSH_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_theta, 0));
     c->theta_pending = false;
@@ -601,7 +776,7 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   const double nd4 = 4.0 * P.n * (double)P.d;
   st = run_k(c, PC_DIST, 2, nd4, 3.0 * P.n * (double)P.n * P.d / 2, s, [&] {
     kern::dist_partial(th, P.ld, P.n, P.dist, c->dranges, c->dpart, s);
-    kern::dist_reduce(c->dpart, P.n, P.dist, c->D, s);
+    kern::dist_reduce(c->dpart, P.n, P.dist, c->slots, c->D, s);
     return PUSH_OK;
   });
   if (st != PUSH_OK) return st;
@@ -740,6 +915,27 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   c->h = F(P.o_h);
   c->dranges = reinterpret_cast<int64_t*>(c->ws + P.o_dranges);
   c->useg = reinterpret_cast<int4*>(c->ws + P.o_useg);
+  c->pth = F(P.o_pth);
+  c->pg = F(P.o_pg);
+  c->pth2 = F(P.o_pth2);
+  c->pack_th = F(P.o_pack_th);
+  c->pack_g = F(P.o_pack_g);
+  c->dist_own = P.dist;
+  c->slots.P = 1;
+  c->slots.smax = P.dist.splits;
+  c->slots.s0[0] = 0;
+  c->slots.s0[1] = P.dist.splits;
+  if (P.ds) {  // own splits, column ranges relative to the panel start
+    const int s0 = P.ds_s0[rank], s1 = P.ds_s0[rank + 1];
+    c->ds_c = P.ds_c0[rank];
+    c->ds_w = P.ds_c0[rank + 1] - P.ds_c0[rank];
+    c->dist_own.splits = s1 - s0;
+    c->dist_own.ranges.clear();
+    for (int k = 2 * s0; k < 2 * s1; ++k) c->dist_own.ranges.push_back(P.dist.ranges[k] - c->ds_c);
+    c->slots.P = world;
+    c->slots.smax = P.ds_smax;
+    for (int q = 0; q <= world; ++q) c->slots.s0[q] = P.ds_s0[q];
+  }
   c->xbuf = F(P.o_xbuf);
   c->ybuf = F(P.o_ybuf);
   c->pred = F(P.o_pred);
@@ -762,7 +958,9 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   PUSH_CUDA_TRY(cudaMemsetAsync(c->theta[0], 0, nld * 4, s));
   PUSH_CUDA_TRY(cudaMemsetAsync(c->theta[1], 0, nld * 4, s));
   PUSH_CUDA_TRY(cudaMemsetAsync(c->grad, 0, nld * 4, s));
-  PUSH_CUDA_TRY(cudaMemcpyAsync(c->dranges, P.dist.ranges.data(), P.dist.ranges.size() * 8, cudaMemcpyHostToDevice, s));
+  if (!c->dist_own.ranges.empty())
+    PUSH_CUDA_TRY(cudaMemcpyAsync(c->dranges, c->dist_own.ranges.data(), c->dist_own.ranges.size() * 8,
+                                  cudaMemcpyHostToDevice, s));
   if (!P.useg.empty())
     PUSH_CUDA_TRY(cudaMemcpyAsync(c->useg, P.useg.data(), P.useg.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
   if (theta0_host) {
@@ -918,6 +1116,24 @@ push_status push_svgd_step(push_ctx* c, void* stream) {
   push_status st = check_ctx(c);
   if (st != PUSH_OK) return st;
   if (c->state != 1) return fail(PUSH_E_STATE, "svgd_step needs fresh gradients (SPEC.md:350)");
+  if (c->P.ds && c->group) {  // loopback d-sharding: the last rank's call runs every member's phases
+    const auto& m = c->group->members;
+    if (c->rank + 1 < c->world) {
+      c->ds_deferred = true;
+    } else {
+      for (push_ctx* pc : m)
+        if (pc != c && (!pc->ds_deferred || pc->state != 1))
+          return fail(PUSH_E_STATE, "loopback d-sharded step: ranks 0..P-2 must call svgd_step first");
+      st = ds_group_step(m, static_cast<cudaStream_t>(stream));
+      if (st != PUSH_OK) return sticky(c, st);
+      for (push_ctx* pc : m) {
+        pc->ds_deferred = false;
+        pc->state = 0;
+        pc->has_step = true;
+      }
+    }
+    return PUSH_OK;
+  }
   st = do_step(c, static_cast<cudaStream_t>(stream));
   if (st != PUSH_OK) return sticky(c, st);
   c->state = 0;
@@ -1127,7 +1343,8 @@ push_status push_gather(push_ctx* c, int32_t what, float* out_host, void* stream
     case PUSH_WHAT_H:
     case PUSH_WHAT_KERNEL: {
       if (!c->has_step) return fail(PUSH_E_STATE, "no SVGD step yet");
-      const float* src = what == PUSH_WHAT_DIST ? c->D : (what == PUSH_WHAT_H ? c->h : c->K);
+      const float* src =
+          what == PUSH_WHAT_DIST ? c->D : (what == PUSH_WHAT_H ? c->h : c->K + (P.ds ? (int64_t)c->row0 * P.n : 0));
       const size_t T = P.tensors;
       const size_t cnt = what == PUSH_WHAT_DIST ? T * P.n * P.n : (what == PUSH_WHAT_H ? T : T * P.nl * P.n);
       cudaError_t e = cudaMemcpyAsync(out_host, src, cnt * 4, cudaMemcpyDeviceToHost, s);

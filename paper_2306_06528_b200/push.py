@@ -24,6 +24,7 @@ STATUS_NAMES = ["PUSH_OK", "PUSH_E_INVALID", "PUSH_E_SHAPE", "PUSH_E_STATE", "PU
 ACT = {"tanh": 0, "relu": 1, "identity": 2}
 VAR_PER_TENSOR, VAR_PAPER_NORM, VAR_PRIOR_SUM = 1, 2, 4  # push_config.variant bits (NEXT-2)
 VARIANT_PAPER = 7
+XCHG = {"allgather": 0, "dshard": 1}
 PRIOR = {"uniform": 0, "gaussian": 1}
 BW = {"median": 0, "median_ln_n": 0, "median_ln_n1": 1, "fixed": 2}
 WHAT = {"theta": 0, "grad": 1, "dist": 2, "h": 3, "loss": 4, "kernel": 5}
@@ -43,7 +44,8 @@ class PushConfig(Structure):
     _fields_ = [("n_particles", c_int32), ("n_layers", c_int32), ("dims", c_int32 * (MAX_LAYERS + 1)),
                 ("activation", c_int32), ("prior", c_int32), ("prior_sigma", c_float), ("lik_scale", c_float),
                 ("bw_rule", c_int32), ("bw_h", c_float), ("step_size", c_float), ("max_batch", c_int32),
-                ("seed", c_uint64), ("swag", c_int32), ("variant", c_int32)]
+                ("seed", c_uint64), ("swag", c_int32), ("variant", c_int32),
+                ("exchange", c_int32), ("reserved", c_int32)]
 
 
 class ProfileRow(Structure):
@@ -110,9 +112,10 @@ def check(status: int):
 
 def make_config(n_particles: int, dims, activation="tanh", prior="uniform", prior_sigma=1.0, lik_scale=1.0,
                 bw_rule="median", bw_h=1.0, step_size=1e-3, max_batch=1, seed=0, swag=False,
-                variant=0) -> PushConfig:
+                variant=0, exchange="allgather") -> PushConfig:
     """variant: 0 (canonical SVGD) or an OR of VAR_PER_TENSOR / VAR_PAPER_NORM / VAR_PRIOR_SUM
-    (VARIANT_PAPER = all three, include/push.h)."""
+    (VARIANT_PAPER = all three, include/push.h).
+    exchange: "allgather" (default) or "dshard" (d-sharded kernel phase, NEXT-4)."""
     c = PushConfig()
     c.n_particles = n_particles
     c.n_layers = len(dims) - 1
@@ -129,6 +132,8 @@ def make_config(n_particles: int, dims, activation="tanh", prior="uniform", prio
     c.seed = seed
     c.swag = 1 if swag else 0
     c.variant = int(variant)
+    c.exchange = XCHG[exchange] if isinstance(exchange, str) else int(exchange)
+    c.reserved = 0
     return c
 
 

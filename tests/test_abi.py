@@ -37,10 +37,11 @@ def test_every_declared_symbol_is_exported(L):
 
 
 def test_config_struct_layout_matches_header():
-    assert ctypes.sizeof(push.PushConfig) == 120
+    assert ctypes.sizeof(push.PushConfig) == 128
     assert push.PushConfig.seed.offset == 104
     assert push.PushConfig.swag.offset == 112
     assert push.PushConfig.variant.offset == 116
+    assert push.PushConfig.exchange.offset == 120
     assert ctypes.sizeof(push.ProfileRow) == 56
 
 
@@ -91,3 +92,21 @@ def test_variant_field_validated_on_host():
         with pytest.raises(push.PushError) as e:
             push.workspace_size(push.make_config(8, [2, 64, 64, 1], max_batch=64, variant=bad))
         assert e.value.status == push.PUSH_E_INVALID
+
+
+def test_exchange_field_validated_on_host():
+    """push_config.exchange: ALLGATHER (0) or DSHARD (1, NEXT-4, variant 0 only); DSHARD's per-rank
+    workspace (column panels n x ld/P) shrinks with the rank count."""
+    mk = lambda **kw: push.make_config(64, [3, 512, 512, 1], max_batch=256, **kw)  # noqa: E731
+    ag = [push.workspace_size(mk(), P) for P in (1, 2, 4, 8)]
+    ds = [push.workspace_size(mk(exchange="dshard"), P) for P in (1, 2, 4, 8)]
+    assert all(b > a for a, b in zip(ds[1:], ds[:-1]))  # strictly shrinking with P
+    assert ds[-1] < ag[-1] * 1.5
+    for bad in (dict(exchange=2), dict(exchange="dshard", variant=push.VARIANT_PAPER)):
+        with pytest.raises(push.PushError) as e:
+            push.workspace_size(mk(**bad), 2)
+        assert e.value.status == push.PUSH_E_INVALID
+    c = mk()
+    c.reserved = 1
+    with pytest.raises(push.PushError):
+        push.workspace_size(c, 1)
