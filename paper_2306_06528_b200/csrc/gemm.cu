@@ -77,6 +77,7 @@ struct KParams {
   int a_pz, b_pz;  // 1: operand batched over particles; 0: shared (particle coordinate 0)
   int store;       // 0: BWD output only feeds the fused partials (delta of a thin first layer): no store
   int chunk_kb;    // k-blocks per TMEM accumulation chunk before the fp32 promotion (pair kernel)
+  float alpha;     // EPI_STORE: C = alpha * acc (1 for split-K partials; -lambda when dW goes straight into G)
   int dbg;         // debug experiments only (pushdbg_gemm): bit 0 raw fp32 operands (no hi/lo split),
                    // bit 1 skip the epilogue math/stores, bit 2 skip the MMAs (commits only),
                    // bit 3 accumulate the whole K in TMEM (no fp32 promotion)
@@ -206,11 +207,12 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
               ptx::sts_f4(pp, v);
             }
           } else {
+            const float al = prm.alpha;
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4)
               ptx::sts_f4(buf + roff + ((c4 ^ swz) << 4),
-                          make_float4(acc[g * 16 + 4 * c4], acc[g * 16 + 4 * c4 + 1], acc[g * 16 + 4 * c4 + 2],
-                                      acc[g * 16 + 4 * c4 + 3]));
+                          make_float4(al * acc[g * 16 + 4 * c4], al * acc[g * 16 + 4 * c4 + 1],
+                                      al * acc[g * 16 + 4 * c4 + 2], al * acc[g * 16 + 4 * c4 + 3]));
           }
           __syncwarp();
           if (bwd && prm.bpart) {  // (bwd is constexpr)
@@ -1044,6 +1046,7 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   kp.a_pz = pb.A.pstride == 0 ? 0 : 1;
   kp.b_pz = pb.B.pstride == 0 ? 0 : 1;
   kp.bias = pb.bias; kp.bias_pstride = pb.bias_pstride;
+  kp.alpha = pb.alpha;
   kp.bpart = pb.bpart; kp.bp_sstride = pb.bp_sstride; kp.bp_pstride = pb.bp_pstride;
   kp.x = pb.x; kp.din = pb.xpart ? pb.din : 0; kp.xpart = pb.xpart;
   kp.xp_sstride = pb.xp_sstride; kp.xp_pstride = pb.xp_pstride;

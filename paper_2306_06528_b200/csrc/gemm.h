@@ -10,7 +10,7 @@ namespace push {
 namespace gemm {
 
 enum Epi : int {
-  EPI_STORE = 0,  // C[s][p][m][n] = acc                                  (a5 weight-grad split-K partials; debug)
+  EPI_STORE = 0,  // C[s][p][m][n] = alpha*acc                                (a5 weight-grad split-K partials; debug)
   EPI_FWD = 1,    // A_l[p][m][n] = sigma(acc + b_l[n])                     (a2 hidden forward)
   EPI_BWD = 2     // delta[p][m][n] = acc * sigma'(aprev[p][m][n])          (a4 backprop)
                   //   + column partial sums of delta per 32-row block    (a5 bias grads of the next layer down)
@@ -41,6 +41,7 @@ struct Problem {
   float* out = nullptr;     // [s][p][m][n]: element at s*out_sstride + p*out_pstride + m*ldo + n
                             // (BWD only: nullptr = compute the fused partials, store nothing)
   int64_t ldo = 0, out_pstride = 0, out_sstride = 0;  // out_sstride must equal batch*out_pstride when splits > 1
+  float alpha = 1.f;            // EPI_STORE: out = alpha * acc
   const float* bias = nullptr;  // FWD: bias of particle p at bias + p*bias_pstride
   int64_t bias_pstride = 0;
   const float* aprev = nullptr;  // BWD: activation a_{l-1} [p][m][n] (ld_aprev, aprev_pstride)

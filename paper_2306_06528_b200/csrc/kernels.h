@@ -78,11 +78,15 @@ struct FinalizeJob {
   int64_t off_w;
   int in, out;
   int nb_w, nb_b;        // blocks for the weight / bias parts
-  int w_warp, b_warp;    // 0 thread per element, 1 warp per element, 2 thread per 4 elements (weights)
+  int w_warp, b_warp;    // 0 thread per element, 1 warp per element, 2 thread per 4 elements (weights),
+                         // 3 weights already in G (-lambda dW stored by the GEMM): add the prior in place
   int blk0;              // first block of this job (set by finalize_all)
 };
 constexpr int kMaxFinalizeJobs = 16;
 FinalizeJob make_finalize_job(const PartView& W, const PartView& Bv, int64_t off_w, int in, int out);
+// Same, for a layer whose weight gradient the GEMM already wrote into G as -lambda dW (split-K 1):
+// only the bias partials are reduced, plus the Gaussian prior added to the weights in place.
+FinalizeJob make_finalize_job_wdirect(const PartView& Bv, int64_t off_w, int in, int out, int prior);
 void finalize_all(const FinalizeJob* jobs, int njobs, const float* theta, float* grad, int64_t ld, float lambda,
                   int prior, float inv_sigma2, int batch, cudaStream_t s);
 

@@ -442,6 +442,11 @@ __device__ __forceinline__ void finalize_range(const PartView& W, const PartView
   }
   const int64_t t = mode == 1 ? t0 + (blk * blockDim.x + threadIdx.x) / 32 : t0 + blk * blockDim.x + threadIdx.x;
   if (t >= t1) return;
+  if (mode == 3) {  // G already holds -lambda dW: add grad log p0 (Gaussian prior only; uniform launches none)
+    const int64_t idx = p * ld + off_w + t;
+    grad[idx] += -theta[idx] * inv_sigma2;
+    return;
+  }
   int splits;
   int64_t ss;
   const float* src = part_ptr(W, Bv, p, t, nin, nw, &splits, &ss);
@@ -499,6 +504,12 @@ FinalizeJob make_finalize_job(const PartView& W, const PartView& Bv, int64_t off
   };
   j.nb_w = blocks(nw, j.w_warp);
   j.nb_b = blocks(out, j.b_warp);
+  return j;
+}
+FinalizeJob make_finalize_job_wdirect(const PartView& Bv, int64_t off_w, int in, int out, int prior) {
+  FinalizeJob j = make_finalize_job(PartView{nullptr, 0, 0, 0, 0}, Bv, off_w, in, out);
+  j.w_warp = 3;
+  j.nb_w = prior == PUSH_PRIOR_GAUSSIAN ? (int)(((int64_t)in * out + 255) / 256) : 0;
   return j;
 }
 void finalize_all(const FinalizeJob* jobs, int njobs, const float* theta, float* grad, int64_t ld, float lambda,

@@ -119,6 +119,11 @@ static int wgrad_splits(int B, int out, int in) {
   return gemm::effective_splits(B, want);
 }
 
+// A weight-gradient GEMM with one split writes -lambda dW straight into G (TMA-legal when the layer's
+// weights start on a 16-B boundary and rows are whole 16-B units); wgrad_splits is monotone in B, so
+// one split at max_batch means one split for every batch and the layer needs no partial buffer.
+static bool wgrad_in_g(int off_w_mod4, int in, int S) { return S == 1 && off_w_mod4 == 0 && in % 4 == 0; }
+
 static push_status make_plan(const push_config* c, int world, Plan* p) {
   push_status st = validate(c, world);
   if (st != PUSH_OK) return st;
@@ -214,12 +219,14 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.o_err2 = take((int64_t)P.nl * P.Bmax);
   P.o_loss = take(P.nl);
   P.o_loss_all = take(P.n);
-  P.o_wpart.assign(P.L, 0);
+  P.o_wpart.assign(P.L, SIZE_MAX);  // SIZE_MAX: no partial buffer (thin layer or dW straight into G)
   P.o_tpart.assign(P.L, 0);
   P.o_bpart.assign(P.L, 0);
   for (int l = 0; l < P.L; ++l) {
     const LayerPlan& lp = P.layers[l];
-    if (lp.gemm) P.o_wpart[l] = take((int64_t)wgrad_splits(P.Bmax, lp.out, lp.in) * P.nl * lp.in * lp.out);
+    const int smax = wgrad_splits(P.Bmax, lp.out, lp.in);
+    if (lp.gemm && !wgrad_in_g((int)(lp.off_w % 4), lp.in, smax))
+      P.o_wpart[l] = take((int64_t)smax * P.nl * lp.in * lp.out);
     // thin weight partials (thin hidden layers) or bias-only column sums (GEMM layers under a thin one)
     if (l < P.L - 1) P.o_tpart[l] = take((int64_t)chunks_max * P.nl * lp.out * (lp.gemm ? 1 : lp.in + 1));
     if (l < P.L - 1) P.o_bpart[l] = take((int64_t)P.RB * P.nl * lp.out);
@@ -445,9 +452,12 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
   push_status st;
   // a5 epilogue: every layer's partials are reduced into G by ONE launch after the backward pass
   std::vector<kern::FinalizeJob> jobs;
-  auto finalize = [&](int l, const kern::PartView& W, const kern::PartView& Bv) {
+  // PUSH_VAR_PRIOR_SUM: G keeps the likelihood term only; a10 adds the unweighted prior sum
+  const int prior_g = (c->cfg.variant & PUSH_VAR_PRIOR_SUM) ? PUSH_PRIOR_UNIFORM : c->cfg.prior;
+  auto finalize = [&](int l, const kern::PartView& W, const kern::PartView& Bv, bool w_in_g = false) {
     const LayerPlan& lp = P.layers[l];
-    jobs.push_back(kern::make_finalize_job(W, Bv, lp.off_w, lp.in, lp.out));
+    jobs.push_back(w_in_g ? kern::make_finalize_job_wdirect(Bv, lp.off_w, lp.in, lp.out, prior_g)
+                          : kern::make_finalize_job(W, Bv, lp.off_w, lp.in, lp.out));
     return PUSH_OK;
   };
 
@@ -547,8 +557,14 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
       pb.A = gemm::Operand{dl, nullptr, true, true, lp.out, P.dlt_pst};
       pb.B = gemm::Operand{ap.p, nullptr, true, true, lp.in, ap.pst};
       pb.epi = gemm::EPI_STORE;
-      pb.out = c->wpart[l]; pb.ldo = lp.in; pb.out_pstride = (int64_t)lp.out * lp.in;
-      pb.out_sstride = (int64_t)nl * lp.out * lp.in;
+      // one split: the epilogue writes -lambda dW straight into G's rows (no partial round trip)
+      const bool w_in_g = wgrad_in_g((int)(lp.off_w % 4), lp.in, S);
+      if (w_in_g) {
+        pb.out = g + lp.off_w; pb.ldo = lp.in; pb.out_pstride = ld; pb.alpha = -lambda;
+      } else {
+        pb.out = c->wpart[l]; pb.ldo = lp.in; pb.out_pstride = (int64_t)lp.out * lp.in;
+        pb.out_sstride = (int64_t)nl * lp.out * lp.in;
+      }
       const double fl = 2.0 * B * lp.out * (double)lp.in * nl;
       st = run_k(c, PC_WGRAD_GEMM, 1, 0, fl, s, [&] { return gemm::run(pb, s); });
       if (st != PUSH_OK) return st;
@@ -563,7 +579,7 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
         if (st != PUSH_OK) return st;
         Bv = kern::PartView{c->tpart[l], chunks, (int64_t)nl * lp.out, lp.out, 1};
       }
-      if ((st = finalize(l, W, Bv)) != PUSH_OK) return st;
+      if ((st = finalize(l, W, Bv, w_in_g)) != PUSH_OK) return st;
     } else if (l == 0 && x0_ready) {
       kern::PartView W{c->xpart, RB, (int64_t)nl * lp.out * lp.in, (int64_t)lp.out * lp.in, lp.in};
       kern::PartView Bv{c->bpart[0], RB, (int64_t)nl * lp.out, lp.out, 1};
@@ -616,9 +632,7 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
     xb ^= 1;
   }
   return run_k(c, PC_FINALIZE, 1, 0, 0, s, [&] {
-    // PUSH_VAR_PRIOR_SUM: G keeps the likelihood term only; a10 adds the unweighted prior sum
-    const int prior = (c->cfg.variant & PUSH_VAR_PRIOR_SUM) ? PUSH_PRIOR_UNIFORM : c->cfg.prior;
-    kern::finalize_all(jobs.data(), (int)jobs.size(), th, g, ld, lambda, prior, inv_s2, nl, s);
+    kern::finalize_all(jobs.data(), (int)jobs.size(), th, g, ld, lambda, prior_g, inv_s2, nl, s);
     return PUSH_OK;
   });
 }
@@ -898,7 +912,7 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   c->dlt[0] = F(P.o_dlt0);
   c->dlt[1] = F(P.o_dlt1);
   for (int l = 0; l < P.L; ++l) {
-    c->wpart.push_back(F(P.o_wpart[l]));
+    c->wpart.push_back(P.o_wpart[l] == SIZE_MAX ? nullptr : F(P.o_wpart[l]));
     c->tpart.push_back(F(P.o_tpart[l]));
     c->bpart.push_back(F(P.o_bpart[l]));
   }
