@@ -159,10 +159,24 @@ __device__ __forceinline__ TileCoord decode(int t, const KParams& prm) {
 // Fused epilogue of one 32-row x CW-column slab held in registers (acc), written through the
 // warp's double-buffered swizzled 32x16 smem half-boxes with TMA stores (see the v3 notes above).
 // aux_ph: parity of the warp's aprev barrier (BWD); the aprev box of group 0 must already be in flight.
+// FWD: lane l's slice b_l[colw + 4 l .. 4 l + 3] of the warp's CW bias columns (b_l need not be 16-B aligned)
+template <int CW, int EPI>
+__device__ __forceinline__ float4 load_bias4(const KParams& prm, int lane, int colw, int p) {
+  static_assert(CW <= 128, "one float4 of bias per lane");
+  float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+  if constexpr (EPI == EPI_FWD) {
+    if (4 * lane < CW) {
+      const float* bias = prm.bias + p * prm.bias_pstride + colw + 4 * lane;
+      b = make_float4(__ldg(bias), __ldg(bias + 1), __ldg(bias + 2), __ldg(bias + 3));
+    }
+  }
+  return b;
+}
 template <int CW, int EPI>
 __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& prm, const CUtensorMap* tOut,
                                          const CUtensorMap* tAux, uint64_t* auxbar, uint32_t& aux_ph,
-                                         uint32_t ebuf_s, int lane, int row0, int colw, int p, int pz) {
+                                         uint32_t ebuf_s, int lane, int row0, int colw, int p, int pz,
+                                         float4 bias4) {
   constexpr bool bwd = EPI == EPI_BWD;
         // Output in 16-column groups g, double-buffered: group g is staged in half-box (g & 1)
         // (32 rows x 16 fp32, SWIZZLE_64B: 16-B chunk c of row r sits at chunk c ^ ((r >> 1) & 3)),
@@ -182,11 +196,13 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
             __syncwarp();
           }
           if constexpr (EPI == EPI_FWD) {
-            const float* bias = prm.bias + p * prm.bias_pstride + col;  // b_l need not be 16-B aligned
+            // b_l[colw + 4 l .. 4 l + 3] sits in lane l (loaded before the accumulator drain): broadcast
+            // shuffles instead of 16 dependent global loads per group
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) {
-              const float4 bv = make_float4(__ldg(bias + 4 * c4), __ldg(bias + 4 * c4 + 1), __ldg(bias + 4 * c4 + 2),
-                                            __ldg(bias + 4 * c4 + 3));
+              const int src = g * 4 + c4;
+              const float4 bv = make_float4(__shfl_sync(0xffffffffu, bias4.x, src), __shfl_sync(0xffffffffu, bias4.y, src),
+                                            __shfl_sync(0xffffffffu, bias4.z, src), __shfl_sync(0xffffffffu, bias4.w, src));
               float4 v;
               v.x = act_fwd(acc[g * 16 + 4 * c4 + 0] + bv.x, prm.act);
               v.y = act_fwd(acc[g * 16 + 4 * c4 + 1] + bv.y, prm.act);
@@ -470,6 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_arrive_expect_tx(&auxbar[e], kHalfBox);
           ptx::tma_load_3d(ebuf, &tAux, &auxbar[e], colw, row0, tc.p);
         }
+        const float4 bias4 = load_bias4<C::CW, EPI>(prm, lane, colw, tc.p);
         float acc[C::CW];
 #pragma unroll
         for (int j = 0; j < C::CW; ++j) acc[j] = 0.f;
@@ -497,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!live || (prm.dbg & 2)) continue;
         const int pz = EPI == EPI_STORE ? tc.split * prm.batch + tc.p : tc.p;
-        epi_tile<C::CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, tc.p, pz);
+        epi_tile<C::CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, tc.p, pz, bias4);
       }
       if (lane == 0) ptx::bulk_wait0();
     }
@@ -765,6 +782,7 @@ __global__ void __launch_bounds__(k2Threads, 1)
         ptx::mbar_arrive_expect_tx(&auxbar[e], kHalfBox);
         ptx::tma_load_3d(ptx_ptr(ebuf_s), &tAux, &auxbar[e], colw, row0, p);
       }
+      const float4 bias4 = load_bias4<k2CW, EPI>(prm, lane, colw, p);
       float acc[k2CW];
 #pragma unroll
       for (int j = 0; j < k2CW; ++j) acc[j] = 0.f;
@@ -791,7 +809,7 @@ __global__ void __launch_bounds__(k2Threads, 1)
       }
       if (!live || (prm.dbg & 2)) continue;
       const int pz = EPI == EPI_STORE ? split * prm.batch + p : p;
-      epi_tile<k2CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, p, pz);
+      epi_tile<k2CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, p, pz, bias4);
     }
     if (lane == 0) ptx::bulk_wait0();
   }

@@ -78,7 +78,7 @@ struct FinalizeJob {
   int64_t off_w;
   int in, out;
   int nb_w, nb_b;        // blocks for the weight / bias parts
-  int w_warp, b_warp;    // 0 thread per element, 1 warp per element, 2 thread per 4 elements (weights),
+  int w_warp, b_warp;    // 0 thread per element, 1 column group (many partials), 2 thread per 4 elements,
                          // 3 weights already in G (-lambda dW stored by the GEMM): add the prior in place
   int blk0;              // first block of this job (set by finalize_all)
 };

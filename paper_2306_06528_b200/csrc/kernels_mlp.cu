@@ -48,6 +48,12 @@ __global__ void __launch_bounds__(256) thin_forward_narrow_kernel(const float* _
   const float* W = theta + p * ld + off_w;
   const float* bias = theta + p * ld + off_b;
   float* o_ = out + p * out_pstride;
+  __shared__ float sx[32][NI];  // the block's x rows, loaded once (broadcast reads below)
+  for (int c = threadIdx.x; c < 32 * NI; c += blockDim.x) {
+    const int r = c / NI, i = c - r * NI;
+    sx[r][i] = (b0 + r < b1 && i < nin) ? __ldg(x + (int64_t)(b0 + r) * nin + i) : 0.f;
+  }
+  __syncthreads();
   for (int o = threadIdx.x * VEC; o < nout; o += blockDim.x * VEC) {
     float w[VEC][NI], bo[VEC];
 #pragma unroll
@@ -56,10 +62,11 @@ __global__ void __launch_bounds__(256) thin_forward_narrow_kernel(const float* _
       for (int i = 0; i < NI; ++i) w[v][i] = (NIN > 0 || i < nin) ? __ldg(W + (int64_t)(o + v) * nin + i) : 0.f;
       bo[v] = __ldg(bias + o + v);
     }
+#pragma unroll 4
     for (int b = b0; b < b1; ++b) {
       float xv[NI];
 #pragma unroll
-      for (int i = 0; i < NI; ++i) xv[i] = (NIN > 0 || i < nin) ? __ldg(x + (int64_t)b * nin + i) : 0.f;
+      for (int i = 0; i < NI; ++i) xv[i] = sx[b - b0][i];
       float z[VEC];
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
@@ -144,6 +151,8 @@ __global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
   const int rb = blockIdx.x;
   const int rows = min(32, a.B - rb * 32);
   const float* __restrict__ Ag = a.A + p * a.a_pstride + (int64_t)rb * 32 * a.H;
+  for (int c = threadIdx.x; c < 32 * DOUT; c += 256) (&sdl[0][0])[c] = 0.f;  // o >= dout stays 0 (times w = 0)
+  if constexpr (!SMEM) __syncthreads();
   if constexpr (SMEM) {
     const int n4 = rows * a.H / 4;
     const float4* src = reinterpret_cast<const float4*>(Ag);
@@ -229,8 +238,195 @@ __global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
     if (dprev) a.bpart_prev[(int64_t)rb * a.bp_sstride + p * a.bp_pstride + i] = bacc;
   }
 }
+// Streaming form of the same block computation (same per-element arithmetic and order, so the same
+// bits): the 32-row block is consumed in slabs of R rows staged by cp.async into an NST-deep ring,
+// the copy of slab k + NST - 1 overlapping phases 1-2 of slab k, and W_L is staged once.  Thread t
+// owns features i = t + 256 m (m < FPT) across all slabs, so the dW / bias partials stay in
+// registers.  Keeps up to NST * R * H * 4 bytes of A in flight per CTA instead of loading the whole
+// slab before any math (the one-shot kernel above stalled on long-scoreboard with one CTA per SM).
+constexpr int kOutStreamSlabBytes = 32 * 1024;
+// Phase 2 of one feature column over nr slab rows: ACT < 0 = no delta below (L = 1); 32-bit offsets.
+template <int DOUT, int ACT>
+__device__ __forceinline__ void out_phase2(const float* ai, int H, int nr, const float (*sd)[DOUT], const float (&wv)[DOUT],
+                                           float (&wacc)[DOUT], float& bacc, float* dpb) {
+  int off = 0;
+#pragma unroll 4
+  for (int r = 0; r < nr; ++r, off += H) {
+    const float av = ai[off];
+    float d = 0.f;
+#pragma unroll
+    for (int o = 0; o < DOUT; ++o) {
+      const float dl = sd[r][o];
+      wacc[o] = fmaf(dl, av, wacc[o]);
+      d = fmaf(dl, wv[o], d);
+    }
+    if constexpr (ACT >= 0) {
+      d *= act_deriv_from_a(av, ACT);
+      dpb[off] = d;
+      bacc += d;
+    }
+  }
+}
+template <int DOUT, int FPT>
+__global__ void __launch_bounds__(256) output_stream_kernel(const OutputArgs a, int R, int NST) {
+  __shared__ float sdl[32][DOUT];
+  __shared__ float serr[32][DOUT];
+  extern __shared__ __align__(16) float sm[];  // [DOUT][H] W_L, then NST slabs of [R][H]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int p = blockIdx.y, rb = blockIdx.x, H = a.H;
+  const int rows = min(32, a.B - rb * 32);
+  const int nslab = (rows + R - 1) / R;
+  float* sW = sm;
+  float* sA = sm + DOUT * H;
+  const float* __restrict__ Ag = a.A + p * a.a_pstride + (int64_t)rb * 32 * H;
+  const float* __restrict__ Wg = a.theta + p * a.ld + a.off_w;
+  const float* __restrict__ bias = a.theta + p * a.ld + a.off_b;
+  const uint32_t sA_u = static_cast<uint32_t>(__cvta_generic_to_shared(sA));
+  auto issue = [&](int k) {  // slab k -> ring slot k % NST (rows past `rows` are not loaded)
+    if (k < nslab) {
+      const int r0 = k * R, nr = min(R, rows - r0);
+      const int n4 = nr * H / 4;
+      const float4* src = reinterpret_cast<const float4*>(Ag + (int64_t)r0 * H);
+      const uint32_t dst = sA_u + (uint32_t)((k % NST) * R * H) * 4u;
+      for (int c = tid; c < n4; c += 256)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * c), "l"(src + c) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int k = 0; k < NST - 1; ++k) issue(k);
+  for (int c = tid; c < a.dout * H; c += 256) sW[c] = __ldg(Wg + c);
+  for (int c = tid; c < 32 * DOUT; c += 256) (&sdl[0][0])[c] = 0.f;  // o >= dout stays 0 (times w = 0)
+  const float scale = 2.0f / (float)((int64_t)a.B * a.dout);
+  float wacc[FPT][DOUT], bacc[FPT], wv[FPT][DOUT];
+  float* __restrict__ dprev = a.dprev ? a.dprev + p * a.dp_pstride + (int64_t)rb * 32 * H : nullptr;
+#pragma unroll
+  for (int m = 0; m < FPT; ++m) {
+    bacc[m] = 0.f;
+#pragma unroll
+    for (int o = 0; o < DOUT; ++o) wacc[m][o] = 0.f;
+  }
+  // phase-1 rows of this warp within a slab: RPW consecutive rows (R >= 8), or one row (R = 4)
+  const int RPW = R >= 8 ? R / 8 : 1;
+  for (int k = 0; k < nslab; ++k) {
+    issue(k + NST - 1);  // one group per iteration (possibly empty): slab k has NST - 1 newer groups
+    if (NST == 3) asm volatile("cp.async.wait_group 2;" ::: "memory");
+    else if (NST == 2) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    if (k == 0) {
+#pragma unroll
+      for (int m = 0; m < FPT; ++m) {
+        const int i = tid + 256 * m;
+#pragma unroll
+        for (int o = 0; o < DOUT; ++o) wv[m][o] = (i < H && o < a.dout) ? sW[o * H + i] : 0.f;
+      }
+    }
+    const float* A = sA + (k % NST) * R * H;  // row r of the block at A[(r - k R) H]
+    const int r_base = k * R;
+    // phase 1: yhat, residual, dL for the slab's rows (per row: lane-strided sum, fixed xor tree)
+    if (warp * RPW < R) {
+      const int lr0 = warp * RPW;
+      bool ok[4];
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) ok[rr] = rr < RPW && r_base + lr0 + rr < rows;
+      const float* a0 = A + lr0 * H;
+      for (int o = 0; o < a.dout; ++o) {
+        const float* wrow = sW + o * H;
+        float part[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
+        for (int i = lane; i < H; i += 32) {
+          const float w = wrow[i];
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr)
+            if (ok[rr]) part[rr] = fmaf(a0[rr * H + i], w, part[rr]);
+        }
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          if (rr >= RPW) break;
+#pragma unroll
+          for (int m = 16; m >= 1; m >>= 1) part[rr] += __shfl_xor_sync(0xffffffffu, part[rr], m);
+          const int r = r_base + lr0 + rr, b = rb * 32 + r;
+          float dl = 0.f;
+          if (r < rows) {
+            const float e = (part[rr] + __ldg(bias + o)) - __ldg(a.y + (int64_t)b * a.dout + o);
+            dl = scale * e;
+            if (lane == 0) serr[r][o] = e;
+          }
+          if (lane == 0 && r < 32) sdl[r][o] = dl;
+        }
+      }
+    }
+    __syncthreads();
+    // phase 2 over the slab's rows, ascending (activation and delta store resolved at compile time)
+    const int nr = min(r_base + R, rows) - r_base;
+    const int mode = dprev ? 1 + a.act : 0;
+#pragma unroll
+    for (int m = 0; m < FPT; ++m) {
+      const int i = tid + 256 * m;
+      if (i < H) {
+        float* dpb = dprev ? dprev + (int64_t)r_base * H + i : nullptr;
+        const float(*sd)[DOUT] = sdl + r_base;
+        switch (mode) {
+          case 0: out_phase2<DOUT, -1>(A + i, H, nr, sd, wv[m], wacc[m], bacc[m], dpb); break;
+          case 1 + PUSH_ACT_TANH: out_phase2<DOUT, PUSH_ACT_TANH>(A + i, H, nr, sd, wv[m], wacc[m], bacc[m], dpb); break;
+          case 1 + PUSH_ACT_RELU: out_phase2<DOUT, PUSH_ACT_RELU>(A + i, H, nr, sd, wv[m], wacc[m], bacc[m], dpb); break;
+          default: out_phase2<DOUT, PUSH_ACT_IDENTITY>(A + i, H, nr, sd, wv[m], wacc[m], bacc[m], dpb); break;
+        }
+      }
+    }
+    __syncthreads();  // slot k % NST is refilled by the next iteration's issue
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  // rows past `rows` contribute dL = 0 to the output-bias partial (as in the one-shot kernel)
+  for (int r = rows + tid; r < 32; r += 256)
+    for (int o = 0; o < a.dout; ++o) sdl[r][o] = 0.f;
+  if (lane < 4 && warp * 4 + lane < rows) {
+    const int r = warp * 4 + lane;
+    float e2 = 0.f;
+    for (int o = 0; o < a.dout; ++o) e2 = fmaf(serr[r][o], serr[r][o], e2);
+    a.err2[p * a.err_pstride + rb * 32 + r] = e2;
+  }
+  __syncthreads();
+  if (tid < a.dout) {
+    float sb = 0.f;
+    for (int r = 0; r < 32; ++r) sb += sdl[r][tid];
+    a.bpart_out[(int64_t)rb * a.bo_sstride + p * a.bo_pstride + tid] = sb;
+  }
+#pragma unroll
+  for (int m = 0; m < FPT; ++m) {
+    const int i = tid + 256 * m;
+    if (i < H) {
+      for (int o = 0; o < a.dout; ++o)
+        a.wpart[(int64_t)rb * a.wo_sstride + p * a.wo_pstride + (int64_t)o * H + i] = wacc[m][o];
+      if (dprev) a.bpart_prev[(int64_t)rb * a.bp_sstride + p * a.bp_pstride + i] = bacc[m];
+    }
+  }
+}
+template <int DOUT, int FPT>
+static void output_stream_launch(const OutputArgs& a, int batch, cudaStream_t s) {
+  int R = 32;
+  while (R > 4 && (int64_t)R * a.H * 4 > kOutStreamSlabBytes) R >>= 1;
+  const int nslab = (std::min(32, a.B) + R - 1) / R;
+  const int NST = nslab >= 3 ? 3 : (nslab == 2 ? 2 : 1);
+  const size_t smem = sizeof(float) * ((size_t)DOUT * a.H + (size_t)NST * R * a.H);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(output_stream_kernel<DOUT, FPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  output_stream_kernel<DOUT, FPT><<<dim3((a.B + 31) / 32, batch), 256, smem, s>>>(a, R, NST);
+}
 template <int DOUT>
 static void output_launch(const OutputArgs& a, int batch, cudaStream_t s) {
+  const bool stream_ok = a.H % 4 == 0 && a.a_pstride % 4 == 0 && (reinterpret_cast<uintptr_t>(a.A) & 15) == 0 &&
+                         a.H <= 2048 && DOUT * ((a.H + 255) / 256) <= 16;
+  if (stream_ok) {
+    const int fpt = (a.H + 255) / 256;
+    if (fpt == 1) return output_stream_launch<DOUT, 1>(a, batch, s);
+    if (fpt == 2) return output_stream_launch<DOUT, 2>(a, batch, s);
+    if (fpt <= 4) return output_stream_launch<DOUT, 4>(a, batch, s);
+    if constexpr (DOUT <= 2) return output_stream_launch<DOUT, 8>(a, batch, s);
+  }
   const dim3 grid((a.B + 31) / 32, batch);
   const bool smem = a.H <= kOutSmemH && a.H % 4 == 0 && a.a_pstride % 4 == 0 &&
                     (reinterpret_cast<uintptr_t>(a.A) & 15) == 0;
@@ -368,9 +564,10 @@ int thin_wgrad(const float* dl, int64_t d_pstride, const float* A, int64_t a_pst
 // ---------------------------------------------------------------- finalize G rows of one layer
 // G_p[off_w + t] = -lambda * sum_s part(s, p, t) + grad log p0(theta_p[off_w + t]) for t in [t0, t1)
 // (t < in*out: weight (o, i) = (t / in, t % in) from W; else bias o = t - in*out from Bv).
-// Few partials (<= kThreadSplits): one thread per element, ascending s.  Many partials: one warp
-// per element, lane l sums s = l, l+32, ... ascending, then a fixed xor tree.  Either order
-// depends only on the partial count, never on the sharding.
+// Few partials (<= kThreadSplits): one thread per element, ascending s.  Many partials over few
+// elements: a CTA per 32 consecutive elements, warp w sums s = w, w+8, ... ascending (coalesced
+// loads, 8 in flight), then the 8 warp sums in ascending w.  Either order depends only on the
+// partial count, never on the sharding.
 constexpr int kThreadSplits = 16;
 __device__ __forceinline__ const float* part_ptr(const PartView& W, const PartView& Bv, int p, int64_t t, int nin,
                                                  int64_t nw, int* splits, int64_t* sstride) {
@@ -401,9 +598,14 @@ template <typename V>
 __device__ __forceinline__ V sum_partials(const V* src, int splits, int64_t ss_v) {
   V zero;
   memset(&zero, 0, sizeof(V));
-  if (splits <= 8) {
+  if (splits <= 8) {  // all loads issued before the (ascending) adds
+    V t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = u < splits ? __ldg(src + u * ss_v) : zero;
     V v = zero;
-    for (int s = 0; s < splits; ++s) v = vadd(v, __ldg(src + s * ss_v));
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < splits) v = vadd(v, t[u]);
     return v;
   }
   V a[8];
@@ -416,7 +618,8 @@ __device__ __forceinline__ V sum_partials(const V* src, int splits, int64_t ss_v
   for (int u = 0; s + u < splits; ++u) a[u] = vadd(a[u], __ldg(src + (s + u) * ss_v));
   return vadd(vadd(vadd(a[0], a[1]), vadd(a[2], a[3])), vadd(vadd(a[4], a[5]), vadd(a[6], a[7])));
 }
-// mode 0: thread per element, 1: warp per element, 2: thread per 4 consecutive elements (float4)
+// mode 0: thread per element, 1: 32 consecutive elements per CTA with the partials split over its 8 warps
+// (many partials), 2: thread per 4 consecutive elements (float4), 3: prior added in place
 __device__ __forceinline__ void finalize_range(const PartView& W, const PartView& Bv, const float* theta,
                                                float* grad, int64_t ld, int64_t off_w, int nin, int nout,
                                                int64_t t0, int64_t t1, int mode, int64_t blk, float lambda,
@@ -440,7 +643,35 @@ __device__ __forceinline__ void finalize_range(const PartView& W, const PartView
                                                          fmaf(-lambda, v.z, pr.z), fmaf(-lambda, v.w, pr.w));
     return;
   }
-  const int64_t t = mode == 1 ? t0 + (blk * blockDim.x + threadIdx.x) / 32 : t0 + blk * blockDim.x + threadIdx.x;
+  if (mode == 1) {  // column group: 32 consecutive elements per CTA, warp w sums s = w, w + 8, ... ascending
+    __shared__ float red[8][33];
+    const int warp = threadIdx.x >> 5;  // blockDim.x == 256
+    const int64_t t = t0 + blk * 32 + lane;
+    float v = 0.f;
+    if (t < t1) {
+      int splits;
+      int64_t ss;
+      const float* src = part_ptr(W, Bv, p, t, nin, nw, &splits, &ss);
+      for (int s0 = warp; s0 < splits; s0 += 64) {  // 8 coalesced loads in flight per lane
+        float tt[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) tt[k] = s0 + 8 * k < splits ? __ldg(src + (int64_t)(s0 + 8 * k) * ss) : 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (s0 + 8 * k < splits) v += tt[k];
+      }
+    }
+    red[warp][lane] = v;
+    __syncthreads();
+    if (warp == 0 && t < t1) {
+      float r = red[0][lane];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) r += red[w][lane];
+      finalize_store(theta, grad, p * ld + off_w + t, r, lambda, prior, inv_sigma2);
+    }
+    return;
+  }
+  const int64_t t = t0 + blk * blockDim.x + threadIdx.x;
   if (t >= t1) return;
   if (mode == 3) {  // G already holds -lambda dW: add grad log p0 (Gaussian prior only; uniform launches none)
     const int64_t idx = p * ld + off_w + t;
@@ -450,15 +681,7 @@ __device__ __forceinline__ void finalize_range(const PartView& W, const PartView
   int splits;
   int64_t ss;
   const float* src = part_ptr(W, Bv, p, t, nin, nw, &splits, &ss);
-  float v = 0.f;
-  if (mode == 1) {
-    for (int s = lane; s < splits; s += 32) v += src[s * ss];
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-    if (lane != 0) return;
-  } else {
-    v = sum_partials(src, splits, ss);
-  }
+  const float v = sum_partials(src, splits, ss);
   finalize_store(theta, grad, p * ld + off_w + t, v, lambda, prior, inv_sigma2);
 }
 // All layers in one launch: block b of the grid belongs to the job whose [blk0, blk0 + nb_w + nb_b)
@@ -485,7 +708,7 @@ __global__ void finalize_all_kernel(const __grid_constant__ FinalizeTable t, con
                    prior, inv_sigma2, p);
 }
 FinalizeJob make_finalize_job(const PartView& W, const PartView& Bv, int64_t off_w, int in, int out) {
-  // warp-per-element only pays off for few elements: it reads each partial row strided (uncoalesced);
+  // many partials over few elements: column groups (partials split over the CTA's warps); otherwise
   // thread-per-element reads one contiguous row of elements per partial, float4-wide when aligned
   auto warp_mode = [](int64_t elems, int splits) { return splits > kThreadSplits && elems < 32768; };
   FinalizeJob j{};
@@ -500,7 +723,7 @@ FinalizeJob make_finalize_job(const PartView& W, const PartView& Bv, int64_t off
   j.w_warp = warp_mode(nw, W.splits) ? 1 : (v4 ? 2 : 0);
   j.b_warp = warp_mode(out, Bv.splits) ? 1 : 0;
   auto blocks = [](int64_t elems, int mode) {
-    return (int)(mode == 1 ? (elems + 7) / 8 : (mode == 2 ? (elems / 4 + 255) / 256 : (elems + 255) / 256));
+    return (int)(mode == 1 ? (elems + 31) / 32 : (mode == 2 ? (elems / 4 + 255) / 256 : (elems + 255) / 256));
   };
   j.nb_w = blocks(nw, j.w_warp);
   j.nb_b = blocks(out, j.b_warp);
