@@ -191,6 +191,15 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
           if constexpr (bwd) {
             ptx::mbar_wait(auxbar, aux_ph);  // aprev of group g has landed in buf
             aux_ph ^= 1;
+            // prefetch aprev of group g + 1 into the other box as soon as the store of group g - 1 (its
+            // previous tenant) has read it, so the load overlaps this group's math and store
+            if (g + 1 < G && lane == 0) {
+              ptx::bulk_wait_read0();
+              const uint32_t nb = ebuf_s + ((g + 1) & 1) * kHalfBox;
+              ptx::mbar_arrive_expect_tx(auxbar, kHalfBox);
+              ptx::tma_load_3d(ptx_ptr(nb), tAux, auxbar, col + 16, row0, p);
+            }
+            __syncwarp();
           } else {
             if (lane == 0) ptx::bulk_wait_read1();  // the store of group g - 2 has finished reading buf
             __syncwarp();
@@ -265,12 +274,6 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
             if (prm.store) {
               ptx::tma_store_3d(tOut, ptx_ptr(buf), col, row0, pz);
               ptx::bulk_commit();
-            }
-            if (bwd && g + 1 < G) {  // prefetch aprev of group g + 1 once the store of group g - 1 has read it
-              ptx::bulk_wait_read1();
-              const uint32_t nb = ebuf_s + ((g + 1) & 1) * kHalfBox;
-              ptx::mbar_arrive_expect_tx(auxbar, kHalfBox);
-              ptx::tma_load_3d(ptx_ptr(nb), tAux, auxbar, col + 16, row0, p);
             }
           }
         }
@@ -989,6 +992,15 @@ bool pair128_default() {
 }
 }  // namespace
 
+// smallest K at which the forward / backward GEMMs take 256-wide pair tiles (single TMEM accumulator);
+// below it they take 128-wide pair tiles with two accumulators.  PUSH_GEMM_FB256_MINK overrides.
+int fb256_min_k() {
+  static const int v = [] {
+    const char* e = getenv("PUSH_GEMM_FB256_MINK");
+    return e && *e ? atoi(e) : 512;
+  }();
+  return v;
+}
 // experiment hook: PUSH_GEMM_CHUNK=<k-blocks per promotion chunk> (pair kernel; default kChunkKB)
 int chunk_kb_env() {
   static const int v = [] {
@@ -1026,7 +1038,7 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   // (profiles/r01_gemm.md).  PUSH_GEMM_1SM=1
   // forces the 1-CTA kernel, PUSH_GEMM_PAIR=1 the pair kernel wherever N % 256 == 0 (A/B comparisons).
   const bool dbg_ok = !(pb.passes >> 8 & (1 | 8)) && !force_1sm();
-  const bool pair256 = dbg_ok && pb.N % 256 == 0 && (pb.epi == EPI_STORE || pb.K >= 512 || force_pair() == 1);
+  const bool pair256 = dbg_ok && pb.N % 256 == 0 && (pb.epi == EPI_STORE || pb.K >= fb256_min_k() || force_pair() == 1);
   const bool pair128 = dbg_ok && !pair256 && pb.N % 128 == 0 && (force_pair() == 2 || pair128_default());
   const bool pair = pair256 || pair128;
   const int BN = pair256 ? 256 : (pair128 ? 128 : choose_bn(pb.N));
