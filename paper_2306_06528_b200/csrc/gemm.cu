@@ -1001,6 +1001,15 @@ int fb256_min_k() {
   }();
   return v;
 }
+// experiment hook: PUSH_GEMM_CHUNK_FB=<k-blocks per chunk> for the forward / backward GEMMs only
+// (scripts/chunk_fb_precision.py: 8 already breaks the 1e-5 g bar on C2- and C5-shaped nets)
+int chunk_kb_fb_env() {
+  static const int v = [] {
+    const char* e = getenv("PUSH_GEMM_CHUNK_FB");
+    return e && *e ? atoi(e) : 0;
+  }();
+  return v;
+}
 // experiment hook: PUSH_GEMM_CHUNK=<k-blocks per promotion chunk> (pair kernel; default kChunkKB)
 int chunk_kb_env() {
   static const int v = [] {
@@ -1069,6 +1078,7 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   kp.passes = pb.passes & 0xff; kp.epi = pb.epi; kp.act = pb.act;
   kp.store = pb.out != nullptr;
   kp.chunk_kb = chunk_kb_env() > 0 ? chunk_kb_env() : kChunkKB;
+  if (pb.epi != EPI_STORE && chunk_kb_fb_env() > 0) kp.chunk_kb = chunk_kb_fb_env();
   kp.dbg = pb.passes >> 8;
   kp.mt = (pb.M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM);
   kp.nt = pb.N / BN;
