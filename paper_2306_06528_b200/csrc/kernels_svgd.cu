@@ -391,6 +391,32 @@ __device__ uint32_t block_select(const float* __restrict__ D, int64_t N, uint32_
   return prefix;
 }
 
+// The (rank+1)-th smallest key given v = the rank-th: v itself if more than rank + 1 keys are <= v,
+// else the smallest key > v (one counting / min pass instead of a second radix select).
+__device__ uint32_t block_next(const float* __restrict__ D, int64_t N, uint32_t rank, uint32_t v, uint32_t* sh) {
+  uint32_t cnt = 0, mn = 0xffffffffu;
+  for (int64_t idx = threadIdx.x; idx < N; idx += blockDim.x) {
+    const uint32_t key = __float_as_uint(D[idx]);
+    cnt += key <= v;
+    if (key > v) mn = min(mn, key);
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, m);
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, m));
+  }
+  if (threadIdx.x == 0) { sh[0] = 0; sh[1] = 0xffffffffu; }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&sh[0], cnt);
+    atomicMin(&sh[1], mn);
+  }
+  __syncthreads();
+  const uint32_t r = sh[0] > rank + 1 ? v : sh[1];
+  __syncthreads();
+  return r;
+}
+
 // Median of all n^2 entries of D without touching the redundant ones: D has a +0 diagonal and
 // D_ij = D_ji >= 0, so the ascending list of all n^2 entries is n zeros followed by every strictly-
 // upper-triangle value u twice, and the two middle order statistics are
@@ -419,9 +445,24 @@ __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(const float* __res
     float v0, v1;
     if (use_tri) {
       const int64_t m = (int64_t)n * (n - 1) / 2;
-      for (int64_t idx = threadIdx.x; idx < N; idx += blockDim.x) {
-        const int i = (int)(idx / n), j = (int)(idx - (int64_t)i * n);
-        if (j > i) skeys[(int64_t)i * n - (int64_t)i * (i + 1) / 2 + (j - i - 1)] = D[idx];
+      // staging: 4 loads in flight per thread (a single CTA streams all n^2 entries; one load at a
+      // time left it latency-bound)
+      constexpr int U = 4;
+      for (int64_t b0 = threadIdx.x; b0 < N; b0 += (int64_t)U * blockDim.x) {
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t idx = b0 + (int64_t)u * blockDim.x;
+          v[u] = idx < N ? D[idx] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t idx = b0 + (int64_t)u * blockDim.x;
+          if (idx < N) {
+            const int i = (int)(idx / n), j = (int)(idx - (int64_t)i * n);
+            if (j > i) skeys[(int64_t)i * n - (int64_t)i * (i + 1) / 2 + (j - i - 1)] = v[u];
+          }
+        }
       }
       __syncthreads();
       if (n == 2) {
@@ -431,12 +472,14 @@ __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(const float* __res
         v0 = v1 = __uint_as_float(block_select(skeys, m, (uint32_t)((int64_t)(n - 1) * (n - 1) / 4 - 1), hist, sh));
       } else {
         const uint32_t k0 = (uint32_t)((int64_t)n * (n - 2) / 4 - 1);
-        v0 = __uint_as_float(block_select(skeys, m, k0, hist, sh));
-        v1 = __uint_as_float(block_select(skeys, m, k0 + 1, hist, sh));
+        const uint32_t u0 = block_select(skeys, m, k0, hist, sh);
+        v0 = __uint_as_float(u0);
+        v1 = __uint_as_float(block_next(skeys, m, k0, u0, sh));
       }
     } else {
-      v0 = __uint_as_float(block_select(D, N, (uint32_t)((N - 1) / 2), hist, sh));
-      v1 = __uint_as_float(block_select(D, N, (uint32_t)(N / 2), hist, sh));
+      const uint32_t u0 = block_select(D, N, (uint32_t)((N - 1) / 2), hist, sh);
+      v0 = __uint_as_float(u0);
+      v1 = (N & 1) ? v0 : __uint_as_float(block_next(D, N, (uint32_t)((N - 1) / 2), u0, sh));
     }
     if (threadIdx.x == 0) {
       const float med = (v0 + v1) * 0.5f;
