@@ -594,18 +594,20 @@ template <>
 __device__ __forceinline__ float vadd(float a, float b) { return a + b; }
 template <>
 __device__ __forceinline__ float4 vadd(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
-template <typename V>
+template <typename V, bool MANY = true>  // MANY = false: splits <= 8 guaranteed (float4 path: registers)
 __device__ __forceinline__ V sum_partials(const V* src, int splits, int64_t ss_v) {
   V zero;
   memset(&zero, 0, sizeof(V));
-  if (splits <= 8) {  // all loads issued before the (ascending) adds
-    V t[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) t[u] = u < splits ? __ldg(src + u * ss_v) : zero;
+  if (!MANY || splits <= 8) {  // ascending; four loads issued before their adds (few registers: occupancy)
     V v = zero;
+    for (int s0 = 0; s0 < splits; s0 += 4) {
+      V t[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (u < splits) v = vadd(v, t[u]);
+      for (int u = 0; u < 4; ++u) t[u] = s0 + u < splits ? __ldg(src + (s0 + u) * ss_v) : zero;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (s0 + u < splits) v = vadd(v, t[u]);
+    }
     return v;
   }
   V a[8];
@@ -632,7 +634,7 @@ __device__ __forceinline__ void finalize_range(const PartView& W, const PartView
     int splits;
     int64_t ss;
     const float* src = part_ptr(W, Bv, p, t, nin, nw, &splits, &ss);
-    const float4 v = sum_partials(reinterpret_cast<const float4*>(src), splits, ss / 4);
+    const float4 v = sum_partials<float4, false>(reinterpret_cast<const float4*>(src), splits, ss / 4);
     const int64_t idx = p * ld + off_w + t;
     float4 pr = make_float4(0.f, 0.f, 0.f, 0.f);
     if (prior == PUSH_PRIOR_GAUSSIAN) {
@@ -718,7 +720,8 @@ FinalizeJob make_finalize_job(const PartView& W, const PartView& Bv, int64_t off
   j.in = in;
   j.out = out;
   const int64_t nw = (int64_t)in * out;
-  const bool v4 = in % 4 == 0 && off_w % 4 == 0 && W.pstride % 4 == 0 && W.sstride % 4 == 0 && W.ostride % 4 == 0 &&
+  const bool v4 = W.splits <= 8 && in % 4 == 0 && off_w % 4 == 0 && W.pstride % 4 == 0 && W.sstride % 4 == 0 &&
+                  W.ostride % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(W.base) & 15) == 0;
   j.w_warp = warp_mode(nw, W.splits) ? 1 : (v4 ? 2 : 0);
   j.b_warp = warp_mode(out, Bv.splits) ? 1 : 0;
