@@ -311,32 +311,53 @@ void dist_partial(const float* theta, int64_t ld, int n, const DistPlan& pl, con
   else dist_launch<64, 4>(theta, ld, n, pl, ranges, part, s);
 }
 
-// One warp per D entry: lane l sums the tensor's splits s = s0 + l, s0 + l + 32, ... ascending, then a
-// fixed xor tree (order depends only on the split table, which depends only on n and the tensor ranges).
-__global__ void dist_reduce_kernel(const float* __restrict__ part, int n, int tensors, const TSplit ts,
-                                   const RankSlots rs, float* __restrict__ D) {
-  const int lane = threadIdx.x & 31;
-  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+// A CTA per 32 consecutive D entries of one tensor: lane = entry (coalesced partial rows), warp w
+// sums the tensor's splits s = s0 + w, s0 + w + 8, ... ascending (8 loads in flight per lane), then the
+// 8 warp sums are added in ascending w.  The order depends only on the split table (n and the tensor
+// ranges), never on the sharding; the rank-block slot of split s is its owner's (NEXT-4).
+__global__ void __launch_bounds__(256) dist_reduce_kernel(const float* __restrict__ part, int n, int tensors,
+                                                          const TSplit ts, const RankSlots rs, float* __restrict__ D) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nn = (int64_t)n * n;
-  if (t >= nn * tensors) return;
-  const int tt = (int)(t / nn);
-  const int64_t e = t - tt * nn;
-  const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
+  const int64_t groups = (nn + 31) / 32;
+  const int tt = (int)(blockIdx.x / groups);
+  const int64_t e = (blockIdx.x - (int64_t)tt * groups) * 32 + lane;
+  const bool ok = tt < tensors && e < nn;
+  const int i = ok ? (int)(e / n) : 0, j = ok ? (int)(e - (int64_t)i * n) : 0;
   float v = 0.f;
-  if (i != j) {
+  if (ok && i != j) {
+    const int s0 = ts.s[tt], s1 = ts.s[tt + 1];
     int q = 0;  // owner rank of split s (monotone in s)
-    for (int s = ts.s[tt] + lane; s < ts.s[tt + 1]; s += 32) {
-      while (q + 1 < rs.P && s >= rs.s0[q + 1]) ++q;
-      v += part[(int64_t)(q * rs.smax + s - rs.s0[q]) * nn + e];
+    for (int sb = s0 + warp; sb < s1; sb += 64) {
+      float t[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int s = sb + 8 * k;
+        if (s < s1) {
+          while (q + 1 < rs.P && s >= rs.s0[q + 1]) ++q;
+          t[k] = __ldg(part + (int64_t)(q * rs.smax + s - rs.s0[q]) * nn + e);
+        } else {
+          t[k] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (sb + 8 * k < s1) v += t[k];
     }
   }
+  red[warp][lane] = v;
+  __syncthreads();
+  if (warp == 0 && ok) {
+    float r = red[0][lane];
 #pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-  if (lane == 0) D[t] = v;  // diagonal is exactly +0
+    for (int w = 1; w < 8; ++w) r += red[w][lane];
+    D[(int64_t)tt * nn + e] = (i == j) ? 0.f : r;  // diagonal is exactly +0
+  }
 }
 void dist_reduce(const float* part, int n, const DistPlan& pl, const RankSlots& rs, float* D, cudaStream_t s) {
-  const int64_t nn = (int64_t)n * n * pl.tensors;
-  dist_reduce_kernel<<<(unsigned)((nn * 32 + 255) / 256), 256, 0, s>>>(part, n, pl.tensors, pl.tsplit, rs, D);
+  const int64_t groups = ((int64_t)n * n + 31) / 32;
+  dist_reduce_kernel<<<(unsigned)(groups * pl.tensors), 256, 0, s>>>(part, n, pl.tensors, pl.tsplit, rs, D);
 }
 
 // ---------------------------------------------------------------- a8 + a9

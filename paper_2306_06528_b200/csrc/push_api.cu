@@ -44,6 +44,7 @@ struct LayerPlan {
   bool gemm = false;             // tensor-core path (hidden layer with in, out % 32 == 0)
   bool wraw = false;             // GEMM reads W straight from Theta (16-B aligned) and splits it in smem
   int64_t woff = 0;              // offset of this layer's hi/lo weight copy (per-particle block), !wraw only
+  int wsplit_max = 1;            // weight-gradient split count at max_batch (partial buffer size)
 };
 
 constexpr int kMaxX0 = 4;  // thin first layer whose weight grads are fused into layer 1's BWD epilogue
@@ -113,15 +114,37 @@ static push_status validate(const push_config* c, int world) {
 // Split-K count of a weight-gradient GEMM (K = B): enough splits that one particle's layer has >= 32
 // 128x128 output tiles, at most 8 and at most one per 1024 rows.  It depends only on (B, layer shape),
 // never on the number of particles per rank, so the dW summation order is the same for every P.
-static int wgrad_splits(int B, int out, int in) {
+// Weight-gradient GEMMs whose N = in is a multiple of 256 run on 256 x 256 CTA-pair tiles: there the
+// count is the one (<= 8, >= 1024 rows per split) that minimises waves x k-blocks per tile over the
+// n particles' tiles on B200's 74 SM pairs; a larger count must cut that by >= 10% (every split adds
+// a partial round trip through HBM and the finalize pass).  This
+// depends on (B, layer shape, n), never on the sharding, so the summation order is P-invariant.
+constexpr int kPlanSmPairs = 148 / 2;
+static int wgrad_splits(int B, int out, int in, int n) {
+  const int cap = std::min(8, std::max(1, B / 1024));
+  if (in % 256 == 0) {
+    const int64_t tiles = (int64_t)((out + 255) / 256) * (in / 256) * n;
+    const int64_t nkb = (B + 31) / 32;
+    int best = 1;
+    int64_t best_cost = INT64_MAX / 16;
+    for (int want = 1; want <= cap; ++want) {
+      const int S = gemm::effective_splits(B, want);
+      const int64_t cost = ((tiles * S + kPlanSmPairs - 1) / kPlanSmPairs) * ((nkb + S - 1) / S);
+      if (10 * cost < 9 * best_cost) {  // a split must buy >= 10%: each one adds a partial round trip
+        best_cost = cost;
+        best = S;
+      }
+    }
+    return best;
+  }
   const int tiles = ((out + 127) / 128) * ((in + 127) / 128);
-  const int want = std::min({8, std::max(1, B / 1024), std::max(1, (32 + tiles - 1) / tiles)});
+  const int want = std::min({cap, std::max(1, (32 + tiles - 1) / tiles)});
   return gemm::effective_splits(B, want);
 }
 
 // A weight-gradient GEMM with one split writes -lambda dW straight into G (TMA-legal when the layer's
-// weights start on a 16-B boundary and rows are whole 16-B units); wgrad_splits is monotone in B, so
-// one split at max_batch means one split for every batch and the layer needs no partial buffer.
+// weights start on a 16-B boundary and rows are whole 16-B units).  Run-time splits are capped at the
+// max_batch count, so one split at max_batch means one split for every batch and no partial buffer.
 static bool wgrad_in_g(int off_w_mod4, int in, int S) { return S == 1 && off_w_mod4 == 0 && in % 4 == 0; }
 
 static push_status make_plan(const push_config* c, int world, Plan* p) {
@@ -224,7 +247,8 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.o_bpart.assign(P.L, 0);
   for (int l = 0; l < P.L; ++l) {
     const LayerPlan& lp = P.layers[l];
-    const int smax = wgrad_splits(P.Bmax, lp.out, lp.in);
+    const int smax = wgrad_splits(P.Bmax, lp.out, lp.in, P.n);
+    P.layers[l].wsplit_max = smax;
     if (lp.gemm && !wgrad_in_g((int)(lp.off_w % 4), lp.in, smax))
       P.o_wpart[l] = take((int64_t)smax * P.nl * lp.in * lp.out);
     // thin weight partials (thin hidden layers) or bias-only column sums (GEMM layers under a thin one)
@@ -551,7 +575,8 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
     const float* dl = c->dlt[xb];
     const ActView ap = layer_input(c, l, x);
     if (lp.gemm) {
-      const int S = wgrad_splits(B, lp.out, lp.in);
+      // never more splits than the partial buffer was sized for at max_batch
+      const int S = std::min(wgrad_splits(B, lp.out, lp.in, P.n), lp.wsplit_max);
       gemm::Problem pb;
       pb.M = lp.out; pb.N = lp.in; pb.K = B; pb.batch = nl; pb.splits = S; pb.passes = 3;
       pb.A = gemm::Operand{dl, nullptr, true, true, lp.out, P.dlt_pst};

@@ -54,6 +54,12 @@ GRAD_CASES = [
     (2, [4, 64, 64, 2], 333, "tanh", "gaussian", 2.0, 1.0, "gauss"),      # d_out = 2, fused x0 with d_in = 4
     (2, [3, 128, 1], 8192, "tanh", "uniform", 1.0, 1.0, "burgers"),       # L = 2: output layer right above thin
     (2, [1, 33, 32, 32, 1], 160, "tanh", "uniform", 1.0, 1.0, "gauss"),   # GEMM layer with W not 16-B aligned
+    # streaming output layer (output_stream_kernel): slab sizes, ragged blocks, d_out, activations
+    (2, [4, 1], 100, "tanh", "uniform", 1.0, 1.0, "gauss"),               # L = 1: no delta below, shared x
+    (2, [2, 64, 64, 3], 150, "identity", "uniform", 1.0, 1.0, "gauss"),   # d_out = 3 (DOUT 4), identity
+    (2, [3, 1024, 1], 300, "tanh", "gaussian", 1.5, 1.0, "burgers"),     # 8-row slabs, 3-deep ring, ragged
+    (2, [2, 2048, 1], 100, "tanh", "uniform", 1.0, 1.0, "gauss"),         # 4-row slabs, 8 features / thread
+    (2, [2, 300, 2], 77, "relu", "uniform", 1.0, 1.0, "gauss"),           # H % 256 != 0, d_out = 2, relu
 ]
 
 
@@ -75,7 +81,7 @@ def test_grads_match_oracle(n, dims, B, act, prior, sigma, lam, data):
 
 # ------------------------------------------------------------------ kernel phase a7-a10
 @pytest.mark.parametrize("n,d", [(1, 100), (2, 37), (3, 1000), (16, 5000), (33, 777), (64, 2048), (100, 96),
-                                 (300, 64), (8, 70001)])
+                                 (300, 64), (8, 70001), (4, 3333), (5, 4099), (6, 20000), (7, 131)])
 def test_step_from_set_grads_matches_oracle(n, d):
     Th = synth.random_theta(n, d, seed=n + d, scale=0.2)
     G = synth.random_grads(n, d, seed=n * d)
