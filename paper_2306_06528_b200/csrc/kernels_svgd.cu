@@ -632,6 +632,109 @@ static void update_launch(const float* theta, const float* grad, int64_t ld, int
   svgd_update_kernel<RB, CT><<<grid, kUpdThreads, smem, s>>>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n,
                                                              theta_next);
 }
+// Many own rows (n_local >= 32): one CTA covers 64 own rows (4 row groups of 16, one per pair of
+// warps) x 256 columns, and the theta_j / g_j column slices are staged ONCE per CTA in shared memory by
+// a cp.async ring of kUpdJ rows, instead of every 16-row CTA streaming them from L2 (4x the L2 reads
+// at n_local = 64, and latency-bound: long-scoreboard stalls at 24% warp occupancy).  Per (i, k) the
+// arithmetic and the ascending-j order are those of svgd_update_kernel<16, 4>: bit-identical results.
+constexpr int kUpdJ = 16, kUpdSCols = 256, kUpdSRows = 64;
+__global__ void __launch_bounds__(256) svgd_update_staged_kernel(const float* __restrict__ theta,
+                                                                 const float* __restrict__ grad, int64_t ld, int n,
+                                                                 int row0, int nl, const float* __restrict__ K,
+                                                                 const float* __restrict__ srow,
+                                                                 const float* __restrict__ hptr, float eps_n,
+                                                                 float* __restrict__ theta_next) {
+  extern __shared__ __align__(16) float usm[];
+  float* sKT = usm;                                   // [n][64]: K_(rb0+i),j at sKT[j*64 + i]
+  float* sTG = usm + (size_t)n * kUpdSRows;           // [2 stages][kUpdJ][2][256]
+  const int tid = threadIdx.x, cg = tid & 63, rg = tid >> 6;
+  const int rb0 = blockIdx.y * kUpdSRows;
+  const int rows = min(kUpdSRows, nl - rb0);
+  const int64_t cb = (int64_t)blockIdx.x * kUpdSCols;
+  for (int idx = tid; idx < kUpdSRows * n; idx += 256) {
+    const int j = idx / kUpdSRows, i = idx - j * kUpdSRows;
+    sKT[idx] = i < rows ? K[(int64_t)(rb0 + i) * n + j] : 0.f;
+  }
+  const uint32_t sTG_u = static_cast<uint32_t>(__cvta_generic_to_shared(sTG));
+  const int nchunk = (n + kUpdJ - 1) / kUpdJ;
+  auto issue = [&](int ck) {  // rows [ck*J, ck*J + J) of theta and g, columns [cb, cb + 256)
+    if (ck < nchunk) {
+      const uint32_t base = sTG_u + (uint32_t)((ck & 1) * kUpdJ * 2 * kUpdSCols) * 4u;
+      for (int q = tid; q < kUpdJ * 2 * (kUpdSCols / 4); q += 256) {
+        const int jj = q / (2 * (kUpdSCols / 4)), rem = q - jj * 2 * (kUpdSCols / 4);
+        const int arr = rem / (kUpdSCols / 4), c4 = rem - arr * (kUpdSCols / 4);
+        const int j = ck * kUpdJ + jj;
+        const int64_t col = cb + 4 * c4;
+        const bool ok = j < n && col < ld;
+        const float* src = (arr ? grad : theta) + (ok ? (int64_t)j * ld + col : 0);
+        const uint32_t dst = base + (uint32_t)((jj * 2 + arr) * kUpdSCols + 4 * c4) * 4u;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue(0);
+  const float r2 = 2.0f / *hptr;
+  float acc[16][4];
+#pragma unroll
+  for (int r = 0; r < 16; ++r)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[r][e] = 0.f;
+  for (int ck = 0; ck < nchunk; ++ck) {
+    issue(ck + 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    const float* st = sTG + (ck & 1) * kUpdJ * 2 * kUpdSCols;
+    const int jn = min(kUpdJ, n - ck * kUpdJ);
+#pragma unroll 2
+    for (int jj = 0; jj < jn; ++jj) {
+      const float4 tv = *reinterpret_cast<const float4*>(st + (jj * 2) * kUpdSCols + 4 * cg);
+      const float4 gv = *reinterpret_cast<const float4*>(st + (jj * 2 + 1) * kUpdSCols + 4 * cg);
+      const float m[4] = {fmaf(-r2, tv.x, gv.x), fmaf(-r2, tv.y, gv.y), fmaf(-r2, tv.z, gv.z), fmaf(-r2, tv.w, gv.w)};
+      const float4* kj = reinterpret_cast<const float4*>(sKT + (ck * kUpdJ + jj) * kUpdSRows + rg * 16);
+#pragma unroll
+      for (int r4 = 0; r4 < 4; ++r4) {
+        const float4 k4 = kj[r4];
+        const float kk[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[4 * r4 + u][e] = fmaf(kk[u], m[e], acc[4 * r4 + u][e]);
+      }
+    }
+    __syncthreads();  // stage (ck & 1) is refilled by the next iteration's issue
+  }
+  const int64_t c = cb + 4 * cg;
+  if (c >= ld) return;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int lr = rg * 16 + r;
+    if (lr < rows) {
+      const int64_t i = row0 + rb0 + lr;
+      const float rs = r2 * srow[rb0 + lr];
+      const float4 tv = *reinterpret_cast<const float4*>(theta + i * ld + c);
+      float4 o;
+      o.x = fmaf(eps_n, fmaf(rs, tv.x, acc[r][0]), tv.x);
+      o.y = fmaf(eps_n, fmaf(rs, tv.y, acc[r][1]), tv.y);
+      o.z = fmaf(eps_n, fmaf(rs, tv.z, acc[r][2]), tv.z);
+      o.w = fmaf(eps_n, fmaf(rs, tv.w, acc[r][3]), tv.w);
+      *reinterpret_cast<float4*>(theta_next + i * ld + c) = o;
+    }
+  }
+}
+static void update_staged_launch(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl,
+                                 const float* K, const float* srow, const float* h, float eps_over_n,
+                                 float* theta_next, cudaStream_t s) {
+  const size_t smem = sizeof(float) * ((size_t)n * kUpdSRows + 2 * kUpdJ * 2 * kUpdSCols);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(svgd_update_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const dim3 grid((unsigned)((ld + kUpdSCols - 1) / kUpdSCols), (unsigned)((nl + kUpdSRows - 1) / kUpdSRows));
+  svgd_update_staged_kernel<<<grid, 256, smem, s>>>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next);
+}
 // (RB, CT) = (16, 4) (8 x 4 when n_local <= 8): measured fastest (C3 1.7 ms vs 2.2 ms for 32 x 2 and
 // 2.5 ms for 64 x 1, whose lower re-read factor does not pay for the smaller loads).
 int update_row_block(int n, int nl, int64_t ld) {
@@ -642,6 +745,8 @@ int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int ro
                 const float* srow, const float* h, float eps_over_n, float* theta_next, cudaStream_t s) {
   if (update_row_block(n, nl, ld) == 8)
     update_launch<8, 4>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next, s);
+  else if (nl >= 32 && n <= 512 && ld % 4 == 0)  // sKT (n x 64) + the 64 KB ring fit in shared memory
+    update_staged_launch(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next, s);
   else
     update_launch<16, 4>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next, s);
   return 1;
