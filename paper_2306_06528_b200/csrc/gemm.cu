@@ -993,11 +993,13 @@ bool pair128_default() {
 }  // namespace
 
 // smallest K at which the forward / backward GEMMs take 256-wide pair tiles (single TMEM accumulator);
-// below it they take 128-wide pair tiles with two accumulators.  PUSH_GEMM_FB256_MINK overrides.
+// below it they take 128-wide pair tiles with two accumulators.  256 since the epilogue bias / aprev
+// changes (C2 1.102 -> 1.073 ms/step: A is read once per row block instead of once per 128-column
+// tile).  PUSH_GEMM_FB256_MINK overrides.
 int fb256_min_k() {
   static const int v = [] {
     const char* e = getenv("PUSH_GEMM_FB256_MINK");
-    return e && *e ? atoi(e) : 512;
+    return e && *e ? atoi(e) : 256;
   }();
   return v;
 }
