@@ -159,6 +159,7 @@ __device__ __forceinline__ TileCoord decode(int t, const KParams& prm) {
 // Fused epilogue of one 32-row x CW-column slab held in registers (acc), written through the
 // warp's double-buffered swizzled 32x16 smem half-boxes with TMA stores (see the v3 notes above).
 // aux_ph: parity of the warp's aprev barrier (BWD); the aprev box of group 0 must already be in flight.
+constexpr int kEpiMaxDin = 4;  // widest thin first layer fused into the BWD epilogue (push_api kMaxX0)
 // FWD: lane l's slice b_l[colw + 4 l .. 4 l + 3] of the warp's CW bias columns (b_l need not be 16-B aligned)
 template <int CW, int EPI>
 __device__ __forceinline__ float4 load_bias4(const KParams& prm, int lane, int colw, int p) {
@@ -182,6 +183,17 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
         // (32 rows x 16 fp32, SWIZZLE_64B: 16-B chunk c of row r sits at chunk c ^ ((r >> 1) & 3)),
         // so the TMA store of group g overlaps the math of group g + 1.
         constexpr int G = CW / 16;
+        // BWD with a fused thin first layer: lane l holds x[row0 + l][0 .. din) (0 past M); the 16 rows a
+        // lane's column partial needs arrive by shuffles instead of 16 global loads per group and input
+        float xrow[kEpiMaxDin];
+#pragma unroll
+        for (int i = 0; i < kEpiMaxDin; ++i) xrow[i] = 0.f;
+        if (bwd && prm.bpart) {
+          const int row = row0 + lane;
+#pragma unroll
+          for (int i = 0; i < kEpiMaxDin; ++i)
+            if (i < prm.din && row < prm.M) xrow[i] = __ldg(prm.x + (long long)row * prm.din + i);
+        }
         const uint32_t roff = lane * 64;
         const int swz = (lane >> 1) & 3;
 #pragma unroll
@@ -255,14 +267,12 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
             for (int r = 0; r < 16; ++r) sm += v[r];
             sm += __shfl_xor_sync(0xffffffffu, sm, 16);
             if (lane < 16) prm.bpart[rb * prm.bp_sstride + p * prm.bp_pstride + col + cl] = sm;
-            for (int i = 0; i < prm.din; ++i) {
+#pragma unroll
+            for (int i = 0; i < kEpiMaxDin; ++i) {
+              if (i >= prm.din) break;
               float sx = 0.f;
 #pragma unroll
-              for (int r = 0; r < 16; ++r) {
-                const int row = row0 + r0 + r;
-                const float xv = row < prm.M ? __ldg(prm.x + (long long)row * prm.din + i) : 0.f;
-                sx = fmaf(v[r], xv, sx);
-              }
+              for (int r = 0; r < 16; ++r) sx = fmaf(v[r], __shfl_sync(0xffffffffu, xrow[i], r0 + r), sx);
               sx += __shfl_xor_sync(0xffffffffu, sx, 16);
               if (lane < 16)
                 prm.xpart[rb * prm.xp_sstride + p * prm.xp_pstride + (long long)(col + cl) * prm.din + i] = sx;
