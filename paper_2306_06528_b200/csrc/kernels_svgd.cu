@@ -735,11 +735,12 @@ static void update_staged_launch(const float* theta, const float* grad, int64_t 
   const dim3 grid((unsigned)((ld + kUpdSCols - 1) / kUpdSCols), (unsigned)((nl + kUpdSRows - 1) / kUpdSRows));
   svgd_update_staged_kernel<<<grid, 256, smem, s>>>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next);
 }
-// (RB, CT) = (16, 4) (8 x 4 when n_local <= 8): measured fastest (C3 1.7 ms vs 2.2 ms for 32 x 2 and
-// 2.5 ms for 64 x 1, whose lower re-read factor does not pay for the smaller loads).
+// (RB, CT) = (16, 4) (8 x 4 when n_local <= 16: twice the CTAs for the L2-resident C2 update, 15 -> 13
+// us): measured fastest (C3 1.7 ms vs 2.2 ms for 32 x 2 and 2.5 ms for 64 x 1, whose lower re-read
+// factor does not pay for the smaller loads); n_local >= 32 takes the staged kernel above.
 int update_row_block(int n, int nl, int64_t ld) {
   (void)n; (void)ld;
-  return nl <= 8 ? 8 : 16;
+  return nl <= 16 ? 8 : 16;
 }
 int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl, const float* K,
                 const float* srow, const float* h, float eps_over_n, float* theta_next, cudaStream_t s) {
