@@ -9,4 +9,12 @@ timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytes
   -k "512 or 300" > $OUT/memcheck_gemm.log 2>&1; echo "memcheck_gemm exit $?" >> $OUT/memcheck_gemm.log
 timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x \
   -k "grads_match_oracle and dims0" > $OUT/racecheck.log 2>&1; echo "racecheck exit $?" >> $OUT/racecheck.log
-for f in memcheck memcheck_gemm racecheck; do tail -n 4 $OUT/$f.log; done
+# the shared-memory kernels added in session 3: streaming output layer (slab ring), staged update,
+# n <= 8 distances, column-group finalize / distance reduction
+timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x \
+  -k "(grads_match_oracle and (dims7 or dims12 or dims14 or dims15)) or (step_from_set_grads and (33-777 or 64-2048 or 5-4099 or 100-96))" \
+  > $OUT/racecheck2.log 2>&1; echo "racecheck2 exit $?" >> $OUT/racecheck2.log
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x \
+  -k "(grads_match_oracle and (dims12 or dims13 or dims14 or dims15 or dims16)) or (step_from_set_grads and (4-3333 or 6-20000 or 300-64))" \
+  > $OUT/memcheck2.log 2>&1; echo "memcheck2 exit $?" >> $OUT/memcheck2.log
+for f in memcheck memcheck_gemm racecheck racecheck2 memcheck2; do tail -n 4 $OUT/$f.log; done
