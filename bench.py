@@ -306,6 +306,12 @@ def run_ours(args, w):
     if all_gemm_ms:
         roof["all_gemm_tflops"] = all_gemm_fl / (all_gemm_ms / 1e3) / 1e12
         roof["all_gemm_share"] = all_gemm_ms / tot
+    # every non-GEMM pass with algorithmic bytes, against the HBM peak (the GEMMs are tensor-bound; the
+    # distances / update passes are ALU-bound at n_local >= ~11 / ~45, L2-resident for small working
+    # sets: DESIGN.md §6 says which roofline binds each at each config)
+    roof["hbm_passes"] = {r["name"]: {"gbs": r["alg_bytes"] / (r["ms"] / 1e3) / 1e9,
+                                      "frac": r["alg_bytes"] / (r["ms"] / 1e3) / 1e9 / peaks["hbm_gbs"]}
+                          for r in prof if r["ms"] and r.get("alg_bytes") and not r["name"].endswith("gemm")}
     upd = next((r for r in prof if r["name"] == "svgd_update"), None)
     if upd and upd["ms"]:
         roof["svgd_update_gbs"] = upd["alg_bytes"] / (upd["ms"] / 1e3) / 1e9
