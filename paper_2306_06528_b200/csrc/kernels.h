@@ -130,6 +130,10 @@ struct RankSlots {
 // D[t][i][j] = sum_{s in tensor t} part[slot(s)][i][j] (ascending s), D_ii = +0
 void dist_reduce(const float* part, int n, const DistPlan& pl, const RankSlots& rs, float* D, cudaStream_t s);
 
+// Gram form of a7: part[s][i][j] (S split-K partials of Theta Theta^T) -> G[i][j] = sum_s part (ascending
+// s, column groups), then D_ij = D_ji = max(G_aa + G_bb - 2 G_ab, 0) with (a, b) = (min, max)(i, j), D_ii = +0
+void gram_to_dist(const float* part, int S, int n, float* G, float* D, cudaStream_t s);
+
 // ---------------------------------------------------------------- a8 + a9 bandwidth and kernel matrix
 // Per tensor t (one CTA each): h_t from D_t (rule, c = fp32 1/ln n or 1/ln(n+1), or fixed bw_h);
 // K[t][i][j] = exp(-D_t[row0+i][j]/h_t), srow[t][i] = sum_j K[t][i][j]

@@ -69,6 +69,7 @@ struct Plan {
   std::vector<int64_t> ds_c0;
   int64_t ds_wmax = 0;  // widest column panel
   int ds_smax = 0;      // most splits on one rank (the all-gathered partial slots per rank)
+  int gram_splits = 0;  // > 0: a7 as the Gram matrix Theta Theta^T on the tensor cores (split-K partials)
   // byte offsets into the workspace
   size_t o_theta0, o_theta1, o_grad, o_whi, o_wlo, o_dlt0, o_dlt1, o_err2, o_loss, o_loss_all, o_opw, o_opb,
       o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf, o_pred, o_swag_mean, o_swag_sq, o_dranges, o_useg,
@@ -212,6 +213,17 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.dist = kern::dist_plan(P.n, P.tensors, P.toff.data(), P.tsize.data(), c->variant ? P.d : P.ld);
   if (c->variant) P.useg = kern::var_segments(P.tensors, P.toff.data(), P.tsize.data());
   P.ds = c->exchange == PUSH_XCHG_DSHARD;
+  // Many particles (n >= 32, n % 32 == 0), canonical all-gather path: a7 is compute-bound there (2 FP32
+  // ops per pair and column on the CUDA cores, the diagonal tile doing both triangles), so D comes from
+  // the Gram matrix G = Theta Theta^T as a split-K 3xTF32 tcgen05 GEMM, D_ij = G_ii + G_jj - 2 G_ij
+  // (clamped at 0; exactly symmetric, D_ii = +0).  Cancellation is ~1e-7 ||theta||^2, i.e. harmless
+  // unless particles coincide to ~1e-2 of their norm (R27).  Partials reuse the direct
+  // path's slots (one slot left for G); the split count depends only on (n, ld).
+  if (!P.ds && c->variant == 0 && P.n >= 32 && P.n % 32 == 0) {
+    const int64_t nkb = (P.ld + 31) / 32;
+    const int want = (int)std::min<int64_t>({(int64_t)P.dist.splits - 1, 148, std::max<int64_t>(1, nkb / 8)});
+    if (want >= 1) P.gram_splits = gemm::effective_splits((int)P.ld, want);
+  }
   if (P.ds) {
     const int S = P.dist.splits;
     for (int q = 0; q <= world; ++q) P.ds_s0.push_back((int)((int64_t)q * S / world));
@@ -813,11 +825,28 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   if ((st = exchange(c, BUF_GRAD, s)) != PUSH_OK) return st;
   const float* th = c->theta[c->cur];
   const double nd4 = 4.0 * P.n * (double)P.d;
-  st = run_k(c, PC_DIST, 2, nd4, 3.0 * P.n * (double)P.n * P.d / 2, s, [&] {
-    kern::dist_partial(th, P.ld, P.n, P.dist, c->dranges, c->dpart, s);
-    kern::dist_reduce(c->dpart, P.n, P.dist, c->slots, c->D, s);
-    return PUSH_OK;
-  });
+  if (P.gram_splits > 0) {
+    const int S = P.gram_splits, n = P.n;
+    st = run_k(c, PC_DIST, 3, nd4, 2.0 * n * (double)n * P.ld, s, [&] {
+      gemm::Problem pb;
+      pb.M = n; pb.N = n; pb.K = (int)P.ld; pb.batch = 1; pb.splits = S; pb.passes = 3;
+      pb.A = gemm::Operand{th, nullptr, true, false, P.ld, 0};
+      pb.B = gemm::Operand{th, nullptr, true, false, P.ld, 0};
+      pb.epi = gemm::EPI_STORE;
+      pb.out = c->dpart; pb.ldo = n; pb.out_pstride = (int64_t)n * n; pb.out_sstride = (int64_t)n * n;
+      push_status g = gemm::run(pb, s);
+      if (g != PUSH_OK) return g;
+      float* G = c->dpart + (int64_t)S * n * n;
+      kern::gram_to_dist(c->dpart, S, n, G, c->D, s);
+      return PUSH_OK;
+    });
+  } else {
+    st = run_k(c, PC_DIST, 2, nd4, 3.0 * P.n * (double)P.n * P.d / 2, s, [&] {
+      kern::dist_partial(th, P.ld, P.n, P.dist, c->dranges, c->dpart, s);
+      kern::dist_reduce(c->dpart, P.n, P.dist, c->slots, c->D, s);
+      return PUSH_OK;
+    });
+  }
   if (st != PUSH_OK) return st;
   st = run_k(c, PC_BANDWIDTH, 1, 4.0 * P.tensors * P.n * P.n, 0, s, [&] {
     kern::bandwidth_kernel(c->D, P.n, c->row0, P.nl, c->cfg.bw_rule, c->c_ln, c->cfg.bw_h, c->h, c->K, c->srow,
