@@ -48,7 +48,7 @@ void init_theta(float* theta, int64_t ld, int row0, int rows, int64_t d, uint64_
 
 // ---------------------------------------------------------------- a7 distances
 // Tile shapes (rows per tile side T, pairs per thread RT x RT, column groups G per CTA):
-//   n <= 8: T=8 (dist_small_kernel below) | n <= 16: T=16 RT=2 G=4 | n <= 32: T=32 RT=2 G=1 | else T=64 RT=4 G=1
+//   n <= 8: dist_small_kernel below (register-only) | n <= 16: T=16 RT=2 G=4 | n <= 32: T=32 RT=2 G=1 | else T=64 RT=4 G=1
 // Each CTA owns one upper-triangular tile pair (bi <= bj) and a fixed column range (split s);
 // sub-chunks of DistCW<T> columns of both row tiles are double-buffered in smem with cp.async.
 // Every accumulation order depends only on (n, ld), never on the number of ranks.
@@ -196,43 +196,50 @@ __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restri
       }
     }
 }
-// Few particles (n <= 8, one 8x8 tile): the tiled kernel above is shared-memory bound there (2 LDS per
-// (pair, column) against one staged float per row), so this one skips shared memory: thread = 4
-// consecutive columns of all N rows (N float4 loads straight to registers, two column groups in
-// flight), accumulating the N(N-1)/2 strictly-upper pair sums in registers over the split's
-// columns (ascending per thread); then per pair a fixed xor tree over the warp and the 8 warps
-// summed in ascending order.  The order depends only on the split's column range, so partials are
-// the same whichever rank computes the split (P-invariance, NEXT-4).  HBM-bound: 4 n bytes/column.
+// Few particles (n <= 8, one tile): the tiled kernel above is shared-memory / latency bound there
+// (2 LDS per (pair, column) against one staged float per row), so this one skips shared memory:
+// thread = CT consecutive columns of all N rows (N vector loads straight to registers, two column
+// groups in flight), accumulating the N(N-1)/2 strictly-upper pair sums in registers over the split's
+// columns (ascending per thread); then per pair a fixed xor tree over the warp and the 8 warps summed
+// in ascending order.  The order depends only on the split's column range, so partials are the same
+// whichever rank computes the split (P-invariance, NEXT-4).  HBM-bound: 4 n bytes per column.
+// (CT = 2 lets n up to 16 keep its 120 pair sums in registers, but that measured slower than the
+// tiled kernel at C2, so only n <= 8 takes this path.)
 constexpr int kDistSmallThreads = 256;
-template <int N>
-__global__ void __launch_bounds__(kDistSmallThreads, 2) dist_small_kernel(const float* __restrict__ theta, int64_t ld,
-                                                                       const int64_t* __restrict__ ranges,
-                                                                       float* __restrict__ part) {
+template <int CT> struct DistVec;
+template <> struct DistVec<4> { using T = float4; };
+template <> struct DistVec<2> { using T = float2; };
+template <int N, int CT>
+__global__ void __launch_bounds__(kDistSmallThreads, N <= 8 ? 2 : 1) dist_small_kernel(
+    const float* __restrict__ theta, int64_t ld, const int64_t* __restrict__ ranges, float* __restrict__ part) {
+  using V = typename DistVec<CT>::T;
   constexpr int NP = N * (N - 1) / 2;
   __shared__ float red[kDistSmallThreads / 32][NP > 0 ? NP : 1];
   const int s = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t c_begin = ranges[2 * s], c_end = ranges[2 * s + 1], c_al = c_begin & ~(int64_t)3;
+  const int64_t c_begin = ranges[2 * s], c_end = ranges[2 * s + 1], c_al = c_begin & ~(int64_t)(CT - 1);
   float acc[NP > 0 ? NP : 1];
 #pragma unroll
   for (int q = 0; q < NP; ++q) acc[q] = 0.f;
-  auto load = [&](int64_t col, float (&v)[N][4]) {
-    if (col >= c_begin && col + 4 <= c_end) {
+  auto load = [&](int64_t col, float (&v)[N][CT]) {
+    if (col >= c_begin && col + CT <= c_end) {
 #pragma unroll
       for (int r = 0; r < N; ++r) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(theta + (int64_t)r * ld + col));
-        v[r][0] = t.x; v[r][1] = t.y; v[r][2] = t.z; v[r][3] = t.w;
+        const V t = __ldg(reinterpret_cast<const V*>(theta + (int64_t)r * ld + col));
+        const float* tf = reinterpret_cast<const float*>(&t);
+#pragma unroll
+        for (int e = 0; e < CT; ++e) v[r][e] = tf[e];
       }
     } else {  // straddling group (per-tensor ranges only) or past the end: outside columns are 0
 #pragma unroll
       for (int r = 0; r < N; ++r)
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
+        for (int e = 0; e < CT; ++e)
           v[r][e] = (col + e >= c_begin && col + e < c_end) ? __ldg(theta + (int64_t)r * ld + col + e) : 0.f;
     }
   };
-  auto accumulate = [&](const float (&v)[N][4]) {
+  auto accumulate = [&](const float (&v)[N][CT]) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < CT; ++e) {
       int q = 0;
 #pragma unroll
       for (int i = 0; i < N; ++i)
@@ -243,17 +250,17 @@ __global__ void __launch_bounds__(kDistSmallThreads, 2) dist_small_kernel(const 
         }
     }
   };
-  constexpr int64_t kStep = 4 * kDistSmallThreads;
-  int64_t col = c_al + 4 * tid;
+  constexpr int64_t kStep = CT * kDistSmallThreads;
+  int64_t col = c_al + CT * tid;
   for (; col + kStep < c_end; col += 2 * kStep) {
-    float v0[N][4], v1[N][4];
+    float v0[N][CT], v1[N][CT];
     load(col, v0);
     load(col + kStep, v1);
     accumulate(v0);
     accumulate(v1);
   }
   if (col < c_end) {
-    float v0[N][4];
+    float v0[N][CT];
     load(col, v0);
     accumulate(v0);
   }
@@ -292,17 +299,17 @@ static void dist_launch(const float* theta, int64_t ld, int n, const DistPlan& p
 }
 void dist_partial(const float* theta, int64_t ld, int n, const DistPlan& pl, const int64_t* ranges, float* part,
                   cudaStream_t s) {
-  if (pl.T == 8 && n >= 2) {
+  if (pl.T == 8 && n >= 2) {  // (n = 9..16 through this kernel measured slower at C2: 39 vs 28 us)
     const dim3 grid(1, pl.splits);
-#define PUSH_DIST_SMALL(NN) dist_small_kernel<NN><<<grid, kDistSmallThreads, 0, s>>>(theta, ld, ranges, part)
+#define PUSH_DIST_SMALL(NN, CT) dist_small_kernel<NN, CT><<<grid, kDistSmallThreads, 0, s>>>(theta, ld, ranges, part)
     switch (n) {
-      case 2: PUSH_DIST_SMALL(2); break;
-      case 3: PUSH_DIST_SMALL(3); break;
-      case 4: PUSH_DIST_SMALL(4); break;
-      case 5: PUSH_DIST_SMALL(5); break;
-      case 6: PUSH_DIST_SMALL(6); break;
-      case 7: PUSH_DIST_SMALL(7); break;
-      default: PUSH_DIST_SMALL(8); break;
+      case 2: PUSH_DIST_SMALL(2, 4); break;
+      case 3: PUSH_DIST_SMALL(3, 4); break;
+      case 4: PUSH_DIST_SMALL(4, 4); break;
+      case 5: PUSH_DIST_SMALL(5, 4); break;
+      case 6: PUSH_DIST_SMALL(6, 4); break;
+      case 7: PUSH_DIST_SMALL(7, 4); break;
+      default: PUSH_DIST_SMALL(8, 4); break;
     }
 #undef PUSH_DIST_SMALL
   } else if (pl.T == 8) dist_launch<8, 1>(theta, ld, n, pl, ranges, part, s);
