@@ -490,6 +490,27 @@ __device__ uint32_t block_next(const float* __restrict__ D, int64_t N, uint32_t 
   return r;
 }
 
+// Few keys (m <= blockDim): the rank-th smallest by counting — thread t holds key t and computes its
+// stable rank #{u < key_t} + #{u' == key_t before t}; ranks are a permutation, so exactly one thread
+// holds rank `rank` (one pass and two barriers instead of four radix passes).  Value-identical to
+// block_select (the same order statistic).
+__device__ uint32_t block_select_small(const float* __restrict__ K, int m, uint32_t rank, uint32_t* sh) {
+  const int t = threadIdx.x;
+  if (t < m) {
+    const uint32_t kt = __float_as_uint(K[t]);
+    uint32_t r = 0;
+    for (int u = 0; u < m; ++u) {
+      const uint32_t ku = __float_as_uint(K[u]);
+      r += (ku < kt) || (ku == kt && u < t);
+    }
+    if (r == rank) sh[0] = kt;
+  }
+  __syncthreads();
+  const uint32_t v = sh[0];
+  __syncthreads();
+  return v;
+}
+
 // Median of all n^2 entries of D without touching the redundant ones: D has a +0 diagonal and
 // D_ij = D_ji >= 0, so the ascending list of all n^2 entries is n zeros followed by every strictly-
 // upper-triangle value u twice, and the two middle order statistics are
@@ -542,10 +563,13 @@ __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(const float* __res
         v0 = 0.f;
         v1 = skeys[0];
       } else if (n & 1) {
-        v0 = v1 = __uint_as_float(block_select(skeys, m, (uint32_t)((int64_t)(n - 1) * (n - 1) / 4 - 1), hist, sh));
+        const uint32_t k = (uint32_t)((int64_t)(n - 1) * (n - 1) / 4 - 1);
+        v0 = v1 = __uint_as_float(m <= (int64_t)blockDim.x ? block_select_small(skeys, (int)m, k, sh)
+                                                            : block_select(skeys, m, k, hist, sh));
       } else {
         const uint32_t k0 = (uint32_t)((int64_t)n * (n - 2) / 4 - 1);
-        const uint32_t u0 = block_select(skeys, m, k0, hist, sh);
+        const uint32_t u0 = m <= (int64_t)blockDim.x ? block_select_small(skeys, (int)m, k0, sh)
+                                                     : block_select(skeys, m, k0, hist, sh);
         v0 = __uint_as_float(u0);
         v1 = __uint_as_float(block_next(skeys, m, k0, u0, sh));
       }
