@@ -77,7 +77,11 @@ enum { PUSH_BW_MEDIAN_LN_N = 0, PUSH_BW_MEDIAN_LN_N1 = 1, PUSH_BW_FIXED = 2 };
 enum {
   PUSH_WHAT_THETA = 0,   /* n x d canonical parameters (current Theta)            */
   PUSH_WHAT_GRAD = 1,    /* n x d canonical g of the last grads call (likelihood term only under PRIOR_SUM) */
-  PUSH_WHAT_DIST = 2,    /* T x n x n squared distances D of the last step (T = 1 unless PER_TENSOR) */
+  PUSH_WHAT_DIST = 2,    /* T x n x n squared distances D of the last step (T = 1 unless PER_TENSOR).
+                            Summed directly as sum_k (theta_ik - theta_jk)^2, except n >= 32 with
+                            n % 32 == 0 on the all-gather path: D_ij = G_ii + G_jj - 2 G_ij from the
+                            Gram matrix (tensor cores), clamped at 0 (R27).  Always exactly
+                            symmetric with a +0 diagonal. */
   PUSH_WHAT_H = 3,       /* T floats: bandwidth h of the last step                    */
   PUSH_WHAT_LOSS = 4,    /* n floats: per-particle MSE of the last grads call (pre-update) */
   PUSH_WHAT_KERNEL = 5   /* T x n_local x n kernel matrix K of the last step (own rows) */
