@@ -1059,8 +1059,8 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   // (profiles/r01_gemm.md).  PUSH_GEMM_1SM=1
   // forces the 1-CTA kernel, PUSH_GEMM_PAIR=1 the pair kernel wherever N % 256 == 0 (A/B comparisons).
   const bool dbg_ok = !(pb.passes >> 8 & (1 | 8)) && !force_1sm();
-  const bool pair256 = dbg_ok && pb.N % 256 == 0 && (pb.epi == EPI_STORE || pb.K >= fb256_min_k() || force_pair() == 1);
-  const bool pair128 = dbg_ok && !pair256 && pb.N % 128 == 0 && (force_pair() == 2 || pair128_default());
+  const bool pair256 = dbg_ok && !pb.no_pair && pb.N % 256 == 0 && (pb.epi == EPI_STORE || pb.K >= fb256_min_k() || force_pair() == 1);
+  const bool pair128 = dbg_ok && !pb.no_pair && !pair256 && pb.N % 128 == 0 && (force_pair() == 2 || pair128_default());
   const bool pair = pair256 || pair128;
   const int BN = pair256 ? 256 : (pair128 ? 128 : choose_bn(pb.N));
   const int box_b = pair ? BN / 2 : BN;

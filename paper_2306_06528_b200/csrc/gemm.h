@@ -42,6 +42,7 @@ struct Problem {
                             // (BWD only: nullptr = compute the fused partials, store nothing)
   int64_t ldo = 0, out_pstride = 0, out_sstride = 0;  // out_sstride must equal batch*out_pstride when splits > 1
   float alpha = 1.f;            // EPI_STORE: out = alpha * acc
+  bool no_pair = false;         // force the 1-CTA kernel (M <= 128: the pair tiles would idle 3/4 of the MMAs)
   const float* bias = nullptr;  // FWD: bias of particle p at bias + p*bias_pstride
   int64_t bias_pstride = 0;
   const float* aprev = nullptr;  // BWD: activation a_{l-1} [p][m][n] (ld_aprev, aprev_pstride)

@@ -829,6 +829,44 @@ int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int ro
   return 1;
 }
 
+// ---------------------------------------------------------------- a10 on the tensor cores (n_local >= 32)
+__global__ void update_lhs_kernel(const float* __restrict__ K, int nl, int n, const float* __restrict__ hptr,
+                                  int g_first, float* __restrict__ lhs) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)nl * 2 * n) return;
+  const int i = (int)(e / (2 * n)), q = (int)(e - (int64_t)i * 2 * n);
+  const int j = q < n ? q : q - n;
+  const bool gpart = (q < n) == (g_first != 0);
+  const float k = K[(int64_t)i * n + j];
+  lhs[e] = gpart ? k : -(2.0f / *hptr) * k;
+}
+void update_lhs(const float* K, int nl, int n, const float* h, bool g_first, float* lhs, cudaStream_t s) {
+  const int64_t tot = (int64_t)nl * 2 * n;
+  update_lhs_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(K, nl, n, h, g_first ? 1 : 0, lhs);
+}
+__global__ void update_fixup_kernel(const float* __restrict__ th, int64_t ld4, const float* __restrict__ srow,
+                                    const float* __restrict__ hptr, float eps_n, float* __restrict__ next) {
+  const int i = blockIdx.y;
+  const float rs = (2.0f / *hptr) * srow[i];
+  const float4* t4 = reinterpret_cast<const float4*>(th) + (int64_t)i * ld4;
+  float4* n4 = reinterpret_cast<float4*>(next) + (int64_t)i * ld4;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ld4; c += (int64_t)gridDim.x * blockDim.x) {
+    const float4 t = __ldg(t4 + c);
+    float4 u = n4[c];
+    u.x = fmaf(eps_n, fmaf(rs, t.x, u.x), t.x);
+    u.y = fmaf(eps_n, fmaf(rs, t.y, u.y), t.y);
+    u.z = fmaf(eps_n, fmaf(rs, t.z, u.z), t.z);
+    u.w = fmaf(eps_n, fmaf(rs, t.w, u.w), t.w);
+    n4[c] = u;
+  }
+}
+void update_fixup(const float* theta_own, int64_t ld, int nl, const float* srow, const float* h, float eps_n,
+                  float* next_own, cudaStream_t s) {
+  const int64_t ld4 = ld / 4;
+  const int bx = (int)std::min<int64_t>((ld4 + 255) / 256, std::max<int64_t>(1, 4 * 148 / nl + 1));
+  update_fixup_kernel<<<dim3(bx, nl), 256, 0, s>>>(theta_own, ld4, srow, h, eps_n, next_own);
+}
+
 // ---------------------------------------------------------------- NEXT-2: PusH's own update (variants)
 // One CTA = one segment of <= 128 columns inside a single tensor t x RB own rows; thread = one column.
 // The CTA keeps K^t's RB rows transposed in smem; per j a thread loads theta_jc and g_jc (coalesced

@@ -70,7 +70,9 @@ struct Plan {
   int64_t ds_wmax = 0;  // widest column panel
   int ds_smax = 0;      // most splits on one rank (the all-gathered partial slots per rank)
   int gram_splits = 0;  // > 0: a7 as the Gram matrix Theta Theta^T on the tensor cores (split-K partials)
+  bool tc_update = false;  // a10 as the contraction [K, -rK] x [G; Theta] on the tensor cores
   // byte offsets into the workspace
+  size_t o_ulhs = 0;
   size_t o_theta0, o_theta1, o_grad, o_whi, o_wlo, o_dlt0, o_dlt1, o_err2, o_loss, o_loss_all, o_opw, o_opb,
       o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf, o_pred, o_swag_mean, o_swag_sq, o_dranges, o_useg,
       o_pth, o_pg, o_pth2, o_pack_th, o_pack_g;
@@ -173,7 +175,8 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
     if (l < P.L - 1) P.Hmax = std::max(P.Hmax, lp.out);
   }
   P.d = off;
-  P.ld = round_up(P.d, 32);
+  // 512-B rows: whole 128-column tiles for the tensor-core update (a10) and the TMA boxes
+  P.ld = round_up(P.d, 128);
   P.fuse_x0 = P.L >= 3 && !P.layers[0].gemm && P.layers[1].gemm && P.layers[0].in <= kMaxX0;
   P.wsplit_total = 0;
   int64_t max_w = 0, max_t = 0;
@@ -224,6 +227,13 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
     const int want = (int)std::min<int64_t>({(int64_t)P.dist.splits - 1, 148, std::max<int64_t>(1, nkb / 8)});
     if (want >= 1) P.gram_splits = gemm::effective_splits((int)P.ld, want);
   }
+  // Many particles (n >= 128, e.g. C4 at n_local = n = 256): a10 is FP32-issue bound on the CUDA cores
+  // (2 n_local flops per streamed element); as a GEMM (M = n_local, N = ld, K = 2n) plus an elementwise
+  // pass it is memory-bound (C4 a10 0.060 -> 0.033 ms).  At n_local = n = 64 (C3, S1) the staged CUDA-core
+  // kernel measured faster (1.19 vs 1.32 ms at C3: the GEMM output and the fix-up pass add 3 n_local ld
+  // floats of traffic), so it keeps those.  2n % 4 == 0 for the K-major left operand.
+  // The choice depends on n only (never on n_local), so every sharding takes the same path (P-invariance).
+  P.tc_update = !P.ds && c->variant == 0 && P.n >= 128 && P.n % 2 == 0 && P.ld % 128 == 0;
   if (P.ds) {
     const int S = P.dist.splits;
     for (int q = 0; q <= world; ++q) P.ds_s0.push_back((int)((int64_t)q * S / world));
@@ -242,9 +252,11 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   };
   const int64_t nld = (int64_t)P.n * P.ld;
   const LayerPlan& top = P.layers[P.L - 1];
+  // Theta[0], G, Theta[1] adjacent (n*ld*4 is a multiple of 256): [Theta_cur; G] or [G; Theta_cur] is
+  // one 2n x ld operand for the tensor-core update
   P.o_theta0 = take(nld);
-  P.o_theta1 = take(nld);
   P.o_grad = take(nld);
+  P.o_theta1 = take(nld);
   P.o_whi = take(P.nl * P.wsplit_total);
   P.o_wlo = take(P.nl * P.wsplit_total);
   P.o_act.resize(P.act_pst.size());
@@ -271,6 +283,7 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.o_opb = take((int64_t)P.RB * P.nl * top.out);
   P.o_xpart = take(P.fuse_x0 ? (int64_t)P.RB * P.nl * P.layers[0].out * P.layers[0].in : 1);
   P.o_dpart = take((int64_t)(P.ds ? world * P.ds_smax : P.dist.splits) * P.n * P.n);
+  P.o_ulhs = take(P.tc_update ? (int64_t)P.nl * 2 * P.n : 1);
   P.o_D = take((int64_t)P.tensors * P.n * P.n);
   P.o_K = take((int64_t)P.tensors * (P.ds ? P.n : P.nl) * P.n);  // d-sharded: K of all n rows
   P.o_s = take((int64_t)P.tensors * (P.ds ? P.n : P.nl));
@@ -331,6 +344,7 @@ struct push_ctx {
   std::vector<float*> wpart, tpart, bpart;  // per layer
   float *opw = nullptr, *opb = nullptr, *xpart = nullptr;
   float *dpart = nullptr, *D = nullptr, *K = nullptr, *srow = nullptr, *h = nullptr;
+  float* ulhs = nullptr;  // tensor-core update: [K, -rK] or [-rK, K] (n_local x 2n)
   int64_t* dranges = nullptr;  // distance split ranges (device copy of P.dist.ranges)
   int4* useg = nullptr;        // variant update segments (device copy of P.useg)
   // NEXT-4 (d-sharded kernel phase): this rank's panel width, its splits (ranges relative to the panel),
@@ -857,8 +871,25 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   const float eps_n = c->cfg.step_size / (float)P.n;
   float* next = c->theta[c->cur ^ 1];
   const int var = c->cfg.variant;
-  st = run_k(c, PC_UPDATE, 1, 2.0 * nd4 + 4.0 * P.nl * (double)P.d, 2.0 * P.nl * (double)P.n * P.d, s, [&] {
-    if (var == 0) {
+  st = run_k(c, PC_UPDATE, (var == 0 && P.tc_update) ? 3 : 1, 2.0 * nd4 + 4.0 * P.nl * (double)P.d,
+             2.0 * P.nl * (double)P.n * P.d, s, [&] {
+    if (var == 0 && P.tc_update) {
+      // U_i = sum_j K_ij g_j - r sum_j K_ij theta_j as one 3xTF32 GEMM over the adjacent [Theta; G] rows
+      // (written into theta_next), then theta'_i = theta_i + (eps/n)(U_i + r s_i theta_i)
+      const bool g_first = c->grad < th;  // layout Theta[0], G, Theta[1]
+      const float* bbase = g_first ? c->grad : th;
+      kern::update_lhs(c->K, P.nl, P.n, c->h, g_first, c->ulhs, s);
+      gemm::Problem pb;
+      pb.M = P.nl; pb.N = (int)P.ld; pb.K = 2 * P.n; pb.batch = 1; pb.splits = 1; pb.passes = 3;
+      pb.A = gemm::Operand{c->ulhs, nullptr, true, false, 2 * P.n, 0};
+      pb.B = gemm::Operand{bbase, nullptr, true, true, P.ld, 0};
+      pb.epi = gemm::EPI_STORE; pb.no_pair = true;
+      pb.out = next + (int64_t)c->row0 * P.ld; pb.ldo = P.ld; pb.out_pstride = (int64_t)P.nl * P.ld;
+      push_status g = gemm::run(pb, s);
+      if (g != PUSH_OK) return g;
+      kern::update_fixup(th + (int64_t)c->row0 * P.ld, P.ld, P.nl, c->srow, c->h, eps_n,
+                         next + (int64_t)c->row0 * P.ld, s);
+    } else if (var == 0) {
       kern::svgd_update(th, c->grad, P.ld, P.n, c->row0, P.nl, c->K, c->srow, c->h, eps_n, next, s);
     } else {  // NEXT-2 (include/push.h PUSH_VAR_*): weights w_d = eps or eps/n, repulsion eps/n
       const bool pn = var & PUSH_VAR_PAPER_NORM;
@@ -957,6 +988,7 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   c->ws = static_cast<uint8_t*>(ws);
   const Plan& P = c->P;
   auto F = [&](size_t o) { return reinterpret_cast<float*>(c->ws + o); };
+  c->ulhs = F(P.o_ulhs);
   c->theta[0] = F(P.o_theta0);
   c->theta[1] = F(P.o_theta1);
   c->grad = F(P.o_grad);

@@ -237,7 +237,12 @@ def test_state_machine_errors():
 
 
 # ------------------------------------------------------------------ sharding (loopback transport)
-@pytest.mark.parametrize("dims,n,B", [([2, 64, 64, 1], 8, 256), ([1, 32, 32, 1], 4, 256)])
+@pytest.mark.parametrize("dims,n,B", [([2, 64, 64, 1], 8, 256), ([1, 32, 32, 1], 4, 256),
+                                      # n = 64: Gram-form distances; staged update at n_local = 64 / 32, the
+                                      # 16-row kernel at n_local = 16 (same arithmetic)
+                                      ([1, 32, 32, 1], 64, 128),
+                                      # n = 128: Gram-form distances and the tensor-core update at every P
+                                      ([1, 32, 32, 1], 128, 64)])
 def test_sharding_bit_identical_across_P(dims, n, B):
     """Theta after 3 steps is bit-identical for P = 1, 2, 4 ranks."""
     x, y = synth.batch("gauss", B, dims[0], dims[-1], 1)
