@@ -65,7 +65,8 @@ DistPlan dist_plan(int n, int tensors, const int64_t* toff, const int64_t* tsize
   pl.npairs = pl.ntile * (pl.ntile + 1) / 2;
   const int cw = pl.T == 8 ? 256 : (pl.T == 16 ? 128 : kDistCW);  // = DistCW<T>::v: split ranges are whole sub-chunks
   const int64_t chunks = (total + cw - 1) / cw;
-  int64_t want = (4 * 148 + pl.npairs - 1) / pl.npairs;
+  // n in (8, 16]: one tile pair, two splits per SM (fewer, longer CTAs and half the partials to reduce)
+  int64_t want = pl.T == 16 ? 2 * 148 : (4 * 148 + pl.npairs - 1) / pl.npairs;
   if (want > chunks) want = chunks;
   if (want < 1) want = 1;
   pl.cols = (((total + want - 1) / want) + cw - 1) / cw * cw;
