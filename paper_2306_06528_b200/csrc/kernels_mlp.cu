@@ -245,6 +245,43 @@ __global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
 // registers.  Keeps up to NST * R * H * 4 bytes of A in flight per CTA instead of loading the whole
 // slab before any math (the one-shot kernel above stalled on long-scoreboard with one CTA per SM).
 constexpr int kOutStreamSlabBytes = 32 * 1024;
+// Phase 1 of NR consecutive slab rows (block rows r_base + lr0 ..): yhat_o = a_r . W_o + b_o with lanes
+// splitting the features (ascending per lane, then a fixed xor tree), e = yhat - y, dL = scale e.
+template <int DOUT, int NR>
+__device__ __forceinline__ void out_phase1(const OutputArgs& a, const float* A, const float* sW, const float* bias,
+                                           int H, int lr0, int r_base, int rows, int rb, int lane, float scale,
+                                           float (*sdl)[DOUT], float (*serr)[DOUT]) {
+  bool ok[NR];
+#pragma unroll
+  for (int rr = 0; rr < NR; ++rr) ok[rr] = r_base + lr0 + rr < rows;
+  const float* a0 = A + lr0 * H;
+  for (int o = 0; o < a.dout; ++o) {
+    const float* wrow = sW + o * H;
+    float part[NR];
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) part[rr] = 0.f;
+#pragma unroll 4
+    for (int i = lane; i < H; i += 32) {
+      const float w = wrow[i];
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr)
+        if (ok[rr]) part[rr] = fmaf(a0[rr * H + i], w, part[rr]);
+    }
+#pragma unroll
+    for (int rr = 0; rr < NR; ++rr) {
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) part[rr] += __shfl_xor_sync(0xffffffffu, part[rr], m);
+      const int r = r_base + lr0 + rr, b = rb * 32 + r;
+      float dl = 0.f;
+      if (r < rows) {
+        const float e = (part[rr] + __ldg(bias + o)) - __ldg(a.y + (int64_t)b * a.dout + o);
+        dl = scale * e;
+        if (lane == 0) serr[r][o] = e;
+      }
+      if (lane == 0 && r < 32) sdl[r][o] = dl;
+    }
+  }
+}
 // Phase 2 of one feature column over nr slab rows: ACT < 0 = no delta below (L = 1); 32-bit offsets.
 template <int DOUT, int ACT>
 __device__ __forceinline__ void out_phase2(const float* ai, int H, int nr, const float (*sd)[DOUT], const float (&wv)[DOUT],
@@ -323,38 +360,15 @@ __global__ void __launch_bounds__(256) output_stream_kernel(const OutputArgs a, 
     }
     const float* A = sA + (k % NST) * R * H;  // row r of the block at A[(r - k R) H]
     const int r_base = k * R;
-    // phase 1: yhat, residual, dL for the slab's rows (per row: lane-strided sum, fixed xor tree)
+    // phase 1: yhat, residual, dL for the slab's rows (per row: lane-strided sum, fixed xor tree);
+    // the rows per warp are a compile-time count (a runtime-masked 4-row loop quadrupled the work at RPW 1)
     if (warp * RPW < R) {
-      const int lr0 = warp * RPW;
-      bool ok[4];
-#pragma unroll
-      for (int rr = 0; rr < 4; ++rr) ok[rr] = rr < RPW && r_base + lr0 + rr < rows;
-      const float* a0 = A + lr0 * H;
-      for (int o = 0; o < a.dout; ++o) {
-        const float* wrow = sW + o * H;
-        float part[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-        for (int i = lane; i < H; i += 32) {
-          const float w = wrow[i];
-#pragma unroll
-          for (int rr = 0; rr < 4; ++rr)
-            if (ok[rr]) part[rr] = fmaf(a0[rr * H + i], w, part[rr]);
-        }
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-          if (rr >= RPW) break;
-#pragma unroll
-          for (int m = 16; m >= 1; m >>= 1) part[rr] += __shfl_xor_sync(0xffffffffu, part[rr], m);
-          const int r = r_base + lr0 + rr, b = rb * 32 + r;
-          float dl = 0.f;
-          if (r < rows) {
-            const float e = (part[rr] + __ldg(bias + o)) - __ldg(a.y + (int64_t)b * a.dout + o);
-            dl = scale * e;
-            if (lane == 0) serr[r][o] = e;
-          }
-          if (lane == 0 && r < 32) sdl[r][o] = dl;
-        }
-      }
+      if (RPW == 4)
+        out_phase1<DOUT, 4>(a, A, sW, bias, H, warp * 4, r_base, rows, rb, lane, scale, sdl, serr);
+      else if (RPW == 2)
+        out_phase1<DOUT, 2>(a, A, sW, bias, H, warp * 2, r_base, rows, rb, lane, scale, sdl, serr);
+      else
+        out_phase1<DOUT, 1>(a, A, sW, bias, H, warp, r_base, rows, rb, lane, scale, sdl, serr);
     }
     __syncthreads();
     // phase 2 over the slab's rows, ascending (activation and delta store resolved at compile time)
