@@ -287,7 +287,7 @@ template <int DOUT, int ACT>
 __device__ __forceinline__ void out_phase2(const float* ai, int H, int nr, const float (*sd)[DOUT], const float (&wv)[DOUT],
                                            float (&wacc)[DOUT], float& bacc, float* dpb) {
   int off = 0;
-#pragma unroll 4
+#pragma unroll 8
   for (int r = 0; r < nr; ++r, off += H) {
     const float av = ai[off];
     float d = 0.f;
