@@ -81,7 +81,9 @@ def test_grads_match_oracle(n, dims, B, act, prior, sigma, lam, data):
 
 # ------------------------------------------------------------------ kernel phase a7-a10
 @pytest.mark.parametrize("n,d", [(1, 100), (2, 37), (3, 1000), (16, 5000), (33, 777), (64, 2048), (100, 96),
-                                 (300, 64), (8, 70001), (4, 3333), (5, 4099), (6, 20000), (7, 131)])
+                                 (300, 64), (8, 70001), (4, 3333), (5, 4099), (6, 20000), (7, 131),
+                                 # tensor-core update (n >= 128) with / without the Gram distances, ld padding
+                                 (130, 999), (160, 3000), (96, 1537)])
 def test_step_from_set_grads_matches_oracle(n, d):
     Th = synth.random_theta(n, d, seed=n + d, scale=0.2)
     G = synth.random_grads(n, d, seed=n * d)
