@@ -15,6 +15,9 @@ timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pyte
   -k "(grads_match_oracle and (dims7 or dims12 or dims14 or dims15)) or (step_from_set_grads and (33-777 or 64-2048 or 5-4099 or 100-96))" \
   > $OUT/racecheck2.log 2>&1; echo "racecheck2 exit $?" >> $OUT/racecheck2.log
 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x \
-  -k "(grads_match_oracle and (dims12 or dims13 or dims14 or dims15 or dims16)) or (step_from_set_grads and (4-3333 or 6-20000 or 300-64))" \
+  -k "(grads_match_oracle and (dims12 or dims13 or dims14 or dims15 or dims16)) or (step_from_set_grads and (4-3333 or 6-20000 or 300-64 or 130-999 or 160-3000 or 96-1537 or 64-2048))" \
   > $OUT/memcheck2.log 2>&1; echo "memcheck2 exit $?" >> $OUT/memcheck2.log
-for f in memcheck memcheck_gemm racecheck racecheck2 memcheck2; do tail -n 4 $OUT/$f.log; done
+# Gram distances + tensor-core update across a loopback group (n = 128, P = 1/2/4)
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x \
+  -k "sharding and 128" > $OUT/memcheck3.log 2>&1; echo "memcheck3 exit $?" >> $OUT/memcheck3.log
+for f in memcheck memcheck_gemm racecheck racecheck2 memcheck2 memcheck3; do tail -n 4 $OUT/$f.log; done
