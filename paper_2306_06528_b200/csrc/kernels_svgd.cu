@@ -610,10 +610,26 @@ __device__ uint32_t block_select_hist(const float* __restrict__ K, int64_t m, ui
 //   n = 2: (0, u[0]);  n odd: u[(n-1)^2/4 - 1] (twice);  n even >= 4: u[n(n-2)/4 - 1], u[n(n-2)/4].
 // For n(n-1)/2 <= kTriKeys the u values are staged in shared memory and selected there.
 constexpr int kTriKeys = 40 * 1024;  // 160 KB of keys
+// K row i and s_i = sum_j K_ij: lane l sums j = l, l+32, ... ascending, then a fixed xor tree (the order
+// depends only on n)
+__device__ __forceinline__ void kernel_row(const float* __restrict__ D, int n, int row0, int i, float h,
+                                           float* __restrict__ K, float* __restrict__ srow, int lane) {
+  const float* drow = D + (int64_t)(row0 + i) * n;
+  float* krow = K + (int64_t)i * n;
+  float acc = 0.f;
+  for (int j = lane; j < n; j += 32) {
+    const float kv = expf(-drow[j] / h);
+    krow[j] = kv;
+    acc += kv;
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if (lane == 0) srow[i] = acc;
+}
 __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(const float* __restrict__ D, int n, int row0, int nl,
                                                               int rule, float c_ln, float bw_h, float* __restrict__ h_out,
                                                               float* __restrict__ K, float* __restrict__ srow,
-                                                              int use_tri) {
+                                                              int use_tri, int krows_here) {
   extern __shared__ float skeys[];
   // CTA b: tensor b's distance matrix, bandwidth, kernel rows and row sums
   D += (int64_t)blockIdx.x * n * n;
@@ -676,22 +692,19 @@ __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(const float* __res
   __syncthreads();
   const float h = s_h;
   if (threadIdx.x == 0) *h_out = h;
-  // K rows and s_i = sum_j K_ij: one warp per own row; lane l sums j = l, l+32, ... ascending, then a
-  // fixed xor tree (the order depends only on n)
+  if (!krows_here) return;  // many rows: kernel_rows_kernel spreads them over the SMs
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  for (int i = warp; i < nl; i += nwarps) {
-    const float* drow = D + (int64_t)(row0 + i) * n;
-    float* krow = K + (int64_t)i * n;
-    float acc = 0.f;
-    for (int j = lane; j < n; j += 32) {
-      const float kv = expf(-drow[j] / h);
-      krow[j] = kv;
-      acc += kv;
-    }
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
-    if (lane == 0) srow[i] = acc;
-  }
+  for (int i = warp; i < nl; i += nwarps) kernel_row(D, n, row0, i, h, K, srow, lane);
+}
+// K rows over many CTAs (warp per own row) once h is known: same per-row arithmetic as above
+__global__ void kernel_rows_kernel(const float* __restrict__ D, int n, int row0, int nl, const float* __restrict__ h_in,
+                                   float* __restrict__ K, float* __restrict__ srow) {
+  const int t = blockIdx.y;  // tensor
+  D += (int64_t)t * n * n;
+  K += (int64_t)t * nl * n;
+  srow += (int64_t)t * nl;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i < nl) kernel_row(D, n, row0, i, h_in[t], K, srow, threadIdx.x & 31);
 }
 void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c_ln, float bw_h, float* h, float* K,
                       float* srow, int tensors, cudaStream_t s) {
@@ -702,8 +715,12 @@ void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c
     cudaFuncSetAttribute(bandwidth_kernel_impl, cudaFuncAttributeMaxDynamicSharedMemorySize, kTriKeys * 4);
     attr = true;
   }
+  // K rows in the same CTA for small n_local * n, else spread over the SMs by a second launch (C4: 256
+  // rows x 256 exp on one SM were a third of the kernel)
+  const int split = (int64_t)nl * n >= 16384;
   bandwidth_kernel_impl<<<tensors, 1024, use_tri ? (size_t)m * 4 : 0, s>>>(D, n, row0, nl, rule, c_ln, bw_h, h, K, srow,
-                                                                    use_tri);
+                                                                    use_tri, split ? 0 : 1);
+  if (split) kernel_rows_kernel<<<dim3((nl + 7) / 8, tensors), 256, 0, s>>>(D, n, row0, nl, h, K, srow);
 }
 
 // ---------------------------------------------------------------- a10 fused update

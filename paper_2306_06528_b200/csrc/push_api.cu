@@ -769,7 +769,7 @@ static push_status ds_phase2(push_ctx* c, cudaStream_t s) {
     return PUSH_OK;
   });
   if (st != PUSH_OK) return st;
-  st = run_k(c, PC_BANDWIDTH, 1, 4.0 * P.n * P.n, 0, s, [&] {
+  st = run_k(c, PC_BANDWIDTH, (int64_t)P.n * P.n >= 16384 ? 2 : 1, 4.0 * P.n * P.n, 0, s, [&] {
     kern::bandwidth_kernel(c->D, P.n, 0, P.n, c->cfg.bw_rule, c->c_ln, c->cfg.bw_h, c->h, c->K, c->srow, 1, s);
     return PUSH_OK;
   });
@@ -862,7 +862,7 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
     });
   }
   if (st != PUSH_OK) return st;
-  st = run_k(c, PC_BANDWIDTH, 1, 4.0 * P.tensors * P.n * P.n, 0, s, [&] {
+  st = run_k(c, PC_BANDWIDTH, (int64_t)P.nl * P.n >= 16384 ? 2 : 1, 4.0 * P.tensors * P.n * P.n, 0, s, [&] {
     kern::bandwidth_kernel(c->D, P.n, c->row0, P.nl, c->cfg.bw_rule, c->c_ln, c->cfg.bw_h, c->h, c->K, c->srow,
                            P.tensors, s);
     return PUSH_OK;
