@@ -251,8 +251,9 @@ push_status push_swag_sample(push_ctx* ctx, uint64_t seed, float* out_dev, void*
 push_status push_predict(push_ctx* ctx, const float* x_dev, int32_t B, float* pred_dev, float* mean_dev,
                          float* std_dev, void* stream);
 
-/* SYNC (collective for THETA / LOSS when world_size > 1).  Copies `what`
- * (PUSH_WHAT_*) to out_host; sizes in the PUSH_WHAT_* comments.
+/* SYNC (collective for THETA, GRAD and LOSS when world_size > 1: each all-gathers the row blocks of
+ * every rank, so every rank must make the same call).  Copies `what` (PUSH_WHAT_*) to out_host; sizes
+ * in the PUSH_WHAT_* comments.  DIST / H / KERNEL are local reads.
  * Errors: PUSH_E_INVALID, PUSH_E_STATE (GRAD/DIST/H/KERNEL/LOSS before they exist). */
 push_status push_gather(push_ctx* ctx, int32_t what, float* out_host, void* stream);
 

@@ -53,6 +53,8 @@ WORKLOADS = {
                    note="256 particles, MLP 1-64x3-1, kernel-bound regime"),
     "C5": Workload("C5", 8, mlp_dims(2, 2048, 6, 1), 1024, "random",
                    note="8 particles, MLP 2-2048x6-1, GEMM-bound regime"),
+    "C5b": Workload("C5b", 8, mlp_dims(2, 2048, 6, 1), 128, "random",
+                    note="8 particles, MLP 2-2048x6-1 at the paper's batch of 128 (PAPER.md:355)"),
     "S1": Workload("S1", 64, mlp_dims(3, 512, 5, 1), 8192, "burgers",
                    note="64 particles x ~1M params (north-star scaling point)"),
 }

@@ -87,3 +87,12 @@ def dyadic_theta(n: int, d: int, seed: int):
     rng = np.random.default_rng(seed)
     k = rng.integers(-32, 33, size=(n, d))
     return (k / 8.0).astype(np.float32)
+
+
+def clustered_theta(n: int, d: int, seed: int, spread: float = 1e-2, center_scale: float = 1.0):
+    """Particles clustered around a common centre: theta_i = mu + spread * delta_i (float32), the
+    regime of a pretrained theta0 plus small noise or of particles that contracted during training
+    (the Gram form of a7 must not cancel here)."""
+    rng = np.random.default_rng(seed)
+    mu = center_scale * rng.standard_normal(d)
+    return (mu + spread * rng.standard_normal((n, d))).astype(np.float32)

@@ -35,6 +35,7 @@
 #include "common.cuh"
 #include "gemm.h"
 #include "ptx.cuh"
+#include "tma_host.h"
 
 namespace push {
 namespace gemm {
@@ -837,6 +838,9 @@ namespace {
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 int g_sms = 0;
+}  // namespace
+
+int sm_count() { return g_sms; }
 
 push_status get_encoder() {
   std::call_once(g_encode_once, [] {
@@ -853,9 +857,9 @@ push_status get_encoder() {
   return PUSH_OK;
 }
 
-// 3-D fp32 tensor map {d0 (contiguous), d1, d2} with box {32, box1, 1}, zero OOB fill.
+// 3-D fp32 tensor map {d0 (contiguous), d1, d2} with box {box0, box1, 1}, zero OOB fill.
 push_status make_map(CUtensorMap* m, const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1_el,
-                     uint64_t stride2_el, uint32_t box1, CUtensorMapSwizzle swz, uint32_t box0 = 32) {
+                     uint64_t stride2_el, uint32_t box1, CUtensorMapSwizzle swz, uint32_t box0) {
   if (d2 <= 1) {  // a shared operand: the stride of a unit dimension is never used
     d2 = 1;
     stride2_el = stride1_el * d1;
@@ -872,6 +876,7 @@ push_status make_map(CUtensorMap* m, const float* base, uint64_t d0, uint64_t d1
   return PUSH_OK;
 }
 
+namespace {
 // B operands are staged in UMMA-canonical swizzled layouts; the A operand only feeds the transform
 // warps (which write it to TMEM), so an MN-major A is staged unswizzled for conflict-free column reads.
 push_status make_operand_map(const float* ptr, const Operand& op, int mn_extent, int K, int batch, int box_rows,
@@ -976,60 +981,15 @@ push_status launch2(bool amn, bool bmn, bool bs, int epi, const CUtensorMap* map
   }
 }
 
-bool force_1sm() {
-  static const int v = [] {
-    const char* e = getenv("PUSH_GEMM_1SM");
-    return e && *e && *e != '0' ? 1 : 0;
-  }();
-  return v != 0;
-}
-// PUSH_GEMM_PAIR=1: 256-wide pair tiles wherever N % 256 == 0; =2: 128-wide pair tiles for the rest
-int force_pair() {
-  static const int v = [] {
-    const char* e = getenv("PUSH_GEMM_PAIR");
-    return e && *e ? atoi(e) : 0;
-  }();
-  return v;
-}
-// 128-wide pair tiles for the forward/backward GEMMs not covered by the 256-wide rule (default on:
-// C2 1.172 -> 1.150 ms/step); PUSH_GEMM_PAIR128=0 falls back to the 1-CTA kernel there.
-bool pair128_default() {
-  static const int v = [] {
-    const char* e = getenv("PUSH_GEMM_PAIR128");
-    return e && *e ? (*e != '0' ? 1 : 0) : 1;
-  }();
-  return v != 0;
-}
 }  // namespace
 
-// smallest K at which the forward / backward GEMMs take 256-wide pair tiles (single TMEM accumulator);
-// below it they take 128-wide pair tiles with two accumulators.  256 since the epilogue bias / aprev
-// changes (C2 1.102 -> 1.073 ms/step: A is read once per row block instead of once per 128-column
-// tile).  PUSH_GEMM_FB256_MINK overrides.
-int fb256_min_k() {
-  static const int v = [] {
-    const char* e = getenv("PUSH_GEMM_FB256_MINK");
-    return e && *e ? atoi(e) : 256;
-  }();
-  return v;
-}
-// experiment hook: PUSH_GEMM_CHUNK_FB=<k-blocks per chunk> for the forward / backward GEMMs only
-// (scripts/chunk_fb_precision.py: 8 already breaks the 1e-5 g bar on C2- and C5-shaped nets)
-int chunk_kb_fb_env() {
-  static const int v = [] {
-    const char* e = getenv("PUSH_GEMM_CHUNK_FB");
-    return e && *e ? atoi(e) : 0;
-  }();
-  return v;
-}
-// experiment hook: PUSH_GEMM_CHUNK=<k-blocks per promotion chunk> (pair kernel; default kChunkKB)
-int chunk_kb_env() {
-  static const int v = [] {
-    const char* e = getenv("PUSH_GEMM_CHUNK");
-    return e && *e ? atoi(e) : 0;
-  }();
-  return v;
-}
+// Kernel choice (profiles/r01_gemm.md): 256-wide CTA-pair tiles for every GEMM with N % 256 == 0 whose
+// K >= kFb256MinK (forward / backward) or with the plain-store epilogue (weight gradients, Gram);
+// 128-wide pair tiles (two rotating TMEM accumulators) for the remaining forward / backward GEMMs with
+// N % 128 == 0; the 1-CTA kernel for the rest.  The fp32 promotion chunk is fixed at kChunkKB k-blocks
+// (longer chunks break the 1e-5 gradient bar).  These are compile-time constants: no environment
+// variable reaches the product path.
+constexpr int kFb256MinK = 256;
 
 int choose_bn(int N) {
   if (N % 128 == 0) return 128;
@@ -1056,11 +1016,10 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   // the 1-CTA kernel) and for forward/backward GEMMs with K >= 512 (C3: 19.5 -> 15.4 ms forward); at
   // K = 256 the 128-wide pair tiles (two rotating TMEM accumulators overlap the fused epilogue with
   // the next tile) are fastest; the 1-CTA kernel covers the remaining (narrow) shapes
-  // (profiles/r01_gemm.md).  PUSH_GEMM_1SM=1
-  // forces the 1-CTA kernel, PUSH_GEMM_PAIR=1 the pair kernel wherever N % 256 == 0 (A/B comparisons).
-  const bool dbg_ok = !(pb.passes >> 8 & (1 | 8)) && !force_1sm();
-  const bool pair256 = dbg_ok && !pb.no_pair && pb.N % 256 == 0 && (pb.epi == EPI_STORE || pb.K >= fb256_min_k() || force_pair() == 1);
-  const bool pair128 = dbg_ok && !pb.no_pair && !pair256 && pb.N % 128 == 0 && (force_pair() == 2 || pair128_default());
+  // (profiles/r01_gemm.md).
+  const bool dbg_ok = !(pb.passes >> 8 & (1 | 8));
+  const bool pair256 = dbg_ok && !pb.no_pair && pb.N % 256 == 0 && (pb.epi == EPI_STORE || pb.K >= kFb256MinK);
+  const bool pair128 = dbg_ok && !pb.no_pair && !pair256 && pb.N % 128 == 0;
   const bool pair = pair256 || pair128;
   const int BN = pair256 ? 256 : (pair128 ? 128 : choose_bn(pb.N));
   const int box_b = pair ? BN / 2 : BN;
@@ -1089,8 +1048,7 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   kp.M = pb.M; kp.N = pb.N; kp.K = pb.K; kp.batch = pb.batch; kp.splits = pb.splits; kp.kb_per_split = kbps;
   kp.passes = pb.passes & 0xff; kp.epi = pb.epi; kp.act = pb.act;
   kp.store = pb.out != nullptr;
-  kp.chunk_kb = chunk_kb_env() > 0 ? chunk_kb_env() : kChunkKB;
-  if (pb.epi != EPI_STORE && chunk_kb_fb_env() > 0) kp.chunk_kb = chunk_kb_fb_env();
+  kp.chunk_kb = kChunkKB;
   kp.dbg = pb.passes >> 8;
   kp.mt = (pb.M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM);
   kp.nt = pb.N / BN;

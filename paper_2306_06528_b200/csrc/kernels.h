@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <vector>
 
+#include "../../include/push.h"
+
 namespace push {
 namespace kern {
 
@@ -130,9 +132,19 @@ struct RankSlots {
 // D[t][i][j] = sum_{s in tensor t} part[slot(s)][i][j] (ascending s), D_ii = +0
 void dist_reduce(const float* part, int n, const DistPlan& pl, const RankSlots& rs, float* D, cudaStream_t s);
 
-// Gram form of a7: part[s][i][j] (S split-K partials of Theta Theta^T) -> G[i][j] = sum_s part (ascending
-// s, column groups), then D_ij = D_ji = max(G_aa + G_bb - 2 G_ab, 0) with (a, b) = (min, max)(i, j), D_ii = +0
-void gram_to_dist(const float* part, int S, int n, float* G, float* D, cudaStream_t s);
+// Centred symmetric Gram form of a7 (gram.cu; canonical kernel, 2 <= n <= kGramMaxN, both exchange modes).
+// Plan: splits x ceil(n/64) i-blocks ~ one wave, ranges whole 128-column units of [0, ld) (T = 0 marks it).
+constexpr int kGramMaxN = 256;
+DistPlan gram_plan(int n, int64_t ld);
+int gram_np(int n);                 // MMA N: n rounded up to a power of two >= 16
+int64_t gram_part_floats(int n);    // floats of one split's partial block: ceil(n/64) x 128 x gram_np(n)
+// part[s] (s < splits, block of gram_part_floats(n)) = [X; Y] of split s's columns of theta (rows 0..n-1,
+// pitch ld, centred on row 0); ranges_dev: the splits' [begin, end) column pairs relative to theta
+push_status gram_partial(const float* theta, int64_t ld, int n, int splits, const int64_t* ranges_dev, float* part,
+                         cudaStream_t s);
+// D_ij = D_ji = max(G_ii + G_jj - 2 G_ij, 0), D_ii = +0, G summed over the S splits in ascending order
+// (split s's block at slot rs(s), as dist_reduce)
+void gram_dist(const float* part, int n, int S, const RankSlots& rs, float* D, cudaStream_t s);
 
 // ---------------------------------------------------------------- a8 + a9 bandwidth and kernel matrix
 // Per tensor t (one CTA each): h_t from D_t (rule, c = fp32 1/ln n or 1/ln(n+1), or fixed bw_h);

@@ -368,51 +368,6 @@ void dist_reduce(const float* part, int n, const DistPlan& pl, const RankSlots& 
   dist_reduce_kernel<<<(unsigned)(groups * pl.tensors), 256, 0, s>>>(part, n, pl.tensors, pl.tsplit, rs, D);
 }
 
-// ---------------------------------------------------------------- a7, Gram form (n >= 32)
-// G[e] = sum_s part[s][e]: a CTA per 32 entries, warp w sums s = w, w + 8, ... ascending, then the warps
-// in ascending order (same scheme as dist_reduce_kernel; the diagonal is kept: it holds ||theta_i||^2)
-__global__ void __launch_bounds__(256) gram_reduce_kernel(const float* __restrict__ part, int64_t nn, int S,
-                                                          float* __restrict__ G) {
-  __shared__ float red[8][33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
-  float v = 0.f;
-  if (e < nn) {
-    for (int sb = warp; sb < S; sb += 64) {
-      float t[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) t[k] = sb + 8 * k < S ? __ldg(part + (int64_t)(sb + 8 * k) * nn + e) : 0.f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (sb + 8 * k < S) v += t[k];
-    }
-  }
-  red[warp][lane] = v;
-  __syncthreads();
-  if (warp == 0 && e < nn) {
-    float r = red[0][lane];
-#pragma unroll
-    for (int w = 1; w < 8; ++w) r += red[w][lane];
-    G[e] = r;
-  }
-}
-__global__ void gram_dist_kernel(const float* __restrict__ G, int n, float* __restrict__ D) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)n * n) return;
-  const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
-  float v = 0.f;
-  if (i != j) {
-    const int a = min(i, j), b = max(i, j);
-    v = fmaxf(fmaf(-2.0f, G[(int64_t)a * n + b], G[(int64_t)a * n + a] + G[(int64_t)b * n + b]), 0.f);
-  }
-  D[e] = v;
-}
-void gram_to_dist(const float* part, int S, int n, float* G, float* D, cudaStream_t s) {
-  const int64_t nn = (int64_t)n * n;
-  gram_reduce_kernel<<<(unsigned)((nn + 31) / 32), 256, 0, s>>>(part, nn, S, G);
-  gram_dist_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(G, n, D);
-}
-
 // ---------------------------------------------------------------- a8 + a9
 // Block-wide radix select of the rank-th smallest key among N non-negative floats
 // (their IEEE bit patterns order like the values).  Histogram counts are

@@ -69,7 +69,7 @@ struct Plan {
   std::vector<int64_t> ds_c0;
   int64_t ds_wmax = 0;  // widest column panel
   int ds_smax = 0;      // most splits on one rank (the all-gathered partial slots per rank)
-  int gram_splits = 0;  // > 0: a7 as the Gram matrix Theta Theta^T on the tensor cores (split-K partials)
+  bool gram = false;    // a7 as the centred symmetric Gram product (gram.cu); dist holds its split plan
   bool tc_update = false;  // a10 as the contraction [K, -rK] x [G; Theta] on the tensor cores
   // byte offsets into the workspace
   size_t o_ulhs = 0;
@@ -216,16 +216,13 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.dist = kern::dist_plan(P.n, P.tensors, P.toff.data(), P.tsize.data(), c->variant ? P.d : P.ld);
   if (c->variant) P.useg = kern::var_segments(P.tensors, P.toff.data(), P.tsize.data());
   P.ds = c->exchange == PUSH_XCHG_DSHARD;
-  // Many particles (n >= 32, n % 32 == 0), canonical all-gather path: a7 is compute-bound there (2 FP32
-  // ops per pair and column on the CUDA cores, the diagonal tile doing both triangles), so D comes from
-  // the Gram matrix G = Theta Theta^T as a split-K 3xTF32 tcgen05 GEMM, D_ij = G_ii + G_jj - 2 G_ij
-  // (clamped at 0; exactly symmetric, D_ii = +0).  Cancellation is ~1e-7 ||theta||^2, i.e. harmless
-  // unless particles coincide to ~1e-2 of their norm (R27).  Partials reuse the direct
-  // path's slots (one slot left for G); the split count depends only on (n, ld).
-  if (!P.ds && c->variant == 0 && P.n >= 32 && P.n % 32 == 0) {
-    const int64_t nkb = (P.ld + 31) / 32;
-    const int want = (int)std::min<int64_t>({(int64_t)P.dist.splits - 1, 148, std::max<int64_t>(1, nkb / 8)});
-    if (want >= 1) P.gram_splits = gemm::effective_splits((int)P.ld, want);
+  // Canonical kernel, 2 <= n <= 256 (both exchange modes): a7 as the centred symmetric Gram product on
+  // the tensor cores (gram.cu; R27) — one HBM stream of Theta, no CUDA-core pair loop.  Its
+  // split plan replaces the direct-form plan; it depends only on (n, ld), so every sharding (and the
+  // d-sharded mode, which owns whole splits) sums the same partials in the same order.
+  if (c->variant == 0 && P.n >= 2 && P.n <= kern::kGramMaxN) {
+    P.dist = kern::gram_plan(P.n, P.ld);
+    P.gram = true;
   }
   // Many particles (n >= 128, e.g. C4 at n_local = n = 256): a10 is FP32-issue bound on the CUDA cores
   // (2 n_local flops per streamed element); as a GEMM (M = n_local, N = ld, K = 2n) plus an elementwise
@@ -282,7 +279,8 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.o_opw = take((int64_t)P.RB * P.nl * top.out * top.in);
   P.o_opb = take((int64_t)P.RB * P.nl * top.out);
   P.o_xpart = take(P.fuse_x0 ? (int64_t)P.RB * P.nl * P.layers[0].out * P.layers[0].in : 1);
-  P.o_dpart = take((int64_t)(P.ds ? world * P.ds_smax : P.dist.splits) * P.n * P.n);
+  P.o_dpart = take((int64_t)(P.ds ? world * P.ds_smax : P.dist.splits) *
+                   (P.gram ? kern::gram_part_floats(P.n) : (int64_t)P.n * P.n));
   P.o_ulhs = take(P.tc_update ? (int64_t)P.nl * 2 * P.n : 1);
   P.o_D = take((int64_t)P.tensors * P.n * P.n);
   P.o_K = take((int64_t)P.tensors * (P.ds ? P.n : P.nl) * P.n);  // d-sharded: K of all n rows
@@ -303,6 +301,11 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.o_swag_sq = take(c->swag ? (int64_t)P.nl * P.ld : 1);
   P.total = cur;
   return PUSH_OK;
+}
+
+// floats of one split's distance partial (the direct form's n x n, or the Gram form's [X; Y] blocks)
+static int64_t part_block(const Plan& P) {
+  return P.gram ? kern::gram_part_floats(P.n) : (int64_t)P.n * P.n;
 }
 
 // ------------------------------------------------------------------ profiling classes
@@ -397,6 +400,15 @@ struct LocalGroup {
 static push_status sticky(push_ctx* c, push_status st) {
   if (st == PUSH_E_CUDA || st == PUSH_E_NCCL) c->broken = true;
   return st;
+}
+
+// Join a Theta all-gather that an eager push_particle_grads left on the comm stream: every
+// entry that reads or exchanges Theta, or issues collectives on `s`, orders itself after it first.
+static push_status join_theta(push_ctx* c, cudaStream_t s) {
+  if (!c->theta_pending) return PUSH_OK;
+  PUSH_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_theta, 0));
+  c->theta_pending = false;
+  return PUSH_OK;
 }
 
 static cudaEvent_t get_event(push_ctx* c) {
@@ -739,7 +751,11 @@ static push_status ds_phase1(push_ctx* c, cudaStream_t s) {
     return e != PUSH_OK ? e : e2;
   });
   if (st != PUSH_OK || c->dist_own.splits == 0) return st;
-  float* part = c->dpart + (int64_t)c->rank * P.ds_smax * P.n * P.n;
+  float* part = c->dpart + (int64_t)c->rank * P.ds_smax * part_block(P);
+  if (P.gram)
+    return run_k(c, PC_DIST, 1, 4.0 * P.n * wo, 2.0 * P.n * (double)P.n * wo, s, [&] {
+      return kern::gram_partial(c->pth, wo, P.n, c->dist_own.splits, c->dranges, part, s);
+    });
   return run_k(c, PC_DIST, 1, 4.0 * P.n * wo, 3.0 * P.n * (double)P.n * wo / 2, s, [&] {
     kern::dist_partial(c->pth, wo, P.n, c->dist_own, c->dranges, part, s);
     return PUSH_OK;
@@ -749,7 +765,7 @@ static push_status ds_phase1(push_ctx* c, cudaStream_t s) {
 static push_status ds_phase2(push_ctx* c, cudaStream_t s) {
   const Plan& P = c->P;
   const int W = c->world;
-  const int64_t blk = (int64_t)P.ds_smax * P.n * P.n, wo = c->ds_w;
+  const int64_t blk = (int64_t)P.ds_smax * part_block(P), wo = c->ds_w;
   push_status st = PUSH_OK;
   if (W > 1 || c->comm) {
     st = run_k(c, PC_EXCHANGE, 0, 4.0 * blk * (W - 1), 0, s, [&]() -> push_status {
@@ -765,7 +781,10 @@ static push_status ds_phase2(push_ctx* c, cudaStream_t s) {
     if (st != PUSH_OK) return st;
   }
   st = run_k(c, PC_DIST, 1, 4.0 * P.n * P.n * (double)P.dist.splits, 0, s, [&] {
-    kern::dist_reduce(c->dpart, P.n, P.dist, c->slots, c->D, s);
+    if (P.gram)
+      kern::gram_dist(c->dpart, P.n, P.dist.splits, c->slots, c->D, s);
+    else
+      kern::dist_reduce(c->dpart, P.n, P.dist, c->slots, c->D, s);
     return PUSH_OK;
   });
   if (st != PUSH_OK) return st;
@@ -831,27 +850,16 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   const Plan& P = c->P;
   push_status st;
   if (P.ds) return ds_group_step({c}, s);  // NCCL ranks (or one rank): three collective phases
-  if (c->theta_pending) {  // join the Theta all-gather started by the gradient call
-    PUSH_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_theta, 0));
-    c->theta_pending = false;
-  }
+  if ((st = join_theta(c, s)) != PUSH_OK) return st;  // the Theta all-gather started by the gradient call
   // C2: g rows of every rank
   if ((st = exchange(c, BUF_GRAD, s)) != PUSH_OK) return st;
   const float* th = c->theta[c->cur];
   const double nd4 = 4.0 * P.n * (double)P.d;
-  if (P.gram_splits > 0) {
-    const int S = P.gram_splits, n = P.n;
-    st = run_k(c, PC_DIST, 3, nd4, 2.0 * n * (double)n * P.ld, s, [&] {
-      gemm::Problem pb;
-      pb.M = n; pb.N = n; pb.K = (int)P.ld; pb.batch = 1; pb.splits = S; pb.passes = 3;
-      pb.A = gemm::Operand{th, nullptr, true, false, P.ld, 0};
-      pb.B = gemm::Operand{th, nullptr, true, false, P.ld, 0};
-      pb.epi = gemm::EPI_STORE;
-      pb.out = c->dpart; pb.ldo = n; pb.out_pstride = (int64_t)n * n; pb.out_sstride = (int64_t)n * n;
-      push_status g = gemm::run(pb, s);
+  if (P.gram) {
+    st = run_k(c, PC_DIST, 2, nd4, 2.0 * P.n * (double)P.n * P.ld, s, [&]() -> push_status {
+      push_status g = kern::gram_partial(th, P.ld, P.n, P.dist.splits, c->dranges, c->dpart, s);
       if (g != PUSH_OK) return g;
-      float* G = c->dpart + (int64_t)S * n * n;
-      kern::gram_to_dist(c->dpart, S, n, G, c->D, s);
+      kern::gram_dist(c->dpart, P.n, P.dist.splits, c->slots, c->D, s);
       return PUSH_OK;
     });
   } else {
@@ -1200,7 +1208,8 @@ push_status push_set_grads(push_ctx* c, const float* g_dev, void* stream) {
   if (st != PUSH_OK) return st;
   if (!g_dev) return fail(PUSH_E_INVALID, "g_dev is NULL");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  st = exchange(c, BUF_THETA, s);
+  st = join_theta(c, s);
+  if (st == PUSH_OK) st = exchange(c, BUF_THETA, s);
   if (st == PUSH_OK)
     st = run_k(c, PC_COPY, 1, 8.0 * c->P.nl * c->P.d, 0, s, [&] {
       kern::copy_rows(g_dev, c->P.d, c->grad + (int64_t)c->row0 * c->P.ld, c->P.ld, c->P.nl, s);
@@ -1258,6 +1267,7 @@ push_status push_step_graph(push_ctx* c, const float* x_dev, const float* y_dev,
   if (c->group && c->world > 1)
     return fail(PUSH_E_STATE, "whole-step calls need every rank's gradients first: use the lockstep calls in a local group");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = join_theta(c, s)) != PUSH_OK) return sticky(c, st);
   const int din = c->P.layers[0].in, dout = c->P.layers[c->P.L - 1].out;
   // the captured step always reads the context's fixed batch buffers
   auto stage = [&]() -> push_status {
@@ -1347,6 +1357,7 @@ push_status push_predict(push_ctx* c, const float* x_dev, int32_t B, float* pred
   if (c->group && c->world > 1)
     return fail(PUSH_E_STATE, "push_predict gathers every rank's predictions: not available in a loopback group");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = join_theta(c, s)) != PUSH_OK) return sticky(c, st);
   if ((st = do_predict(c, x_dev, B, s)) != PUSH_OK) return sticky(c, st);
   const int dout = c->P.layers[c->P.L - 1].out;
   const size_t per = (size_t)B * dout;
@@ -1369,11 +1380,7 @@ push_status push_ensemble_step(push_ctx* c, void* stream) {
   if (st != PUSH_OK) return st;
   if (c->state != 1) return fail(PUSH_E_STATE, "ensemble_step needs fresh gradients");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (c->theta_pending) {  // the Theta all-gather (started by the gradient call) must finish first
-    cudaError_t e = cudaStreamWaitEvent(s, c->ev_theta, 0);
-    if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
-    c->theta_pending = false;
-  }
+  if ((st = join_theta(c, s)) != PUSH_OK) return sticky(c, st);  // the gradient call's Theta all-gather
   const Plan& P = c->P;
   float* th = c->theta[c->cur] + (int64_t)c->row0 * P.ld;
   const float* g = c->grad + (int64_t)c->row0 * P.ld;
@@ -1423,6 +1430,7 @@ push_status push_gather(push_ctx* c, int32_t what, float* out_host, void* stream
   if (st != PUSH_OK) return st;
   if (!out_host) return fail(PUSH_E_INVALID, "out_host is NULL");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = join_theta(c, s)) != PUSH_OK) return sticky(c, st);
   const Plan& P = c->P;
   auto sync = [&]() -> push_status {
     PUSH_CUDA_TRY(cudaStreamSynchronize(s));

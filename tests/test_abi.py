@@ -83,8 +83,9 @@ def test_bad_dims_rejected(L):
 
 def test_variant_field_validated_on_host():
     """push_config.variant: 0..7 accepted (OR of PUSH_VAR_*), anything else PUSH_E_INVALID; per-tensor
-    plans need workspace for T = 2L distance / kernel matrices."""
-    base = push.workspace_size(push.make_config(8, [2, 64, 64, 1], max_batch=64))
+    plans need workspace for T = 2L distance / kernel matrices (compared with a direct-form, T = 1 variant:
+    the canonical plan's Gram partials are sized differently)."""
+    base = push.workspace_size(push.make_config(8, [2, 64, 64, 1], max_batch=64, variant=push.VAR_PAPER_NORM))
     for v in range(8):
         ws = push.workspace_size(push.make_config(8, [2, 64, 64, 1], max_batch=64, variant=v))
         assert ws >= base if v & push.VAR_PER_TENSOR else ws > 0

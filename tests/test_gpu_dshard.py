@@ -51,6 +51,7 @@ def _run(dims, n, B, P, exchange, steps=3, seed=9):
     ([2, 256, 256, 1], 16, 512),      # many splits, ragged split counts per rank
     ([1, 8, 1], 8, 64),               # d = 25: one split, ranks 1.. own no columns
     ([3, 40, 24, 2], 24, 100),        # thin layers, ld padding inside the last rank's panel
+    ([1, 32, 32, 1], 64, 128),        # n = 64: the Gram-form partials (NP = 64) on column panels
 ])
 def test_dshard_bit_identical_to_allgather(dims, n, B):
     base = _run(dims, n, B, 1, "allgather")

@@ -108,7 +108,7 @@ def cfg_dims(cfg):
     return [cfg.dims[i] for i in range(cfg.n_layers + 1)]
 
 
-@pytest.mark.parametrize("n", [2, 3, 4, 9, 16, 25, 300])
+@pytest.mark.parametrize("n", [2, 3, 4, 9, 16, 25, 64, 128, 160, 256, 300])
 def test_bandwidth_bit_exact_on_dyadic_lattice(n):
     """Dyadic Theta: every D_ij is exact in fp32 and fp64, so the GPU median equals the
     oracle's bit for bit and h = fp32(med) * fp32(1/ln n) (R4)."""
@@ -127,7 +127,7 @@ def test_bandwidth_bit_exact_on_dyadic_lattice(n):
 
 
 @pytest.mark.parametrize("rule", ["median_ln_n", "median_ln_n1", "fixed"])
-@pytest.mark.parametrize("n", [5, 16, 64])
+@pytest.mark.parametrize("n", [5, 16, 64, 160, 256])
 def test_bandwidth_reproduced_from_gpu_distances(rule, n):
     """Selection on the GPU's own fp32 D (oracle median, same precision) reproduces h bit-exactly."""
     d = 3000
@@ -144,6 +144,25 @@ def test_bandwidth_reproduced_from_gpu_distances(rule, n):
     med = np.float32(osvgd.median_all(D.astype(np.float64)))
     c = np.float32(1.0 / math.log(n if rule == "median_ln_n" else n + 1))
     assert h == med * c
+
+
+@pytest.mark.parametrize("n,spread", [(16, 1e-2), (64, 1e-1), (64, 1e-2), (128, 1e-2), (256, 1e-3), (300, 1e-2)])
+def test_clustered_particles_distances(n, spread):
+    """theta_i = mu + spread * delta_i (|mu| ~ 1): the Gram form centred on particle 0 keeps D to the
+    1e-5 bar where the uncentred Gram form cancels (R27), and the step matches."""
+    d = 20000
+    Th = synth.clustered_theta(n, d, seed=n, spread=spread)
+    G = synth.random_grads(n, d, seed=5)
+    ctx = push.Context(push.make_config(n, [d - 1, 1], max_batch=1, step_size=0.05), theta0=Th)
+    ctx.set_grads(_dev(G))
+    ctx.svgd_step()
+    ref, info = osvgd.svgd_step(Th, G, 0.05)
+    D = ctx.gather("dist")
+    assert np.array_equal(D, D.T) and np.all(np.diag(D) == 0)
+    off = ~np.eye(n, dtype=bool)
+    assert np.max(np.abs(D[off] - info["D"][off]) / info["D"][off]) <= 1e-5
+    assert float(ctx.gather("h")[0]) == pytest.approx(info["h"], rel=1e-5)
+    assert rel_err(ctx.gather("theta"), ref) <= 1e-4
 
 
 def test_single_particle_is_gradient_ascent():

@@ -5,7 +5,7 @@ from inputs import WORKLOADS, param_count, synth
 
 
 def test_param_counts_match_survey_appendix():
-    expect = {"C1": 1153, "C2": 198401, "C3": 3153921, "C4": 8513, "C5": 20989953, "S1": 1053185}
+    expect = {"C1": 1153, "C2": 198401, "C3": 3153921, "C4": 8513, "C5": 20989953, "C5b": 20989953, "S1": 1053185}
     for k, v in expect.items():
         assert WORKLOADS[k].d == v
     # the paper's scaling nets: 10 DxD layers + Dx1 (App. A)
