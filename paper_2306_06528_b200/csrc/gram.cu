@@ -37,59 +37,72 @@ namespace kern {
 
 namespace {
 constexpr int kGBK = 32;              // fp32 of K per k-block (one 128-B SWIZZLE_128B row per particle)
-constexpr int kGChunkKB = 4;          // k-blocks per TMEM accumulation chunk before the fp32 promotion
-constexpr int kGThreads = 32 * 14;    // warp 0 TMA, warp 1 MMA, warps 2-5 transform, warps 6-13 epilogue
+constexpr int kGGroups = 2;           // transform groups (4 warps each) taking alternate stages
+constexpr int kGXf0 = 2, kGEpi0 = kGXf0 + 4 * kGGroups;
+constexpr int kGThreads = 32 * (kGEpi0 + 8);  // + 8 epilogue warps
 constexpr int kGSmemTiles = 192 * 1024;
 
+// A stage carries KPS k-blocks (every per-stage barrier round trip — TMA landing, transform, MMA
+// issue, commit — amortised over 4 k-blocks: one k-block per stage measured 0.5 us per k-block at S1,
+// latency-bound) and equals the fp32 promotion chunk, so one accumulator drain per stage.
 template <int NP>
 struct GCfg {
-  static constexpr int TILE = NP * 128;                       // NP rows x 128 B
-  static constexpr int STAGES = std::min(16, kGSmemTiles / TILE);
+  static constexpr int KPS = NP <= 64 ? 4 : (NP <= 128 ? 2 : 1);  // k-blocks per stage (<= 128 of K)
+  static constexpr int TILE = NP * kGBK * 4;                  // one k-block: NP rows x 128 B
+  static constexpr int STAGE = KPS * TILE;
+  static constexpr int CHUNK = 4 / KPS;                        // stages per accumulation chunk (128 of K)
+  static constexpr int STAGES = std::min(8, kGSmemTiles / STAGE);
   static constexpr int NACC = NP <= 128 ? 2 : 1;               // TMEM accumulators of NP columns
-  static constexpr int NSLOT = 4;                              // TMEM A slots of 32 columns
-  static constexpr int ASLOT0 = NACC * NP;
+  static constexpr int ASET = KPS * 32;                      // TMEM columns of one stage's A operand
+  static constexpr int ASLOT0 = NACC * NP;                     // kGGroups A sets (one per transform group)
   static constexpr int CW = NP >= 32 ? NP / 2 : 16;            // accumulator columns per epilogue thread
   static constexpr int EPI_SPLIT = NP / CW;                    // epilogue warps per TMEM lane quarter
-  static constexpr int SMEM = 1024 + STAGES * TILE + 512;
-  static_assert(ASLOT0 + 32 * NSLOT <= 512, "tmem");
-  static_assert(CW % 16 == 0 && STAGES >= 2, "cfg");
+  static constexpr int OUTER = NP > 64 ? (NP - 64) * 8 / 128 : 0;  // 16-B units per thread outside the i-block
+  static constexpr int SMEM = 1024 + STAGES * (STAGE + 512) + 512;
+  static_assert(ASLOT0 + ASET * kGGroups <= 512, "tmem");
+  static_assert(CW % 16 == 0 && STAGES >= 2 && STAGES % kGGroups == 0, "cfg");
 };
 
-__device__ __forceinline__ void bar_transform() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// TMEM lane L of the A operand / accumulator <-> i-block row and part: lane quarter q holds rows
+// 16q .. 16q + 15, lane 2r' the Hi (X) and lane 2r' + 1 the Lo (Y) of row 16q + r'.  Hi and Lo of a row
+// sit in the SAME warp, so the pair syncs with __syncwarp before the raw row is overwritten in place.
+__device__ __forceinline__ int lane_row(int q, int lane) { return 16 * q + (lane >> 1); }
 
 template <int NP>
 __global__ void __launch_bounds__(kGThreads, 1)
-    gram_partial_kernel(const __grid_constant__ CUtensorMap tTh, const int64_t* __restrict__ ranges, int n, int n_ib,
-                        float* __restrict__ part) {
+    gram_partial_kernel(const __grid_constant__ CUtensorMap tTh, const __grid_constant__ CUtensorMap tC,
+                        const int64_t* __restrict__ ranges, int n, int n_ib, float* __restrict__ part) {
   using C = GCfg<NP>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::TILE);
+  uint8_t* cbuf = smem + C::STAGES * C::STAGE;  // [STAGES][128] fp32: row 0 (the centre c) of the stage
+  uint64_t* full = reinterpret_cast<uint64_t*>(cbuf + C::STAGES * 512);
   uint64_t* ready = full + C::STAGES;
   uint64_t* empty = ready + C::STAGES;
-  uint64_t* aempty = empty + C::STAGES;
-  uint64_t* tfull = aempty + C::NSLOT;
+  uint64_t* aempty = empty + C::STAGES;  // [kGGroups] A set g free
+  uint64_t* tfull = aempty + kGGroups;
   uint64_t* tempty = tfull + C::NACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::NACC);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, ib = blockIdx.y;
   const int64_t c0 = ranges[2 * split], c1 = ranges[2 * split + 1];
-  const int nkb = (int)((c1 - c0) / kGBK);
+  const int nst = (int)((c1 - c0) / (kGBK * C::KPS));  // ranges are whole 128-column units
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&ready[s], 128);
+      ptx::mbar_init(&ready[s], 128);  // the 4 warps of the group that transforms stage s
       ptx::mbar_init(&empty[s], 1);
     }
-    for (int j = 0; j < C::NSLOT; ++j) ptx::mbar_init(&aempty[j], 1);
+    for (int j = 0; j < kGGroups; ++j) ptx::mbar_init(&aempty[j], 1);
     for (int b = 0; b < C::NACC; ++b) {
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], 32 * 4 * C::EPI_SPLIT);
     }
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tTh);
+    ptx::prefetch_tmap(&tC);
   }
   if (warp == 1) {
     ptx::tmem_alloc(tmem_slot, 512);
@@ -101,98 +114,118 @@ __global__ void __launch_bounds__(kGThreads, 1)
   const uint32_t tmem_base = ptx::lds_u32(ptx::smem_u32(tmem_slot));
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer: rows 0..NP-1 (OOB rows zero-filled), 32 columns
-      for (int i = 0; i < nkb; ++i) {
+    if (lane == 0) {
+      // ---------------- TMA producer: C::KPS tiles of rows 0..NP-1 (OOB rows zero-filled) per stage and
+      // the stage's 128 columns of row 0 (the centre)
+      for (int i = 0; i < nst; ++i) {
         const int s = i % C::STAGES;
+        const int k = (int)(c0 + (int64_t)i * kGBK * C::KPS);
         ptx::mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[s], C::TILE);
-        ptx::tma_load_3d(smem + s * C::TILE, &tTh, &full[s], (int)(c0 + (int64_t)i * kGBK), 0, 0);
+        ptx::mbar_arrive_expect_tx(&full[s], C::STAGE + 128 * C::KPS);
+#pragma unroll
+        for (int j = 0; j < C::KPS; ++j)
+          ptx::tma_load_3d(smem + s * C::STAGE + j * C::TILE, &tTh, &full[s], k + j * kGBK, 0, 0);
+        ptx::tma_load_3d(cbuf + s * 512, &tC, &full[s], k, 0, 0);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    if (lane == 0) {  // ---------------- MMA issuer: CHUNK stages = one accumulation chunk into buffer ch % NACC
       constexpr uint32_t idesc = ptx::idesc_tf32(128, NP, false, false);
-      uint32_t ch = 0;
-      for (int i = 0; i < nkb; ++i) {
-        const bool first = (i % kGChunkKB) == 0;
-        const bool last = (i % kGChunkKB) == kGChunkKB - 1 || i == nkb - 1;
-        const int b = ch % C::NACC;
+      int ch = 0;
+      for (int i = 0; i < nst; ++i) {
+        const bool first = i % C::CHUNK == 0, last = i % C::CHUNK == C::CHUNK - 1 || i == nst - 1;
+        const int b = ch % C::NACC, s = i % C::STAGES, g = i % kGGroups;
         if (first) ptx::mbar_wait(&tempty[b], ((ch / C::NACC) & 1) ^ 1);
-        const int s = i % C::STAGES, slot = i % C::NSLOT;
         ptx::mbar_wait(&ready[s], (i / C::STAGES) & 1);
         ptx::tc_fence_after();
-        const uint32_t bb = ptx::smem_u32(smem + s * C::TILE);
-        const uint32_t ta = tmem_base + C::ASLOT0 + slot * 32;
         const uint32_t d = tmem_base + b * NP;
+        const uint32_t ta = tmem_base + C::ASLOT0 + g * C::ASET;
 #pragma unroll
-        for (int ks = 0; ks < kGBK / 8; ++ks)
-          ptx::mma_tf32_ts(d, ta + ks * 8, ptx::umma_desc(bb + ks * 32, 16, 1024, 2), idesc,
-                           (first && ks == 0) ? 0u : 1u);
+        for (int j = 0; j < C::KPS; ++j) {
+          const uint32_t bb = ptx::smem_u32(smem + s * C::STAGE + j * C::TILE);
+#pragma unroll
+          for (int ks = 0; ks < kGBK / 8; ++ks)
+            ptx::mma_tf32_ts(d, ta + j * 32 + ks * 8, ptx::umma_desc(bb + ks * 32, 16, 1024, 2), idesc,
+                             (first && j == 0 && ks == 0) ? 0u : 1u);
+        }
         ptx::mma_commit(&empty[s]);
-        ptx::mma_commit(&aempty[slot]);
+        ptx::mma_commit(&aempty[g]);
         if (last) {
           ptx::mma_commit(&tfull[b]);
           ++ch;
         }
       }
     }
-  } else if (warp < 6) {
-    // ---------------- transform.  TMEM lane tl = 32 (warp & 3) + lane (the quarter a warp may access):
-    // lanes 0-63 take Hi of i-block row (tl & 63), lanes 64-127 its Lo.  Thread t also rewrites the B
-    // tile in place: 16-B chunk cc = t & 7 of rows t >> 3, t >> 3 + 16, ... become Hi (rows >= n: 0).
-    const int t = threadIdx.x - 64;
-    const int tl = 32 * (warp & 3) + lane;
-    const int arow = ib * 64 + (tl & 63);  // particle row (== row of the staged tile)
-    const bool want_lo = tl >= 64;
-    const int cc = t & 7;
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % C::STAGES, slot = i % C::NSLOT;
+  } else if (warp < kGEpi0) {
+    // ---------------- transform group g: stages g, g + kGGroups, ... into A set g.  Thread: TMEM lane
+    // 32q + lane = Hi or Lo of i-block row lane_row(q, lane); the Hi thread writes the row's Hi back in
+    // place (the B operand).  Rows of the tile outside the i-block (n > 64) are converted unit by unit.
+    const int g = (warp - kGXf0) >> 2, q = warp & 3, t = threadIdx.x - 32 * (kGXf0 + 4 * g);
+    const int arow = ib * 64 + lane_row(q, lane);
+    const bool want_lo = lane & 1;
+    const bool in_tile = arow < NP;
+    const bool live = arow < n;
+    const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + C::ASLOT0 + g * C::ASET;
+    for (int i = g; i < nst; i += kGGroups) {
+      const int s = i % C::STAGES;
       ptx::mbar_wait(&full[s], (i / C::STAGES) & 1);
-      ptx::mbar_wait(&aempty[slot], ((i / C::NSLOT) & 1) ^ 1);
+      ptx::mbar_wait(&aempty[g], ((i / kGGroups) & 1) ^ 1);
       ptx::tc_fence_after();
-      const uint32_t st = ptx::smem_u32(smem + s * C::TILE);
-      // c = raw row 0 (swizzle of row 0 is the identity), read before any in-place write
-      float cv[32];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 v = ptx::lds_f4(st + (q << 4));
-        cv[4 * q] = v.x; cv[4 * q + 1] = v.y; cv[4 * q + 2] = v.z; cv[4 * q + 3] = v.w;
-      }
-      uint32_t a[32];
-      if (arow < n) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 v = ptx::lds_f4(st + arow * 128 + ((q ^ (arow & 7)) << 4));
-          const float xv[4] = {v.x - cv[4 * q], v.y - cv[4 * q + 1], v.z - cv[4 * q + 2], v.w - cv[4 * q + 3]};
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float h = ptx::tf32_rna_fast(xv[u]);
-            a[4 * q + u] = __float_as_uint(want_lo ? xv[u] - h : h);
-          }
-        }
-      } else {
+      const uint32_t cs = ptx::smem_u32(cbuf + s * 512);
+#pragma unroll 1
+      for (int j = 0; j < C::KPS; ++j) {
+        const uint32_t st = ptx::smem_u32(smem + s * C::STAGE + j * C::TILE);
+        uint32_t a[32];
 #pragma unroll
         for (int k = 0; k < 32; ++k) a[k] = 0u;
-      }
-      ptx::tmem_st_32x32b_x32(tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + C::ASLOT0 + slot * 32, a);
-      float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f);  // chunk cc of c (no dynamic register indexing)
+        if (live) {
+          float4 v[8], cv[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q == cc) c4 = make_float4(cv[4 * q], cv[4 * q + 1], cv[4 * q + 2], cv[4 * q + 3]);
-      bar_transform();  // every raw read of the stage is done before the tile is overwritten
-#pragma unroll 4
-      for (int j = t >> 3; j < NP; j += 16) {
-        const uint32_t ad = st + j * 128 + ((cc ^ (j & 7)) << 4);
-        float4 v = ptx::lds_f4(ad);
-        if (j < n) {
-          v.x = ptx::tf32_rna_fast(v.x - c4.x);
-          v.y = ptx::tf32_rna_fast(v.y - c4.y);
-          v.z = ptx::tf32_rna_fast(v.z - c4.z);
-          v.w = ptx::tf32_rna_fast(v.w - c4.w);
-        } else {
-          v = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int u = 0; u < 8; ++u) {
+            cv[u] = ptx::lds_f4(cs + j * 128 + (u << 4));
+            v[u] = ptx::lds_f4(st + arow * 128 + ((u ^ (arow & 7)) << 4));
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float xv[4] = {v[u].x - cv[u].x, v[u].y - cv[u].y, v[u].z - cv[u].z, v[u].w - cv[u].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float h = ptx::tf32_rna_fast(xv[e]);
+              a[4 * u + e] = __float_as_uint(want_lo ? xv[e] - h : h);
+            }
+          }
         }
-        ptx::sts_f4(ad, v);
+        ptx::tmem_st_32x32b_x32(ta + j * 32, a);
+        __syncwarp();  // the Lo thread of the pair has read the raw row
+        if (!want_lo && in_tile) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            ptx::sts_f4(st + arow * 128 + ((u ^ (arow & 7)) << 4),
+                        make_float4(__uint_as_float(a[4 * u]), __uint_as_float(a[4 * u + 1]),
+                                    __uint_as_float(a[4 * u + 2]), __uint_as_float(a[4 * u + 3])));
+        }
+        if constexpr (C::OUTER > 0) {
+          float4 v[C::OUTER];
+          uint32_t ad[C::OUTER];
+          int rows[C::OUTER];
+#pragma unroll
+          for (int k = 0; k < C::OUTER; ++k) {
+            const int u = t + 128 * k, ro = u >> 3, cc = u & 7;
+            const int r = ro < ib * 64 ? ro : ro + 64;  // skip the i-block's own 64 rows
+            rows[k] = r;
+            ad[k] = st + r * 128 + ((cc ^ (r & 7)) << 4);
+            v[k] = ptx::lds_f4(ad[k]);
+          }
+#pragma unroll
+          for (int k = 0; k < C::OUTER; ++k) {
+            const float4 c4 = ptx::lds_f4(cs + j * 128 + ((t + 128 * k) & 7) * 16);
+            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (rows[k] < n)
+              o = make_float4(ptx::tf32_rna_fast(v[k].x - c4.x), ptx::tf32_rna_fast(v[k].y - c4.y),
+                              ptx::tf32_rna_fast(v[k].z - c4.z), ptx::tf32_rna_fast(v[k].w - c4.w));
+            ptx::sts_f4(ad[k], o);
+          }
+        }
       }
       ptx::tmem_st_wait();
       ptx::fence_proxy_async_smem();
@@ -201,16 +234,16 @@ __global__ void __launch_bounds__(kGThreads, 1)
     }
   } else {
     // ---------------- epilogue: quarter q of the 128 lanes, column half h
-    const int e = warp - 6, q = warp & 3, h = e >> 2;
+    const int e = warp - kGEpi0, q = warp & 3, h = e >> 2;
     if (h < C::EPI_SPLIT) {
       const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
       float acc[C::CW];
 #pragma unroll
       for (int j = 0; j < C::CW; ++j) acc[j] = 0.f;
-      const int nch = (nkb + kGChunkKB - 1) / kGChunkKB;
-      for (int ch = 0; ch < nch; ++ch) {
-        const int b = ch % C::NACC;
-        ptx::mbar_wait(&tfull[b], (ch / C::NACC) & 1);
+      const int nch = (nst + C::CHUNK - 1) / C::CHUNK;
+      for (int i = 0; i < nch; ++i) {
+        const int b = i % C::NACC;
+        ptx::mbar_wait(&tfull[b], (i / C::NACC) & 1);
         ptx::tc_fence_after();
 #pragma unroll
         for (int cb = 0; cb < C::CW; cb += 16) {
@@ -223,8 +256,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[b]);
       }
-      // [X; Y] block of (split, i-block): row r = TMEM lane, NP columns
-      float* dst = part + (((int64_t)split * n_ib + ib) * 128 + q * 32 + lane) * NP + h * C::CW;
+      // [X; Y] block of (split, i-block): X row r at r, Y row r at 64 + r; NP columns
+      const int prow = (lane & 1) * 64 + lane_row(q, lane);
+      float* dst = part + (((int64_t)split * n_ib + ib) * 128 + prow) * NP + h * C::CW;
 #pragma unroll
       for (int j = 0; j < C::CW; j += 4)
         *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
@@ -238,9 +272,12 @@ __global__ void __launch_bounds__(kGThreads, 1)
 template <int NP>
 push_status gram_launch(const float* theta, int64_t ld, int n, int splits, const int64_t* ranges, float* part,
                         cudaStream_t s) {
-  CUtensorMap map;
+  CUtensorMap map, cmap;
   push_status st = gemm::make_map(&map, theta, (uint64_t)ld, (uint64_t)n, 1, (uint64_t)ld, 0, NP,
                                   CU_TENSOR_MAP_SWIZZLE_128B);
+  if (st != PUSH_OK) return st;
+  st = gemm::make_map(&cmap, theta, (uint64_t)ld, 1, 1, (uint64_t)ld, 0, 1, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      kGBK * GCfg<NP>::KPS);
   if (st != PUSH_OK) return st;
   static bool attr = false;
   if (!attr) {
@@ -249,7 +286,7 @@ push_status gram_launch(const float* theta, int64_t ld, int n, int splits, const
     attr = true;
   }
   const int n_ib = (n + 63) / 64;
-  gram_partial_kernel<NP><<<dim3(splits, n_ib), kGThreads, GCfg<NP>::SMEM, s>>>(map, ranges, n, n_ib, part);
+  gram_partial_kernel<NP><<<dim3(splits, n_ib), kGThreads, GCfg<NP>::SMEM, s>>>(map, cmap, ranges, n, n_ib, part);
   PUSH_CUDA_TRY(cudaGetLastError());
   return PUSH_OK;
 }
@@ -301,66 +338,69 @@ push_status gram_partial(const float* theta, int64_t ld, int n, int splits, cons
   }
 }
 
-// D from the split partials.  A CTA covers 32 consecutive entries (i, j) of row i (lane = j); only
-// j > i is computed (written to (i, j) and (j, i)), the diagonal is +0.  Warp w sums the splits
-// s = w, w + 8, ... ascending, the 8 warp sums are added in ascending w (the order depends only on the
-// split count).  Per split: g_ij += (X(i,j) + Y(i,j)) + Y(j,i), g_aa += (X(a,a) + Y(a,a)) + Y(a,a).
-__global__ void __launch_bounds__(256) gram_dist_kernel(const float* __restrict__ part, int n, int np, int n_ib,
-                                                        int S, const RankSlots rs, float* __restrict__ D) {
-  __shared__ float red[3][8][33];
+// Sum of the split partials: sums[e] = sum_s part[slot(s)][e] over one partial block (e < pb).  A CTA
+// covers 32 consecutive elements (lane = element, coalesced), warp w sums s = w, w + 8, ... ascending with
+// 8 loads in flight, then the 8 warp sums are added in ascending w: the order depends only on S.
+__global__ void __launch_bounds__(256) gram_reduce_kernel(const float* __restrict__ part, int64_t pb, int S,
+                                                          const RankSlots rs, float* __restrict__ sums) {
+  __shared__ float red[8][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t e = (int64_t)blockIdx.x * 32 + lane;
-  const int64_t nn = (int64_t)n * n;
-  const bool ok = e < nn;
-  const int i = ok ? (int)(e / n) : 0, j = ok ? (int)(e - (int64_t)i * n) : 0;
-  const bool upper = ok && j > i;
-  if (!__syncthreads_or(upper)) {  // no entry above the diagonal: only the diagonal (if any) is written
-    if (warp == 0 && ok && i == j) D[e] = 0.f;
-    return;
-  }
-  const int64_t pb = (int64_t)n_ib * 128 * np;
-  // row offsets inside a split block: X row of particle a at ((a/64)*128 + a%64) * np, Y row 64 further
-  auto xrow = [&](int a) { return ((int64_t)(a >> 6) * 128 + (a & 63)) * np; };
-  const int64_t xi = xrow(i), xj = xrow(j);
-  float gij = 0.f, gii = 0.f, gjj = 0.f;
-  if (upper) {
+  float v = 0.f;
+  if (e < pb) {
     int q = 0;
-    for (int s = warp; s < S; s += 8) {
-      while (q + 1 < rs.P && s >= rs.s0[q + 1]) ++q;
-      const float* b = part + (int64_t)(q * rs.smax + s - rs.s0[q]) * pb;
-      const float x_ij = __ldg(b + xi + j), y_ij = __ldg(b + xi + 64 * np + j), y_ji = __ldg(b + xj + 64 * np + i);
-      const float x_ii = __ldg(b + xi + i), y_ii = __ldg(b + xi + 64 * np + i);
-      const float x_jj = __ldg(b + xj + j), y_jj = __ldg(b + xj + 64 * np + j);
-      gij += (x_ij + y_ij) + y_ji;
-      gii += (x_ii + y_ii) + y_ii;
-      gjj += (x_jj + y_jj) + y_jj;
+    for (int sb = warp; sb < S; sb += 64) {
+      float t[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int s = sb + 8 * k;
+        t[k] = 0.f;
+        if (s < S) {
+          while (q + 1 < rs.P && s >= rs.s0[q + 1]) ++q;
+          t[k] = __ldg(part + (int64_t)(q * rs.smax + s - rs.s0[q]) * pb + e);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (sb + 8 * k < S) v += t[k];
     }
   }
-  red[0][warp][lane] = gij;
-  red[1][warp][lane] = gii;
-  red[2][warp][lane] = gjj;
+  red[warp][lane] = v;
   __syncthreads();
-  if (warp == 0 && ok) {
-    if (i == j) {
-      D[e] = 0.f;
-    } else if (upper) {
-      float a = red[0][0][lane], b = red[1][0][lane], c = red[2][0][lane];
+  if (warp == 0 && e < pb) {
+    float r = red[0][lane];
 #pragma unroll
-      for (int w = 1; w < 8; ++w) {
-        a += red[0][w][lane];
-        b += red[1][w][lane];
-        c += red[2][w][lane];
-      }
-      const float d = fmaxf(fmaf(-2.0f, a, b + c), 0.f);
-      D[e] = d;
-      D[(int64_t)j * n + i] = d;
-    }
+    for (int w = 1; w < 8; ++w) r += red[w][lane];
+    sums[e] = r;
   }
 }
 
-void gram_dist(const float* part, int n, int S, const RankSlots& rs, float* D, cudaStream_t s) {
-  const int64_t groups = ((int64_t)n * n + 31) / 32;
-  gram_dist_kernel<<<(unsigned)groups, 256, 0, s>>>(part, n, gram_np(n), (n + 63) / 64, S, rs, D);
+// D_ij = D_ji = max(G_ii + G_jj - 2 G_ij, 0) for i < j, D_ii = +0, with G_ab = (SX_ab + SY_ab) + SY_ba
+// (SX / SY: the summed X / Y blocks; row a of i-block a/64 at (a/64)*128 + a%64, Y 64 rows further)
+__global__ void gram_d_kernel(const float* __restrict__ sums, int n, int np, float* __restrict__ D) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n * n) return;
+  const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
+  if (j < i) return;
+  if (i == j) {
+    D[e] = 0.f;
+    return;
+  }
+  auto xrow = [&](int a) { return ((int64_t)(a >> 6) * 128 + (a & 63)) * np; };
+  const int64_t xi = xrow(i), xj = xrow(j), yo = 64 * (int64_t)np;
+  const float gij = (sums[xi + j] + sums[xi + yo + j]) + sums[xj + yo + i];
+  const float gii = (sums[xi + i] + sums[xi + yo + i]) + sums[xi + yo + i];
+  const float gjj = (sums[xj + j] + sums[xj + yo + j]) + sums[xj + yo + j];
+  const float d = fmaxf(fmaf(-2.0f, gij, gii + gjj), 0.f);
+  D[e] = d;
+  D[(int64_t)j * n + i] = d;
+}
+
+void gram_dist(const float* part, int n, int S, const RankSlots& rs, float* sums, float* D, cudaStream_t s) {
+  const int64_t pb = gram_part_floats(n);
+  gram_reduce_kernel<<<(unsigned)((pb + 31) / 32), 256, 0, s>>>(part, pb, S, rs, sums);
+  const int64_t nn = (int64_t)n * n;
+  gram_d_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(sums, n, gram_np(n), D);
 }
 
 }  // namespace kern

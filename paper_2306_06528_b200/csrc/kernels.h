@@ -142,9 +142,9 @@ int64_t gram_part_floats(int n);    // floats of one split's partial block: ceil
 // pitch ld, centred on row 0); ranges_dev: the splits' [begin, end) column pairs relative to theta
 push_status gram_partial(const float* theta, int64_t ld, int n, int splits, const int64_t* ranges_dev, float* part,
                          cudaStream_t s);
-// D_ij = D_ji = max(G_ii + G_jj - 2 G_ij, 0), D_ii = +0, G summed over the S splits in ascending order
-// (split s's block at slot rs(s), as dist_reduce)
-void gram_dist(const float* part, int n, int S, const RankSlots& rs, float* D, cudaStream_t s);
+// sums = the S split blocks summed in ascending order (split s's block at slot rs(s), as dist_reduce;
+// gram_part_floats(n) floats), then D_ij = D_ji = max(G_ii + G_jj - 2 G_ij, 0), D_ii = +0 (two launches)
+void gram_dist(const float* part, int n, int S, const RankSlots& rs, float* sums, float* D, cudaStream_t s);
 
 // ---------------------------------------------------------------- a8 + a9 bandwidth and kernel matrix
 // Per tensor t (one CTA each): h_t from D_t (rule, c = fp32 1/ln n or 1/ln(n+1), or fixed bw_h);

@@ -72,7 +72,7 @@ struct Plan {
   bool gram = false;    // a7 as the centred symmetric Gram product (gram.cu); dist holds its split plan
   bool tc_update = false;  // a10 as the contraction [K, -rK] x [G; Theta] on the tensor cores
   // byte offsets into the workspace
-  size_t o_ulhs = 0;
+  size_t o_ulhs = 0, o_gsum = 0;
   size_t o_theta0, o_theta1, o_grad, o_whi, o_wlo, o_dlt0, o_dlt1, o_err2, o_loss, o_loss_all, o_opw, o_opb,
       o_xpart, o_dpart, o_D, o_K, o_s, o_h, o_xbuf, o_ybuf, o_pred, o_swag_mean, o_swag_sq, o_dranges, o_useg,
       o_pth, o_pg, o_pth2, o_pack_th, o_pack_g;
@@ -282,6 +282,7 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.o_dpart = take((int64_t)(P.ds ? world * P.ds_smax : P.dist.splits) *
                    (P.gram ? kern::gram_part_floats(P.n) : (int64_t)P.n * P.n));
   P.o_ulhs = take(P.tc_update ? (int64_t)P.nl * 2 * P.n : 1);
+  P.o_gsum = take(P.gram ? kern::gram_part_floats(P.n) : 1);
   P.o_D = take((int64_t)P.tensors * P.n * P.n);
   P.o_K = take((int64_t)P.tensors * (P.ds ? P.n : P.nl) * P.n);  // d-sharded: K of all n rows
   P.o_s = take((int64_t)P.tensors * (P.ds ? P.n : P.nl));
@@ -347,6 +348,7 @@ struct push_ctx {
   std::vector<float*> wpart, tpart, bpart;  // per layer
   float *opw = nullptr, *opb = nullptr, *xpart = nullptr;
   float *dpart = nullptr, *D = nullptr, *K = nullptr, *srow = nullptr, *h = nullptr;
+  float* gsum = nullptr;  // Gram form: the split partials summed
   float* ulhs = nullptr;  // tensor-core update: [K, -rK] or [-rK, K] (n_local x 2n)
   int64_t* dranges = nullptr;  // distance split ranges (device copy of P.dist.ranges)
   int4* useg = nullptr;        // variant update segments (device copy of P.useg)
@@ -782,7 +784,7 @@ static push_status ds_phase2(push_ctx* c, cudaStream_t s) {
   }
   st = run_k(c, PC_DIST, 1, 4.0 * P.n * P.n * (double)P.dist.splits, 0, s, [&] {
     if (P.gram)
-      kern::gram_dist(c->dpart, P.n, P.dist.splits, c->slots, c->D, s);
+      kern::gram_dist(c->dpart, P.n, P.dist.splits, c->slots, c->gsum, c->D, s);
     else
       kern::dist_reduce(c->dpart, P.n, P.dist, c->slots, c->D, s);
     return PUSH_OK;
@@ -859,7 +861,7 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
     st = run_k(c, PC_DIST, 2, nd4, 2.0 * P.n * (double)P.n * P.ld, s, [&]() -> push_status {
       push_status g = kern::gram_partial(th, P.ld, P.n, P.dist.splits, c->dranges, c->dpart, s);
       if (g != PUSH_OK) return g;
-      kern::gram_dist(c->dpart, P.n, P.dist.splits, c->slots, c->D, s);
+      kern::gram_dist(c->dpart, P.n, P.dist.splits, c->slots, c->gsum, c->D, s);
       return PUSH_OK;
     });
   } else {
@@ -1018,6 +1020,7 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   c->loss_all = F(P.o_loss_all);
   c->dpart = F(P.o_dpart);
   c->D = F(P.o_D);
+  c->gsum = F(P.o_gsum);
   c->K = F(P.o_K);
   c->srow = F(P.o_s);
   c->h = F(P.o_h);
