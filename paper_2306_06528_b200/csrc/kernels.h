@@ -158,9 +158,11 @@ void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c
 int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl, const float* K,
                 const float* srow, const float* h, float eps_over_n, float* theta_next, cudaStream_t s);
 int update_row_block(int n, int nl, int64_t ld);
-// Tensor-core update (n_local >= 32): lhs [nl][2n] = [K, -rK] (g_first) or [-rK, K], r = 2/h; then
-// theta_next[i][c] = theta[i][c] + eps_n (U[i][c] + r s_i theta[i][c]) with U already in theta_next
-void update_lhs(const float* K, int nl, int n, const float* h, bool g_first, float* lhs, cudaStream_t s);
+// Tensor-core update (push_api update_tc): lhs [nl][2n] = [K, -rK] (g_first) or [-rK, K], r = 2/h, rows at
+// `pitch` (>= 2n, a multiple of 4), npad >= nl rows (the padding is zeroed); the GEMM writes
+// U = lhs [G; Theta] into theta_next, then theta_next[i][c] = theta[i][c] + eps_n (U[i][c] + r s_i theta[i][c])
+void update_lhs(const float* K, int nl, int npad, int n, int pitch, const float* h, bool g_first, float* lhs,
+                cudaStream_t s);
 void update_fixup(const float* theta_own, int64_t ld, int nl, const float* srow, const float* h, float eps_n,
                   float* next_own, cudaStream_t s);
 // NEXT-2 variants: column segments of <= kVarSegCols columns inside one tensor (x = begin, y = end, z = tensor)

@@ -892,20 +892,26 @@ int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int ro
 }
 
 // ---------------------------------------------------------------- a10 on the tensor cores (n_local >= 32)
-__global__ void update_lhs_kernel(const float* __restrict__ K, int nl, int n, const float* __restrict__ hptr,
-                                  int g_first, float* __restrict__ lhs) {
+__global__ void update_lhs_kernel(const float* __restrict__ K, int nl, int npad, int n, int pitch,
+                                  const float* __restrict__ hptr, int g_first, float* __restrict__ lhs) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)nl * 2 * n) return;
-  const int i = (int)(e / (2 * n)), q = (int)(e - (int64_t)i * 2 * n);
+  if (e >= (int64_t)npad * pitch) return;
+  const int i = (int)(e / pitch), q = (int)(e - (int64_t)i * pitch);
+  if (q >= 2 * n || i >= nl) {  // padding rows (to a multiple of 32) and columns (to a 16-B pitch): zero
+    lhs[e] = 0.f;
+    return;
+  }
   const int j = q < n ? q : q - n;
   const bool gpart = (q < n) == (g_first != 0);
   const float k = K[(int64_t)i * n + j];
   lhs[e] = gpart ? k : -(2.0f / *hptr) * k;
 }
-void update_lhs(const float* K, int nl, int n, const float* h, bool g_first, float* lhs, cudaStream_t s) {
-  const int64_t tot = (int64_t)nl * 2 * n;
-  update_lhs_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(K, nl, n, h, g_first ? 1 : 0, lhs);
+void update_lhs(const float* K, int nl, int npad, int n, int pitch, const float* h, bool g_first, float* lhs,
+                cudaStream_t s) {
+  const int64_t tot = (int64_t)npad * pitch;
+  update_lhs_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(K, nl, npad, n, pitch, h, g_first ? 1 : 0, lhs);
 }
+
 __global__ void update_fixup_kernel(const float* __restrict__ th, int64_t ld4, const float* __restrict__ srow,
                                     const float* __restrict__ hptr, float eps_n, float* __restrict__ next) {
   const int i = blockIdx.y;

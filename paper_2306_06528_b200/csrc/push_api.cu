@@ -47,6 +47,7 @@ struct LayerPlan {
   int wsplit_max = 1;            // weight-gradient split count at max_batch (partial buffer size)
 };
 
+constexpr int kTcUpdateMinN = 128;  // a10 on the tensor cores from this many particles (measured crossover)
 constexpr int kMaxX0 = 4;  // thin first layer whose weight grads are fused into layer 1's BWD epilogue
 
 struct Plan {
@@ -224,13 +225,14 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
     P.dist = kern::gram_plan(P.n, P.ld);
     P.gram = true;
   }
-  // Many particles (n >= 128, e.g. C4 at n_local = n = 256): a10 is FP32-issue bound on the CUDA cores
-  // (2 n_local flops per streamed element); as a GEMM (M = n_local, N = ld, K = 2n) plus an elementwise
-  // pass it is memory-bound (C4 a10 0.060 -> 0.033 ms).  At n_local = n = 64 (C3, S1) the staged CUDA-core
-  // kernel measured faster (1.19 vs 1.32 ms at C3: the GEMM output and the fix-up pass add 3 n_local ld
-  // floats of traffic), so it keeps those.  2n % 4 == 0 for the K-major left operand.
-  // The choice depends on n only (never on n_local), so every sharding takes the same path (P-invariance).
-  P.tc_update = !P.ds && c->variant == 0 && P.n >= 128 && P.n % 2 == 0 && P.ld % 128 == 0;
+  // Many particles (n >= kTcUpdateMinN, e.g. C4 at n = 256): a10 is FP32-issue bound on the CUDA cores
+  // (2 n_local flops per streamed element); as the contraction U = [K, -rK] [G; Theta] on the tensor
+  // cores (3xTF32, K = 2n) plus an elementwise pass it is memory-bound (C4 a10 0.060 -> 0.033 ms).  At
+  // n = 64 (C3, S1) the staged CUDA-core kernel measured faster (1.19 vs 1.32 ms at C3; fusing the fix-up
+  // into a transposed GEMM epilogue measured slower still, 2.3 ms), so it keeps those.  The choice
+  // depends on n only (never on n_local or the exchange mode), so every sharding and the d-sharded
+  // panels take the same arithmetic (P-invariance).
+  P.tc_update = c->variant == 0 && P.n >= kTcUpdateMinN && P.ld % 128 == 0;
   if (P.ds) {
     const int S = P.dist.splits;
     for (int q = 0; q <= world; ++q) P.ds_s0.push_back((int)((int64_t)q * S / world));
@@ -281,14 +283,16 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.o_xpart = take(P.fuse_x0 ? (int64_t)P.RB * P.nl * P.layers[0].out * P.layers[0].in : 1);
   P.o_dpart = take((int64_t)(P.ds ? world * P.ds_smax : P.dist.splits) *
                    (P.gram ? kern::gram_part_floats(P.n) : (int64_t)P.n * P.n));
-  P.o_ulhs = take(P.tc_update ? (int64_t)P.nl * 2 * P.n : 1);
+  P.o_ulhs = take(P.tc_update ? (int64_t)(P.ds ? P.n : P.nl) * round_up(2 * P.n, 4) : 1);
   P.o_gsum = take(P.gram ? kern::gram_part_floats(P.n) : 1);
   P.o_D = take((int64_t)P.tensors * P.n * P.n);
   P.o_K = take((int64_t)P.tensors * (P.ds ? P.n : P.nl) * P.n);  // d-sharded: K of all n rows
   P.o_s = take((int64_t)P.tensors * (P.ds ? P.n : P.nl));
   const int64_t pan = P.ds ? (int64_t)P.n * P.ds_wmax : 1;  // column panels (n x w) and send/recv staging
-  P.o_pth = take(pan);
-  P.o_pg = take(pan);
+  // [Theta panel (even steps); G panel; Theta panel (odd steps)] at the own pitch: the tensor-core update's
+  // 2n x w operand in the same row order as the all-gather path's Theta[0], G, Theta[1] (bit-identity)
+  P.o_pth = take(3 * pan);
+  P.o_pg = take(1);
   P.o_pth2 = take(pan);
   P.o_pack_th = take(pan);
   P.o_pack_g = take(pan);
@@ -357,7 +361,7 @@ struct push_ctx {
   int64_t ds_w = 0, ds_c = 0;
   push::kern::DistPlan dist_own;
   push::kern::RankSlots slots{};
-  float *pth = nullptr, *pg = nullptr, *pth2 = nullptr, *pack_th = nullptr, *pack_g = nullptr;
+  float *pbase = nullptr, *pg = nullptr, *pth2 = nullptr, *pack_th = nullptr, *pack_g = nullptr;  // pg = pbase + n w
   bool ds_deferred = false;  // local group: this rank's step runs in the last rank's call
   float *xbuf = nullptr, *ybuf = nullptr;
   float* pred = nullptr;  // predictive pushforward: n x B x d_out (own rows, then all-gathered)
@@ -713,6 +717,30 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
 //   3  transpose back: panel rows of rank r -> r's next Theta buffer, columns of q
 // Every element sees the same splits, sums and update arithmetic as the all-gather path: results are
 // bit-identical for every P.
+// a10 on the tensor cores (P.tc_update): U = lhs B with lhs = [K, -rK] (g_first) or [-rK, K] (`rows` rows
+// of K) and B = the 2n x w operand at `b` (pitch w, MN-major: [G; Theta] when g_first, else [Theta; G]),
+// written into `out`, then out[i] = own[i] + eps_n (U_i + r s_i own[i]) (update_fixup; pitch w).
+static push_status update_tc(push_ctx* c, const float* b, bool g_first, int64_t w, int rows, const float* K,
+                             const float* srow, const float* own, float* out, float eps_n, cudaStream_t s) {
+  const Plan& P = c->P;
+  if (w == 0) return PUSH_OK;
+  const int pitch = (int)round_up(2 * P.n, 4);
+  kern::update_lhs(K, rows, rows, P.n, pitch, c->h, g_first, c->ulhs, s);
+  gemm::Problem pb;
+  pb.M = rows; pb.N = (int)w; pb.K = 2 * P.n; pb.batch = 1; pb.splits = 1; pb.passes = 3;
+  pb.A = gemm::Operand{c->ulhs, nullptr, true, false, pitch, 0};
+  pb.B = gemm::Operand{b, nullptr, true, true, w, 0};
+  pb.epi = gemm::EPI_STORE; pb.no_pair = true;
+  pb.out = out; pb.ldo = w; pb.out_pstride = (int64_t)rows * w;
+  push_status st = gemm::run(pb, s);
+  if (st != PUSH_OK) return st;
+  kern::update_fixup(own, w, rows, srow, c->h, eps_n, out, s);
+  return PUSH_OK;
+}
+
+// the d-sharded Theta panel of the current step (n x w at the own pitch; see Plan.o_pth)
+static float* pan_theta(push_ctx* c) { return c->pbase + (c->cur ? 2 : 0) * (int64_t)c->P.n * c->ds_w; }
+
 static push_status ds_phase1(push_ctx* c, cudaStream_t s) {
   const Plan& P = c->P;
   const int W = c->world, nl = P.nl;
@@ -722,7 +750,7 @@ static push_status ds_phase1(push_ctx* c, cudaStream_t s) {
       for (int q = 0; q < W && wo > 0; ++q) {
         push_ctx* pc = c->group ? c->group->members[q] : c;
         const int64_t src = (int64_t)q * nl * ld + c->ds_c;
-        PUSH_CUDA_TRY(cudaMemcpy2DAsync(c->pth + (int64_t)q * nl * wo, wo * 4, pc->theta[c->cur] + src, ld * 4,
+        PUSH_CUDA_TRY(cudaMemcpy2DAsync(pan_theta(c) + (int64_t)q * nl * wo, wo * 4, pc->theta[c->cur] + src, ld * 4,
                                         wo * 4, nl, cudaMemcpyDeviceToDevice, s));
         PUSH_CUDA_TRY(cudaMemcpy2DAsync(c->pg + (int64_t)q * nl * wo, wo * 4, pc->grad + src, ld * 4, wo * 4, nl,
                                         cudaMemcpyDeviceToDevice, s));
@@ -746,7 +774,7 @@ static push_status ds_phase1(push_ctx* c, cudaStream_t s) {
       const int64_t dst = (int64_t)q * nl * P.ds_wmax;
       if (wq > 0 && e == PUSH_OK) e = nccl::send_f32(c->pack_th + dst, nl * wq, q, c->comm, s);
       if (wq > 0 && e == PUSH_OK) e = nccl::send_f32(c->pack_g + dst, nl * wq, q, c->comm, s);
-      if (wo > 0 && e == PUSH_OK) e = nccl::recv_f32(c->pth + (int64_t)q * nl * wo, nl * wo, q, c->comm, s);
+      if (wo > 0 && e == PUSH_OK) e = nccl::recv_f32(pan_theta(c) + (int64_t)q * nl * wo, nl * wo, q, c->comm, s);
       if (wo > 0 && e == PUSH_OK) e = nccl::recv_f32(c->pg + (int64_t)q * nl * wo, nl * wo, q, c->comm, s);
     }
     const push_status e2 = nccl::group_end();
@@ -756,10 +784,10 @@ static push_status ds_phase1(push_ctx* c, cudaStream_t s) {
   float* part = c->dpart + (int64_t)c->rank * P.ds_smax * part_block(P);
   if (P.gram)
     return run_k(c, PC_DIST, 1, 4.0 * P.n * wo, 2.0 * P.n * (double)P.n * wo, s, [&] {
-      return kern::gram_partial(c->pth, wo, P.n, c->dist_own.splits, c->dranges, part, s);
+      return kern::gram_partial(pan_theta(c), wo, P.n, c->dist_own.splits, c->dranges, part, s);
     });
   return run_k(c, PC_DIST, 1, 4.0 * P.n * wo, 3.0 * P.n * (double)P.n * wo / 2, s, [&] {
-    kern::dist_partial(c->pth, wo, P.n, c->dist_own, c->dranges, part, s);
+    kern::dist_partial(pan_theta(c), wo, P.n, c->dist_own, c->dranges, part, s);
     return PUSH_OK;
   });
 }
@@ -796,8 +824,12 @@ static push_status ds_phase2(push_ctx* c, cudaStream_t s) {
   });
   if (st != PUSH_OK || wo == 0) return st;
   const float eps_n = c->cfg.step_size / (float)P.n;
-  return run_k(c, PC_UPDATE, 1, 12.0 * P.n * (double)wo, 2.0 * P.n * (double)P.n * wo, s, [&] {
-    kern::svgd_update(c->pth, c->pg, wo, P.n, 0, P.n, c->K, c->srow, c->h, eps_n, c->pth2, s);
+  return run_k(c, PC_UPDATE, P.tc_update ? 3 : 1, 12.0 * P.n * (double)wo, 2.0 * P.n * (double)P.n * wo, s,
+               [&]() -> push_status {
+    float* pth = pan_theta(c);
+    if (P.tc_update)  // every row of the panel; [Theta; G] or [G; Theta] as the all-gather path at this parity
+      return update_tc(c, c->cur ? c->pg : pth, c->cur == 1, wo, P.n, c->K, c->srow, pth, c->pth2, eps_n, s);
+    kern::svgd_update(pth, c->pg, wo, P.n, 0, P.n, c->K, c->srow, c->h, eps_n, c->pth2, s);
     return PUSH_OK;
   });
 }
@@ -884,21 +916,10 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   st = run_k(c, PC_UPDATE, (var == 0 && P.tc_update) ? 3 : 1, 2.0 * nd4 + 4.0 * P.nl * (double)P.d,
              2.0 * P.nl * (double)P.n * P.d, s, [&] {
     if (var == 0 && P.tc_update) {
-      // U_i = sum_j K_ij g_j - r sum_j K_ij theta_j as one 3xTF32 GEMM over the adjacent [Theta; G] rows
-      // (written into theta_next), then theta'_i = theta_i + (eps/n)(U_i + r s_i theta_i)
-      const bool g_first = c->grad < th;  // layout Theta[0], G, Theta[1]
-      const float* bbase = g_first ? c->grad : th;
-      kern::update_lhs(c->K, P.nl, P.n, c->h, g_first, c->ulhs, s);
-      gemm::Problem pb;
-      pb.M = P.nl; pb.N = (int)P.ld; pb.K = 2 * P.n; pb.batch = 1; pb.splits = 1; pb.passes = 3;
-      pb.A = gemm::Operand{c->ulhs, nullptr, true, false, 2 * P.n, 0};
-      pb.B = gemm::Operand{bbase, nullptr, true, true, P.ld, 0};
-      pb.epi = gemm::EPI_STORE; pb.no_pair = true;
-      pb.out = next + (int64_t)c->row0 * P.ld; pb.ldo = P.ld; pb.out_pstride = (int64_t)P.nl * P.ld;
-      push_status g = gemm::run(pb, s);
-      if (g != PUSH_OK) return g;
-      kern::update_fixup(th + (int64_t)c->row0 * P.ld, P.ld, P.nl, c->srow, c->h, eps_n,
-                         next + (int64_t)c->row0 * P.ld, s);
+      // layout Theta[0], G, Theta[1]: [G; Theta_cur] or [Theta_cur; G] is one 2n x ld operand
+      const bool g_first = c->grad < th;
+      return update_tc(c, g_first ? c->grad : th, g_first, P.ld, P.nl, c->K, c->srow,
+                       th + (int64_t)c->row0 * P.ld, next + (int64_t)c->row0 * P.ld, eps_n, s);
     } else if (var == 0) {
       kern::svgd_update(th, c->grad, P.ld, P.n, c->row0, P.nl, c->K, c->srow, c->h, eps_n, next, s);
     } else {  // NEXT-2 (include/push.h PUSH_VAR_*): weights w_d = eps or eps/n, repulsion eps/n
@@ -1026,8 +1047,7 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   c->h = F(P.o_h);
   c->dranges = reinterpret_cast<int64_t*>(c->ws + P.o_dranges);
   c->useg = reinterpret_cast<int4*>(c->ws + P.o_useg);
-  c->pth = F(P.o_pth);
-  c->pg = F(P.o_pg);
+  c->pbase = F(P.o_pth);
   c->pth2 = F(P.o_pth2);
   c->pack_th = F(P.o_pack_th);
   c->pack_g = F(P.o_pack_g);
@@ -1040,6 +1060,7 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
     const int s0 = P.ds_s0[rank], s1 = P.ds_s0[rank + 1];
     c->ds_c = P.ds_c0[rank];
     c->ds_w = P.ds_c0[rank + 1] - P.ds_c0[rank];
+    c->pg = c->pbase + (int64_t)P.n * c->ds_w;
     c->dist_own.splits = s1 - s0;
     c->dist_own.ranges.clear();
     for (int k = 2 * s0; k < 2 * s1; ++k) c->dist_own.ranges.push_back(P.dist.ranges[k] - c->ds_c);

@@ -208,6 +208,26 @@ def test_loss_trajectory_c1_100_steps():
     assert ml[-1] < ml[0]
 
 
+@pytest.mark.parametrize("cfgname,steps", [("C2", 100), ("C4", 100), ("C5b", 5)])
+def test_loss_trajectory_free_running(cfgname, steps):
+    """Free-running loss trajectory (PAPER.md:661-664 loss tracking; north star: <= 1e-2 relative) of
+    the bench path (push_step_graph after the eager first call) against the oracle's own run from the
+    same K0 init and batches.  C5b (8 x 21M params) runs 5 steps: the fp64 oracle's update alone takes
+    ~20 s per step there."""
+    w = WORKLOADS[cfgname]
+    dims = list(w.dims)
+    ctx = push.Context(push.make_config(w.n_particles, dims, max_batch=w.batch, step_size=1e-3, seed=0))
+    th0 = ctx.gather("theta")
+    loss = torch.empty(w.n_particles, device="cuda")
+    losses = []
+    for t in range(steps):
+        x, y = synth.workload_batch(w, t)
+        ctx.step_graph(_dev(x), _dev(y), loss)
+        losses.append(loss.double().mean().item())
+    _, ml, _, _ = osvgd.svgd_run(th0, dims, lambda t: synth.workload_batch(w, t), steps, 1e-3)
+    np.testing.assert_allclose(np.array(losses), ml, rtol=1e-2)
+
+
 def test_step_host_equals_device_path():
     w = WORKLOADS["C1"]
     x, y = synth.workload_batch(w, 0)
@@ -326,9 +346,10 @@ def test_c2_full_size_sampled_parity():
     assert float(ctx.gather("h")[0]) == pytest.approx(info["h"], rel=1e-5)
 
 
-@pytest.mark.parametrize("cfgname", ["S1"])
+@pytest.mark.parametrize("cfgname", ["S1", "C3", "C5"])
 def test_full_size_sampled_parity_graph_path(cfgname):
-    """North-star point S1 (64 particles x 1,053,185 params, B = 8192) through the bench's launch path
+    """Full-size configs through the bench's launch path — S1 (north-star point, 64 x 1,053,185 params,
+    K = 512 GEMMs), C3 (64 x 3,153,921, K = 1024 GEMMs) and C5 (8 x 20,989,953, B = 1024, K = 2048 GEMMs)
     (push_step_graph after an eager warm-up step): g of sampled particles against the oracle one by one;
     D, h bit-compatible with the oracle's definition; theta' on sampled columns against the oracle's
     phi (column-separable) with the oracle's own K and h computed from the full Theta."""
@@ -346,6 +367,9 @@ def test_full_size_sampled_parity_graph_path(cfgname):
         assert inf_rel(g[i:i + 1], gref[None]) <= 1e-5, i
     D = osvgd.sq_dists(th0)
     h = osvgd.bandwidth(D)
+    Dg = ctx.gather("dist").astype(np.float64)
+    off = ~np.eye(w.n_particles, dtype=bool)
+    assert np.max(np.abs(Dg[off] - D[off]) / D[off]) <= 1e-5
     assert float(ctx.gather("h")[0]) == pytest.approx(h, rel=1e-5)
     K = osvgd.kernel_matrix(D, h)
     rng = np.random.default_rng(0)
