@@ -7,9 +7,12 @@ One step = one pass of the whole hot path: per-particl
 gradient of log p on the batch, Theta/G exchange (N > 1), pairwise distances, median
 bandwidth, kernel matrix and the fused SVGD update of every particle.
 
-Default workload: BASELINE.json configs[1] = C2 (16 particles, MLP 2-256x4-1, 8192 points
-of the 2-D advection field per batch) on one B200.  For N > 1 (torchrun, one rank per
-GPU, NCCL) the same n particles are sharded n/N per GPU (strong scaling).
+Default workload: S1, the north-star scaling point (64 particles x 1,053,185 parameters, MLP
+3-512x5-1, 8192 points of the Burgers field per batch), for N = 1 and
+N > 1 (the metric is quoted at 1/2/4/8 GPUs on this point).  `--config C2` gives
+BASELINE.json configs[1].  For N > 1 the same n particles are sharded n/N per GPU (strong
+scaling), one rank per GPU over NCCL: under torchrun, or launched by bench.py itself (it
+re-executes through torch.distributed.run when WORLD_SIZE is unset and --gpus N > 1).
 
 Timing: W untimed warm-up steps; K timed steps bracketed by barrier + synchronize, CUDA
 events on the launching stream, max over ranks.  The per-step working set (activations
@@ -39,6 +42,7 @@ from inputs import WORKLOADS, synth  # noqa: E402
 METRIC = "SVGD particle-steps/s and param-updates/s at 1/2/4/8 B200; % HBM/tensor roofline"
 UNIT = "particle-steps/s"
 TF32_OVER_BF16 = 1.1 / 2.25   # nominal dense tf32 / bf16 ratio (B200_PROFILING.md)
+DEFAULT_CONFIG = "S1"
 
 
 def load_peaks():
@@ -98,13 +102,100 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+def cublas_tf32_tflops(dev):
+    """Measured dense TF32 tensor throughput (cuBLAS 8192^3 fp32 matmul with TF32 allowed, best of 10):
+    context for the 3xTF32 roofline (the official peak stays bf16-measured x the nominal ratio)."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        a = torch.randn(8192, 8192, device=dev)
+        b = torch.randn(8192, 8192, device=dev)
+        for _ in range(3):
+            a @ b
+        best = 1e9
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(10):
+            e0.record()
+            a @ b
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2.0 * 8192 ** 3 / (best / 1e3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def allgather_busbw(w, ws, dev):
+    """NCCL all-gather bus bandwidth at this config's per-rank Theta / G block (n_local x ld floats), the
+    exchange's message size (SURVEY.md §8(d) NVLink row): busbw = algbw (P-1)/P, max time over ranks."""
+    import torch
+    import torch.distributed as dist
+    ld = (w.d + 127) // 128 * 128
+    cnt = (w.n_particles // ws) * ld
+    src = torch.zeros(cnt, device=dev)
+    dst = torch.empty(cnt * ws, device=dev)
+    for _ in range(3):
+        dist.all_gather_into_tensor(dst, src)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        dist.all_gather_into_tensor(dst, src)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / 10], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    algbw = 4.0 * cnt * ws / (ms / 1e3) / 1e9
+    return {"bytes_per_rank": 4 * cnt, "ms": ms, "algbw_gbs": algbw, "busbw_gbs": algbw * (ws - 1) / ws,
+            "how": "torch.distributed all_gather_into_tensor (NCCL), 10 iterations, max over ranks"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # ---------------------------------------------------------------------------- oracle baseline
-def cpu_baseline(w, budget_s: float = 20.0):
-    """Time the float64 oracle as it stands on the host cores on a bounded sample of the workload:
-    the gradient of k particles (k grown until ~budget/2) plus the full kernel/update phase once;
-    particle-steps/s = n / (n * t_grad_per_particle + t_update)."""
+def oracle_step_time(w, th, G, x, y, budget_s):
+    """Seconds of ONE full oracle step (oracle/ as it stands, float64 numpy) estimated from a bounded
+    sample: the gradients of the first k particles (k grown until ~budget/2; the per-particle cost is
+    identical) scaled by n/k, plus the kernel/update phase (distances, bandwidth, K, phi) on the first
+    m columns (m sized to ~budget/2; its cost is linear in the columns) scaled by d/m.
+    Returns (seconds, k, m)."""
     from oracle import mlp as omlp
     from oracle import svgd as osvgd
+    dims = list(w.dims)
+    t0 = time.perf_counter()
+    k = 0
+    while k < w.n_particles:
+        G[k], _ = omlp.grad_log_post(th[k], dims, x, y)
+        k += 1
+        if time.perf_counter() - t0 > budget_s / 2:
+            break
+    t_grad = (time.perf_counter() - t0) / k
+    d = th.shape[1]
+    m = min(d, 4096)
+    while True:
+        t1 = time.perf_counter()
+        osvgd.svgd_step(th[:, :m], G[:, :m], 1e-3)
+        t_upd = time.perf_counter() - t1
+        if m == d or t_upd > budget_s / 8:
+            break
+        m = min(d, m * 4)
+    return w.n_particles * t_grad + t_upd * d / m, k, m
+
+
+def cpu_baseline(w, budget_s: float = 20.0):
+    """The float64 oracle timed on the host cores on a bounded sample of the workload (oracle_step_time)."""
     try:
         from threadpoolctl import threadpool_info
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
@@ -114,52 +205,52 @@ def cpu_baseline(w, budget_s: float = 20.0):
     x, y = synth.workload_batch(w, 0)
     from oracle import init as oinit
     th = oinit.init_theta(w.n_particles, dims, 0).astype(np.float64)
-    t0 = time.perf_counter()
-    k = 0
     G = np.zeros_like(th)
-    while k < w.n_particles:
-        G[k], _ = omlp.grad_log_post(th[k], dims, x, y)
-        k += 1
-        if time.perf_counter() - t0 > budget_s / 2:
-            break
-    t_grad = (time.perf_counter() - t0) / k
-    t1 = time.perf_counter()
-    osvgd.svgd_step(th, G, 1e-3)
-    t_upd = time.perf_counter() - t1
-    per_step = w.n_particles * t_grad + t_upd
-    return {"value": w.n_particles / per_step, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{k} of {w.n_particles} particle gradients (B={w.batch}, float64 numpy) + one full "
-                      f"kernel/update phase; step time extrapolated as n*t_grad + t_update = {per_step:.2f} s"}
+    per_step, k, m = oracle_step_time(w, th, G, x, y, budget_s)
+    return {"value": w.n_particles / per_step, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(),
+            "nproc": os.cpu_count(), "kind": "oracle",
+            "sample": f"{k} of {w.n_particles} particle gradients (B={w.batch}) scaled by n/k, plus the kernel/"
+                      f"update phase on {m} of {w.d} columns scaled by d/m: one step = {per_step:.2f} s",
+            "c1_single_thread": c1_single_thread()}
+
+
+def c1_single_thread():
+    """the oracle also timed on ONE thread on C1 (4 particles, 1-32-32-1, 10 steps)."""
+    from oracle import init as oinit
+    from oracle import svgd as osvgd
+    w = WORKLOADS["C1"]
+    dims = list(w.dims)
+    th = oinit.init_theta(w.n_particles, dims, 0).astype(np.float64)
+    try:
+        from threadpoolctl import threadpool_limits
+        ctx = threadpool_limits(limits=1)
+    except Exception:
+        import contextlib
+        ctx = contextlib.nullcontext()
+    with ctx:
+        t0 = time.perf_counter()
+        osvgd.svgd_run(th, dims, lambda t: synth.workload_batch(w, t), 10, 1e-3)
+        dt = time.perf_counter() - t0
+    return {"value": w.n_particles * 10 / dt, "unit": UNIT, "cores": 1, "sample": "C1, 10 full oracle steps"}
 
 
 def run_reference(args, w):
+    """Reference arm (tier rules): the oracle as it stands on the host cores, each step a bounded sample
+    of the workload (oracle_step_time, ~4 s), on our arm's config / metric / unit."""
     rank, ws, _ = dist_env()
     if rank != 0:
         return
     from oracle import init as oinit
-    from oracle import mlp as omlp
-    from oracle import svgd as osvgd
     dims = list(w.dims)
     th = oinit.init_theta(w.n_particles, dims, 0).astype(np.float64)
-    # bounded sample per step: gradients of `k` particles + the full kernel/update phase
-    x, y = synth.workload_batch(w, 0)
-    t = time.perf_counter()
-    omlp.grad_log_post(th[0], dims, x, y)
-    t1 = time.perf_counter() - t
-    k = max(1, min(w.n_particles, int(6.0 / max(t1, 1e-6))))
-    times = []
     G = np.zeros_like(th)
+    times = []
+    k = m = 0
     for s in range(args.warmup + args.steps):
         xs, ys = synth.workload_batch(w, s)
-        t0 = time.perf_counter()
-        for i in range(k):
-            G[i], _ = omlp.grad_log_post(th[i], dims, xs, ys)
-        tg = (time.perf_counter() - t0) / k
-        t0 = time.perf_counter()
-        th, _ = osvgd.svgd_step(th, G, 1e-3)
-        tu = time.perf_counter() - t0
+        t, k, m = oracle_step_time(w, th, G, xs, ys, 4.0)
         if s >= args.warmup:
-            times.append(w.n_particles * tg + tu)
+            times.append(t)
     step = float(np.mean(times))
     try:
         from threadpoolctl import threadpool_info
@@ -172,9 +263,9 @@ def run_reference(args, w):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name + ": " + w.note, "n_particles": w.n_particles, "d": w.d,
                        "batch": w.batch},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"per step: {k} of {w.n_particles} particle gradients timed and scaled by n, "
-                                       f"plus the full kernel/update phase"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
+                             "sample": f"per step: {k} of {w.n_particles} particle gradients scaled by n/k plus "
+                                       f"the kernel/update phase on {m} of {w.d} columns scaled by d/m"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -263,6 +354,9 @@ def run_ours(args, w):
            "h2d_bytes_per_step": int(xs[0].numel() * 4 + ys[0].numel() * 4),
            "d2h_bytes_per_step": int(ctx.n_local * 4)}
 
+    ag = allgather_busbw(w, ws, dev) if ws > 1 else None
+    tf32_meas = cublas_tf32_tflops(dev) if rank == 0 else None
+
     if rank != 0:
         ctx.close()
         pdist.finalize(ws)
@@ -286,32 +380,27 @@ def run_ours(args, w):
             traffic_src = f"profiles/traffic_{w.name}.json ({tj.get('how', '')})"
     per_launch = max(dom["launches"], 1)
     if dom["name"].endswith("gemm"):
-        peak = peaks["bf16_tflops_sustained"] * TF32_OVER_BF16 / 3.0
+        # the profiled pass times the kernel inside a sub-second run at full clock: the BURST bf16 figure
+        # applies, converted to 3xTF32 useful flops by the guide's nominal tf32/bf16 ratio
+        peak = peaks["bf16_tflops"] * TF32_OVER_BF16 / 3.0
         ach = dom["alg_flops"] / (dom["ms"] / 1e3) / 1e12
         roof = {"bound": "tensor", "kernel": "gemm3xtf32 (" + dom["name"] + ")", "achieved": ach, "peak": peak,
                 "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic,
                 "algorithmic_per_launch": dom["alg_flops"] / per_launch,
-                "peak_note": f"{peak_kind} bf16 sustained x {TF32_OVER_BF16:.3f} (tf32/bf16 nominal) / 3 passes "
-                             "(3xTF32 useful flops)"}
-    else:
-        # FP32 CUDA-core peak: 148 SMs x 128 FP32 lanes x 2 flops (FMA) x the max SM clock
-        fp32_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        ridge = fp32_peak * 1e12 / (peaks["hbm_gbs"] * 1e9)  # flop per byte
-        if dom.get("alg_flops") and dom["alg_bytes"] and dom["alg_flops"] / dom["alg_bytes"] > ridge:
-            ach = dom["alg_flops"] / (dom["ms"] / 1e3) / 1e12
-            roof = {"bound": "alu", "kernel": dom["name"], "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
-                    "frac": ach / fp32_peak, "traffic": traffic,
-                    "algorithmic_per_launch": dom["alg_flops"] / per_launch,
-                    "peak_note": f"FP32 FMA issue: 148 SMs x 128 lanes x 2 x {peaks.get('sm_max_mhz', 1965.0):.0f} MHz "
-                                 f"(intensity {dom['alg_flops'] / dom['alg_bytes']:.1f} flop/B > ridge {ridge:.1f})"}
-        else:
-            peak = peaks["hbm_gbs"]
-            ach = dom["alg_bytes"] / (dom["ms"] / 1e3) / 1e9
-            roof = {"bound": "hbm", "kernel": dom["name"], "achieved": ach, "peak": peak, "unit": "GB/s",
-                    "frac": ach / peak, "traffic": traffic, "algorithmic_per_launch": dom["alg_bytes"] / per_launch,
-                    "peak_note": f"{peak_kind} hbm_gbs"}
+                "peak_note": f"{peak_kind} bf16 burst {peaks['bf16_tflops']:.1f} TF/s x {TF32_OVER_BF16:.3f} "
+                             "(tf32/bf16 nominal) / 3 products (3xTF32 useful flops); kernel timed in a "
+                             "sub-second pass at full clock"}
+        if tf32_meas:
+            roof["cublas_tf32_tflops_measured"] = tf32_meas
+            roof["frac_vs_cublas_tf32"] = ach / (tf32_meas / 3.0)
     if traffic_src:
         roof["traffic_note"] = "DRAM bytes per launch (read + write) from " + traffic_src
+    npath = os.path.join(ROOT, "profiles", f"ncu_{w.name}.json")
+    if os.path.exists(npath):  # ncu --set full summary of this config's step (scripts/ncu_summary.py --json)
+        with open(npath) as f:
+            nj = json.load(f)
+        if dom["name"] in nj.get("classes", {}):
+            roof["ncu"] = dict(nj["classes"][dom["name"]], source=f"profiles/ncu_{w.name}.json")
     all_gemm_ms = sum(r["ms"] for r in gemm_rows)
     all_gemm_fl = sum(r["alg_flops"] for r in gemm_rows)
     if all_gemm_ms:
@@ -338,6 +427,8 @@ def run_ours(args, w):
                        "launch": "eager" if args.no_graph else "cuda-graph (batch staged D2D into the context each step)"},
             "param_updates_per_s": value * w.d, "clocks": clk, "e2e": e2e,
             "gpu_launches": int(launches), "roofline": roof, "phases": phases}
+    if ag:
+        line["allgather"] = ag
     if ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w)
     print(json.dumps(line), flush=True)
@@ -345,12 +436,43 @@ def run_ours(args, w):
     pdist.finalize(ws)
 
 
+def self_launch(args):
+    """`python bench.py --gpus N` (N > 1) without a torchrun environment: re-execute this script under
+    torch.distributed.run with one rank per GPU (127.0.0.1 rendezvous).  Rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def run_dry(args, w):
+    """Launcher check without a GPU (tests/test_bench_launch.py): every rank joins a gloo process group,
+    the max-over-ranks reduction runs, rank 0 prints one JSON line."""
+    import torch.distributed as dist
+    rank, ws, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    from paper_2306_06528_b200 import dist as pdist
+    t = pdist.max_over_ranks(float(rank + 1), ws)
+    r0, nl = pdist.shard_rows(w.n_particles, ws, rank)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": ws, "ranks_max": t, "workload": w.name,
+                          "rows_rank0": [r0, nl]}), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(WORKLOADS))
+    ap.add_argument("--dry-run", action="store_true", help="launcher check on CPU (gloo), no GPU work")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of the captured CUDA graph")
@@ -360,12 +482,16 @@ def main():
     ap.add_argument("--variant", default="canonical", choices=["canonical", "paper"],
                     help="paper: PusH's own update (per-tensor kernel, 1/n on the repulsion, prior sum; NEXT-2)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     w = WORKLOADS[args.config]
     if args.n_particles:
         import dataclasses
         w = dataclasses.replace(w, n_particles=args.n_particles,
                                 note=f"{w.note} [n overridden to {args.n_particles}]")
-    if args.impl == "reference":
+    if args.dry_run:
+        run_dry(args, w)
+    elif args.impl == "reference":
         run_reference(args, w)
     else:
         run_ours(args, w)

@@ -23,6 +23,18 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v
          "--expt-relaxed-constexpr", "-DNDEBUG"]
 
 
+def nccl_include() -> list:
+    """nccl.h for the ncclConfig_t layout (types only: NCCL itself is dlopen'ed at run time)."""
+    try:
+        import nvidia.nccl
+        d = os.path.join(list(nvidia.nccl.__path__)[0], "include")
+        if os.path.exists(os.path.join(d, "nccl.h")):
+            return ["-I", d]
+    except Exception:
+        pass
+    return []
+
+
 def nvcc() -> str:
     for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
         if c and os.path.exists(c):
@@ -36,9 +48,9 @@ def sources():
 
 def _compile(src: str) -> str:
     obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-    cmd = [nvcc(), *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [nvcc(), *ARCH, *FLAGS, *nccl_include(), "-c", src, "-o", obj]
     if src.endswith(".cpp"):
-        cmd = [nvcc(), "-x", "cu", *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmd = [nvcc(), "-x", "cu", *ARCH, *FLAGS, *nccl_include(), "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

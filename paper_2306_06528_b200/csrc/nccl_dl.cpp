@@ -4,6 +4,7 @@
 #include "nccl_dl.h"
 
 #include <dlfcn.h>
+#include <nccl.h>  // types only (ncclConfig_t, NCCL_CONFIG_INITIALIZER); every call goes through dlsym
 
 #include <mutex>
 #include <string>
@@ -22,6 +23,9 @@ using FnSend = Result (*)(const void*, size_t, int, int, Comm, cudaStream_t);
 using FnRecv = Result (*)(void*, size_t, int, int, Comm, cudaStream_t);
 using FnGroup = Result (*)();
 using FnGetErrorString = const char* (*)(Result);
+using FnCommInitRankConfig = Result (*)(Comm*, int, UniqueId, int, ncclConfig_t*);
+using FnCommCount = Result (*)(Comm, int*);
+using FnGetAsyncError = Result (*)(Comm, Result*);
 
 struct Api {
   void* h = nullptr;
@@ -34,6 +38,9 @@ struct Api {
   FnRecv recv = nullptr;
   FnGroup group_start = nullptr, group_end = nullptr;
   FnGetErrorString err = nullptr;
+  FnCommInitRankConfig init_config = nullptr;
+  FnCommCount count = nullptr;
+  FnGetAsyncError async_err = nullptr;
   std::string why;
 };
 Api g_api;
@@ -68,6 +75,9 @@ push_status load() {
     g_api.recv = reinterpret_cast<FnRecv>(dlsym(h, "ncclRecv"));
     g_api.group_start = reinterpret_cast<FnGroup>(dlsym(h, "ncclGroupStart"));
     g_api.group_end = reinterpret_cast<FnGroup>(dlsym(h, "ncclGroupEnd"));
+    g_api.init_config = reinterpret_cast<FnCommInitRankConfig>(dlsym(h, "ncclCommInitRankConfig"));
+    g_api.count = reinterpret_cast<FnCommCount>(dlsym(h, "ncclCommCount"));
+    g_api.async_err = reinterpret_cast<FnGetAsyncError>(dlsym(h, "ncclCommGetAsyncError"));
     if (!g_api.get_unique_id || !g_api.comm_init_rank || !g_api.all_gather || !g_api.comm_destroy || !g_api.send ||
         !g_api.recv || !g_api.group_start || !g_api.group_end)
       g_api.why = "libnccl.so.2 lacks required symbols";
@@ -83,11 +93,31 @@ push_status get_unique_id(UniqueId* id) {
   return r ? nfail("ncclGetUniqueId", r) : PUSH_OK;
 }
 
-push_status comm_init_rank(Comm* comm, int nranks, const UniqueId& id, int rank) {
+push_status comm_init_rank(Comm* comm, int nranks, const UniqueId& id, int rank, int max_ctas) {
   push_status st = load();
   if (st != PUSH_OK) return st;
+  if (max_ctas > 0 && g_api.init_config) {
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.maxCTAs = max_ctas;
+    Result r = g_api.init_config(comm, nranks, id, rank, &cfg);
+    return r ? nfail("ncclCommInitRankConfig", r) : PUSH_OK;
+  }
   Result r = g_api.comm_init_rank(comm, nranks, id, rank);
   return r ? nfail("ncclCommInitRank", r) : PUSH_OK;
+}
+
+push_status comm_count(Comm comm, int* count) {
+  if (!g_api.count) return fail(PUSH_E_NCCL, "ncclCommCount not available");
+  Result r = g_api.count(comm, count);
+  return r ? nfail("ncclCommCount", r) : PUSH_OK;
+}
+
+push_status async_error(Comm comm) {
+  if (!comm || !g_api.async_err) return PUSH_OK;
+  Result e = 0;
+  Result r = g_api.async_err(comm, &e);
+  if (r) return nfail("ncclCommGetAsyncError", r);
+  return e ? nfail("NCCL asynchronous error", e) : PUSH_OK;
 }
 
 push_status allgather_f32(const float* send, float* recv, size_t count, Comm comm, cudaStream_t s) {

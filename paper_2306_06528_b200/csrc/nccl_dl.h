@@ -15,7 +15,13 @@ using Comm = void*;
 
 push_status load();
 push_status get_unique_id(UniqueId* id);
-push_status comm_init_rank(Comm* comm, int nranks, const UniqueId& id, int rank);
+// ncclCommInitRankConfig with maxCTAs = max_ctas (NCCL 2.28 config struct): caps the SMs the collectives
+// take from the concurrently running GEMMs (the Theta all-gather overlaps the gradient phase)
+push_status comm_init_rank(Comm* comm, int nranks, const UniqueId& id, int rank, int max_ctas = 0);
+// ncclCommCount (the communicator's rank count, checked against world_size after init)
+push_status comm_count(Comm comm, int* count);
+// ncclCommGetAsyncError: PUSH_OK, or PUSH_E_NCCL with the error text (a failed or aborted peer)
+push_status async_error(Comm comm);
 // in-place when send == recv + rank*count
 push_status allgather_f32(const float* send, float* recv, size_t count, Comm comm, cudaStream_t s);
 // grouped point-to-point (the NEXT-4 all-to-all transposes): group_start; send/recv ...; group_end

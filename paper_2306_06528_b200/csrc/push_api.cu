@@ -7,7 +7,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -47,6 +50,7 @@ struct LayerPlan {
   int wsplit_max = 1;            // weight-gradient split count at max_batch (partial buffer size)
 };
 
+constexpr int kNcclMaxCtas = 16;    // SMs the NCCL collectives may take while the GEMMs run (ncclConfig maxCTAs)
 constexpr int kTcUpdateMinN = 128;  // a10 on the tensor cores from this many particles (measured crossover)
 constexpr int kMaxX0 = 4;  // thin first layer whose weight grads are fused into layer 1's BWD epilogue
 
@@ -377,7 +381,7 @@ struct push_ctx {
   std::shared_ptr<push::LocalGroup> group;
   // comm stream: the Theta all-gather (a6/C1) runs beside the gradient kernels (P > 1)
   cudaStream_t comm_stream = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_theta = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_theta = nullptr, ev_fork2 = nullptr, ev_grad = nullptr;
   bool theta_pending = false;
   // CUDA-graph replay of a whole step (push_step_graph): one executable per Theta buffer parity
   struct GraphEntry {
@@ -885,8 +889,14 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   push_status st;
   if (P.ds) return ds_group_step({c}, s);  // NCCL ranks (or one rank): three collective phases
   if ((st = join_theta(c, s)) != PUSH_OK) return st;  // the Theta all-gather started by the gradient call
-  // C2: g rows of every rank
-  if ((st = exchange(c, BUF_GRAD, s)) != PUSH_OK) return st;
+  // C2: g rows of every rank, on the comm stream while a7-a9 (which read Theta only) run; joined before a10
+  const bool xg = c->world > 1 || c->comm;
+  if (xg) {
+    PUSH_CUDA_TRY(cudaEventRecord(c->ev_fork2, s));
+    PUSH_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_fork2, 0));
+    if ((st = exchange(c, BUF_GRAD, c->comm_stream)) != PUSH_OK) return st;
+    PUSH_CUDA_TRY(cudaEventRecord(c->ev_grad, c->comm_stream));
+  }
   const float* th = c->theta[c->cur];
   const double nd4 = 4.0 * P.n * (double)P.d;
   if (P.gram) {
@@ -910,6 +920,7 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
     return PUSH_OK;
   });
   if (st != PUSH_OK) return st;
+  if (xg) PUSH_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_grad, 0));  // G rows of every rank have landed
   const float eps_n = c->cfg.step_size / (float)P.n;
   float* next = c->theta[c->cur ^ 1];
   const int var = c->cfg.variant;
@@ -995,7 +1006,42 @@ static push_status check_ctx(push_ctx* c) {
   if (!c) return fail(PUSH_E_INVALID, "ctx is NULL");
   if (c->broken) return fail(PUSH_E_STATE, "context is in a failed state after an earlier CUDA/NCCL error");
   cudaSetDevice(c->device);
+  if (c->comm) {  // a failed or aborted peer surfaces here (re-raised at the next call)
+    push_status st = nccl::async_error(c->comm);
+    if (st != PUSH_OK) {
+      c->broken = true;
+      return st;
+    }
+  }
   return PUSH_OK;
+}
+
+// Host wait on `s` that polls the NCCL communicator while it waits: a dead or failed peer would otherwise
+// block cudaStreamSynchronize forever.  On an asynchronous NCCL error, or after kSyncTimeoutS without
+// progress, the communicator is aborted (its kernels are released) and the context turns broken.
+constexpr double kSyncTimeoutS = 600.0;
+static push_status wait_stream(push_ctx* c, cudaStream_t s) {
+  if (!c->comm) {
+    PUSH_CUDA_TRY(cudaStreamSynchronize(s));
+    return PUSH_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return PUSH_OK;
+    if (q != cudaErrorNotReady) return fail(PUSH_E_CUDA, std::string("stream: ") + cudaGetErrorString(q));
+    push_status st = nccl::async_error(c->comm);
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (st == PUSH_OK && dt > kSyncTimeoutS)
+      st = fail(PUSH_E_NCCL, "no progress for " + std::to_string((int)kSyncTimeoutS) + " s (peer lost?)");
+    if (st != PUSH_OK) {
+      c->broken = true;
+      nccl::comm_release(c->comm, true);  // ncclCommAbort: unblocks the pending collectives
+      c->comm = nullptr;
+      return st;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
 }
 
 static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int world, void* ws, size_t ws_bytes,
@@ -1085,6 +1131,8 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   PUSH_CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
   PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_theta, cudaEventDisableTiming));
+  PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming));
+  PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_grad, cudaEventDisableTiming));
   cudaStream_t s = nullptr;
   const size_t nld = (size_t)P.n * P.ld;
   PUSH_CUDA_TRY(cudaMemsetAsync(c->theta[0], 0, nld * 4, s));
@@ -1166,7 +1214,16 @@ push_status push_init(const push_config* cfg, int32_t rank, int32_t world_size, 
   if (st == PUSH_OK && world_size > 1) {
     nccl::UniqueId u;
     std::memcpy(u.internal, nccl_id, 128);
-    st = nccl::comm_init_rank(&c->comm, world_size, u, rank);
+    st = nccl::comm_init_rank(&c->comm, world_size, u, rank, kNcclMaxCtas);
+    int cnt = 0;
+    if (st == PUSH_OK) st = nccl::comm_count(c->comm, &cnt);
+    if (st == PUSH_OK && cnt != world_size)
+      st = fail(PUSH_E_NCCL, "NCCL communicator has " + std::to_string(cnt) + " ranks, expected " +
+                                 std::to_string(world_size));
+    if (st == PUSH_OK)
+      fprintf(stderr, "libpush_b200: NCCL communicator rank %d of %d (nranks %d, maxCTAs %d, device %d)\n", rank,
+              world_size, cnt, kNcclMaxCtas, c->device);
+    if (st != PUSH_OK && c->comm) nccl::comm_release(c->comm, true), c->comm = nullptr;
   } else if (st == PUSH_OK && force_nccl()) {
     // test hook (PUSH_FORCE_NCCL=1): a single-rank NCCL communicator, so that one GPU exercises the
     // NCCL exchange path (comm stream, in-place all-gathers, graph capture of NCCL calls)
@@ -1367,9 +1424,7 @@ push_status push_step_host(push_ctx* c, const float* x_host, const float* y_host
     cudaError_t e = cudaMemcpyAsync(loss_host, c->loss, 4 * c->P.nl, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
   }
-  cudaError_t e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return sticky(c, fail(PUSH_E_CUDA, cudaGetErrorString(e)));
-  return PUSH_OK;
+  return sticky(c, wait_stream(c, s));
 }
 
 push_status push_predict(push_ctx* c, const float* x_dev, int32_t B, float* pred_dev, float* mean_dev, float* std_dev,
@@ -1456,10 +1511,7 @@ push_status push_gather(push_ctx* c, int32_t what, float* out_host, void* stream
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if ((st = join_theta(c, s)) != PUSH_OK) return sticky(c, st);
   const Plan& P = c->P;
-  auto sync = [&]() -> push_status {
-    PUSH_CUDA_TRY(cudaStreamSynchronize(s));
-    return PUSH_OK;
-  };
+  auto sync = [&]() -> push_status { return wait_stream(c, s); };
   switch (what) {
     case PUSH_WHAT_THETA:
     case PUSH_WHAT_GRAD: {
@@ -1558,6 +1610,8 @@ push_status push_destroy(push_ctx* c) {
     if (gph.exec) cudaGraphExecDestroy(gph.exec);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_theta) cudaEventDestroy(c->ev_theta);
+  if (c->ev_fork2) cudaEventDestroy(c->ev_fork2);
+  if (c->ev_grad) cudaEventDestroy(c->ev_grad);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
