@@ -174,7 +174,7 @@ __device__ __forceinline__ float4 load_bias4(const KParams& prm, int lane, int c
   }
   return b;
 }
-template <int CW, int EPI>
+template <int CW, int EPI, int ACT>
 __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& prm, const CUtensorMap* tOut,
                                          const CUtensorMap* tAux, uint64_t* auxbar, uint32_t& aux_ph,
                                          uint32_t ebuf_s, int lane, int row0, int colw, int p, int pz,
@@ -226,10 +226,10 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
               const float4 bv = make_float4(__shfl_sync(0xffffffffu, bias4.x, src), __shfl_sync(0xffffffffu, bias4.y, src),
                                             __shfl_sync(0xffffffffu, bias4.z, src), __shfl_sync(0xffffffffu, bias4.w, src));
               float4 v;
-              v.x = act_fwd(acc[g * 16 + 4 * c4 + 0] + bv.x, prm.act);
-              v.y = act_fwd(acc[g * 16 + 4 * c4 + 1] + bv.y, prm.act);
-              v.z = act_fwd(acc[g * 16 + 4 * c4 + 2] + bv.z, prm.act);
-              v.w = act_fwd(acc[g * 16 + 4 * c4 + 3] + bv.w, prm.act);
+              v.x = act_fwd(acc[g * 16 + 4 * c4 + 0] + bv.x, ACT);
+              v.y = act_fwd(acc[g * 16 + 4 * c4 + 1] + bv.y, ACT);
+              v.z = act_fwd(acc[g * 16 + 4 * c4 + 2] + bv.z, ACT);
+              v.w = act_fwd(acc[g * 16 + 4 * c4 + 3] + bv.w, ACT);
               ptx::sts_f4(buf + roff + ((c4 ^ swz) << 4), v);
             }
           } else if constexpr (bwd) {
@@ -238,10 +238,10 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
               const uint32_t pp = buf + roff + ((c4 ^ swz) << 4);
               const float4 a = ptx::lds_f4(pp);
               float4 v;
-              v.x = acc[g * 16 + 4 * c4 + 0] * act_deriv_from_a(a.x, prm.act);
-              v.y = acc[g * 16 + 4 * c4 + 1] * act_deriv_from_a(a.y, prm.act);
-              v.z = acc[g * 16 + 4 * c4 + 2] * act_deriv_from_a(a.z, prm.act);
-              v.w = acc[g * 16 + 4 * c4 + 3] * act_deriv_from_a(a.w, prm.act);
+              v.x = acc[g * 16 + 4 * c4 + 0] * act_deriv_from_a(a.x, ACT);
+              v.y = acc[g * 16 + 4 * c4 + 1] * act_deriv_from_a(a.y, ACT);
+              v.z = acc[g * 16 + 4 * c4 + 2] * act_deriv_from_a(a.z, ACT);
+              v.w = acc[g * 16 + 4 * c4 + 3] * act_deriv_from_a(a.w, ACT);
               ptx::sts_f4(pp, v);
             }
           } else {
@@ -289,6 +289,21 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
           }
         }
       }
+
+// The activation is resolved once per tile, so each epilogue body is straight-line code (a per-element
+// runtime switch left a branch between every element's tanh and no instruction-level parallelism).
+template <int CW, int EPI>
+__device__ __forceinline__ void epi_tile_act(const float (&acc)[CW], const KParams& prm, const CUtensorMap* tOut,
+                                             const CUtensorMap* tAux, uint64_t* auxbar, uint32_t& aux_ph,
+                                             uint32_t ebuf_s, int lane, int row0, int colw, int p, int pz,
+                                             float4 bias4) {
+  if (EPI == EPI_STORE || prm.act == PUSH_ACT_IDENTITY)
+    epi_tile<CW, EPI, PUSH_ACT_IDENTITY>(acc, prm, tOut, tAux, auxbar, aux_ph, ebuf_s, lane, row0, colw, p, pz, bias4);
+  else if (prm.act == PUSH_ACT_TANH)
+    epi_tile<CW, EPI, PUSH_ACT_TANH>(acc, prm, tOut, tAux, auxbar, aux_ph, ebuf_s, lane, row0, colw, p, pz, bias4);
+  else
+    epi_tile<CW, EPI, PUSH_ACT_RELU>(acc, prm, tOut, tAux, auxbar, aux_ph, ebuf_s, lane, row0, colw, p, pz, bias4);
+}
 
 template <int BN, bool AMN, bool BMN, bool BSPLIT, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -528,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!live || (prm.dbg & 2)) continue;
         const int pz = EPI == EPI_STORE ? tc.split * prm.batch + tc.p : tc.p;
-        epi_tile<C::CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, tc.p, pz, bias4);
+        epi_tile_act<C::CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, tc.p, pz, bias4);
       }
       if (lane == 0) ptx::bulk_wait0();
     }
@@ -823,7 +838,7 @@ __global__ void __launch_bounds__(k2Threads, 1)
       }
       if (!live || (prm.dbg & 2)) continue;
       const int pz = EPI == EPI_STORE ? split * prm.batch + p : p;
-      epi_tile<k2CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, p, pz, bias4);
+      epi_tile_act<k2CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, p, pz, bias4);
     }
     if (lane == 0) ptx::bulk_wait0();
   }

@@ -50,6 +50,7 @@ struct LayerPlan {
   int wsplit_max = 1;            // weight-gradient split count at max_batch (partial buffer size)
 };
 
+constexpr int kGramMinN = 32;       // a7 in the Gram form from this many particles (measured crossover)
 constexpr int kNcclMaxCtas = 16;    // SMs the NCCL collectives may take while the GEMMs run (ncclConfig maxCTAs)
 constexpr int kTcUpdateMinN = 128;  // a10 on the tensor cores from this many particles (measured crossover)
 constexpr int kMaxX0 = 4;  // thin first layer whose weight grads are fused into layer 1's BWD epilogue
@@ -221,11 +222,13 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.dist = kern::dist_plan(P.n, P.tensors, P.toff.data(), P.tsize.data(), c->variant ? P.d : P.ld);
   if (c->variant) P.useg = kern::var_segments(P.tensors, P.toff.data(), P.tsize.data());
   P.ds = c->exchange == PUSH_XCHG_DSHARD;
-  // Canonical kernel, 2 <= n <= 256 (both exchange modes): a7 as the centred symmetric Gram product on
+  // Canonical kernel, 32 <= n <= 256 (both exchange modes): a7 as the centred symmetric Gram product on
   // the tensor cores (gram.cu; R27) — one HBM stream of Theta, no CUDA-core pair loop.  Its
   // split plan replaces the direct-form plan; it depends only on (n, ld), so every sharding (and the
-  // d-sharded mode, which owns whole splits) sums the same partials in the same order.
-  if (c->variant == 0 && P.n >= 2 && P.n <= kern::kGramMaxN) {
+  // d-sharded mode, which owns whole splits) sums the same partials in the same order.  Below 32
+  // particles the direct form is HBM-bound already (n <= 8: 0.84 of HBM at C5) and a Gram stage carries
+  // too few bytes (C5: 1.09 ms Gram vs 0.12 ms direct; C2: 29 vs 25 us).
+  if (c->variant == 0 && P.n >= kGramMinN && P.n <= kern::kGramMaxN) {
     P.dist = kern::gram_plan(P.n, P.ld);
     P.gram = true;
   }
