@@ -47,16 +47,15 @@ constexpr int kXfWarp0 = 2, kXfWarps = 4, kXfThreads = 32 * kXfWarps;
 constexpr int kEpiWarp0 = kXfWarp0 + kXfWarps, kEpiWarps = 8;
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
 constexpr int kHalfBox = 32 * 16 * 4;  // one 32 x 16 fp32 SWIZZLE_64B output box
-constexpr int kEpiBox = 2 * kHalfBox;  // double-buffered per epilogue warp
 constexpr int kMaxSmem = 232448;      // 227 KB opt-in dynamic shared memory per CTA
 
-template <int BN>
+template <int BN, int NB = 2>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // A (fp32), B_hi, B_lo
-  static constexpr int EPI_BYTES = kEpiWarps * kEpiBox;
-  static constexpr int BAR_BYTES = 512;
+  static constexpr int EPI_BYTES = kEpiWarps * NB * kHalfBox;
+  static constexpr int BAR_BYTES = 1024;
   static constexpr int STAGES_RAW = (kMaxSmem - 1024 - EPI_BYTES - BAR_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
   static constexpr int NACC = 2;                       // TMEM accumulator buffers (BN columns each)
@@ -174,12 +173,20 @@ __device__ __forceinline__ float4 load_bias4(const KParams& prm, int lane, int c
   }
   return b;
 }
+// Boxes per epilogue warp: the BWD epilogue keeps kAuxAhead aprev loads in flight ahead of the group it
+// computes (its HBM load latency was exposed on every 16-column group with one box ahead), so it needs
+// 2 + kAuxAhead boxes; the others double-buffer their stores.
+constexpr int kAuxAhead = 2;
+template <int EPI>
+struct EpiBoxes { static constexpr int NB = EPI == EPI_BWD ? 2 + kAuxAhead : 2; };
+
 template <int CW, int EPI, int ACT>
 __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& prm, const CUtensorMap* tOut,
                                          const CUtensorMap* tAux, uint64_t* auxbar, uint32_t& aux_ph,
                                          uint32_t ebuf_s, int lane, int row0, int colw, int p, int pz,
                                          float4 bias4) {
   constexpr bool bwd = EPI == EPI_BWD;
+  constexpr int NB = EpiBoxes<EPI>::NB;
         // Output in 16-column groups g, double-buffered: group g is staged in half-box (g & 1)
         // (32 rows x 16 fp32, SWIZZLE_64B: 16-B chunk c of row r sits at chunk c ^ ((r >> 1) & 3)),
         // so the TMA store of group g overlaps the math of group g + 1.
@@ -200,17 +207,17 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const int col = colw + g * 16;
-          const uint32_t buf = ebuf_s + (g & 1) * kHalfBox;
+          const uint32_t buf = ebuf_s + (g % NB) * kHalfBox;
           if constexpr (bwd) {
-            ptx::mbar_wait(auxbar, aux_ph);  // aprev of group g has landed in buf
-            aux_ph ^= 1;
-            // prefetch aprev of group g + 1 into the other box as soon as the store of group g - 1 (its
-            // previous tenant) has read it, so the load overlaps this group's math and store
-            if (g + 1 < G && lane == 0) {
-              ptx::bulk_wait_read0();
-              const uint32_t nb = ebuf_s + ((g + 1) & 1) * kHalfBox;
-              ptx::mbar_arrive_expect_tx(auxbar, kHalfBox);
-              ptx::tma_load_3d(ptx_ptr(nb), tAux, auxbar, col + 16, row0, p);
+            ptx::mbar_wait(auxbar + (g % NB), (aux_ph >> (g % NB)) & 1);  // aprev of group g is in buf
+            aux_ph ^= 1u << (g % NB);
+            // prefetch aprev of group g + kAuxAhead into box (g + kAuxAhead) % NB once the store of its
+            // previous tenant (group g - 2) has read it: only the latest store (group g - 1) may be pending
+            if (g + kAuxAhead < G && lane == 0) {
+              ptx::bulk_wait_read1();
+              const int nbx = (g + kAuxAhead) % NB;
+              ptx::mbar_arrive_expect_tx(auxbar + nbx, kHalfBox);
+              ptx::tma_load_3d(ptx_ptr(ebuf_s + nbx * kHalfBox), tAux, auxbar + nbx, col + 16 * kAuxAhead, row0, p);
             }
             __syncwarp();
           } else {
@@ -310,7 +317,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tBhi,
                       const __grid_constant__ CUtensorMap tBlo, const __grid_constant__ CUtensorMap tOut,
                       const __grid_constant__ CUtensorMap tAux, const KParams prm) {
-  using C = Cfg<BN>;
+  constexpr int NB = EpiBoxes<EPI>::NB;
+  using C = Cfg<BN, NB>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B aligned base for the SWIZZLE_128B atoms; pointer arithmetic on the __shared__ array keeps
   // every derived pointer in the shared state space (LDS/STS, not generic loads)
@@ -322,8 +330,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* aempty = empty + C::STAGES;  // [NSLOT] the MMAs reading TMEM A slot j have completed
   uint64_t* tfull = aempty + C::NSLOT;   // [NACC] accumulator b holds a finished K-chunk
   uint64_t* tempty = tfull + C::NACC;    // [NACC] accumulator b has been drained to registers
-  uint64_t* auxbar = tempty + C::NACC;   // [kEpiWarps] aprev box landed in the warp's smem box
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + kEpiWarps);
+  uint64_t* auxbar = tempty + C::NACC;   // [kEpiWarps][NB] aprev landed in box b of the warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + kEpiWarps * NB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb_total = (prm.K + BK - 1) / BK;
@@ -339,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], 32 * 4 * C::EPI_SPLIT);
     }
-    for (int e = 0; e < kEpiWarps; ++e) ptx::mbar_init(&auxbar[e], 1);
+    for (int e = 0; e < kEpiWarps * NB; ++e) ptx::mbar_init(&auxbar[e], 1);
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tA);
     ptx::prefetch_tmap(&tBhi);
@@ -495,8 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;      // TMEM lane quarter this warp may access
     const int h = e >> 2;        // column half
     if (h < C::EPI_SPLIT) {
-      float* ebuf = reinterpret_cast<float*>(ebuf_all + e * kEpiBox);
-      const uint32_t ebuf_s = ptx::smem_u32(ebuf);
+      const uint32_t ebuf_s = ptx::smem_u32(ebuf_all + e * NB * kHalfBox);
       const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
       uint32_t ch = 0, aux_ph = 0;
       constexpr bool bwd = EPI == EPI_BWD;
@@ -510,10 +517,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row0 = tc.m0 + q * 32;
         const bool live = row0 < prm.M;
         const int colw = n0 + h * C::CW;
-        if (bwd && live && lane == 0) {  // prefetch aprev of group 0 while the MMAs run
+        if (bwd && live && lane == 0) {  // prefetch aprev of the first groups while the MMAs run
           ptx::bulk_wait_read0();
-          ptx::mbar_arrive_expect_tx(&auxbar[e], kHalfBox);
-          ptx::tma_load_3d(ebuf, &tAux, &auxbar[e], colw, row0, tc.p);
+#pragma unroll
+          for (int g = 0; g < kAuxAhead && g < C::CW / 16; ++g) {
+            ptx::mbar_arrive_expect_tx(&auxbar[e * NB + g], kHalfBox);
+            ptx::tma_load_3d(ptx_ptr(ebuf_s + g * kHalfBox), &tAux, &auxbar[e * NB + g], colw + 16 * g, row0, tc.p);
+          }
         }
         const float4 bias4 = load_bias4<C::CW, EPI>(prm, lane, colw, tc.p);
         float acc[C::CW];
@@ -543,7 +553,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!live || (prm.dbg & 2)) continue;
         const int pz = EPI == EPI_STORE ? tc.split * prm.batch + tc.p : tc.p;
-        epi_tile_act<C::CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, tc.p, pz, bias4);
+        epi_tile_act<C::CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e * NB], aux_ph, ebuf_s, lane, row0, colw, tc.p, pz,
+                                 bias4);
       }
       if (lane == 0) ptx::bulk_wait0();
     }
@@ -571,13 +582,13 @@ constexpr int k2XfWarp0 = 4, k2EpiWarp0 = 8;
 // PBN = pair tile width: 256 (one TMEM accumulator of 256 columns, 128 columns per epilogue thread)
 // or 128 (two rotating accumulators of 128 columns, so the fused epilogue overlaps the next tile, and
 // 32-KB stages, so 6 of them fit).
-template <int PBN>
+template <int PBN, int NB = 2>
 struct Cfg2 {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = (PBN / 2) * BK * 4;
   static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;
-  static constexpr int EPI_BYTES = kEpiWarps * kEpiBox;
-  static constexpr int BAR_BYTES = 512;
+  static constexpr int EPI_BYTES = kEpiWarps * NB * kHalfBox;
+  static constexpr int BAR_BYTES = 1024;
   static constexpr int STAGES_RAW = (kMaxSmem - 1024 - EPI_BYTES - BAR_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
   static constexpr int NSLOT = 4;
@@ -594,7 +605,8 @@ __global__ void __launch_bounds__(k2Threads, 1)
     gemm3xtf32_2sm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tBhi,
                           const __grid_constant__ CUtensorMap tBlo, const __grid_constant__ CUtensorMap tOut,
                           const __grid_constant__ CUtensorMap tAux, const KParams prm) {
-  using C = Cfg2<PBN>;
+  constexpr int NB = EpiBoxes<EPI>::NB;
+  using C = Cfg2<PBN, NB>;
   constexpr int k2BN = PBN, k2CW = C::CW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -605,8 +617,8 @@ __global__ void __launch_bounds__(k2Threads, 1)
   uint64_t* aempty = empty + C::STAGES;   // [NSLOT] the MMAs reading TMEM A slot j have completed
   uint64_t* tfull = aempty + C::NSLOT;    // [NACC] accumulator b holds a finished K-chunk
   uint64_t* tempty = tfull + C::NACC;     // [NACC] leader: both CTAs have drained accumulator b
-  uint64_t* auxbar = tempty + C::NACC;    // [kEpiWarps]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + kEpiWarps);
+  uint64_t* auxbar = tempty + C::NACC;    // [kEpiWarps][NB]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + kEpiWarps * NB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = ptx::cluster_ctarank();
@@ -623,7 +635,7 @@ __global__ void __launch_bounds__(k2Threads, 1)
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], 2 * kEpiWarps);  // one arrival per epilogue warp of each CTA
     }
-    for (int e = 0; e < kEpiWarps; ++e) ptx::mbar_init(&auxbar[e], 1);
+    for (int e = 0; e < kEpiWarps * NB; ++e) ptx::mbar_init(&auxbar[e], 1);
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tA);
     ptx::prefetch_tmap(&tBhi);
@@ -792,7 +804,7 @@ __global__ void __launch_bounds__(k2Threads, 1)
     const int e = warp - k2EpiWarp0;
     const int q = warp & 3;
     const int h = e >> 2;
-    const uint32_t ebuf_s = ptx::smem_u32(ebuf_all + e * kEpiBox);
+    const uint32_t ebuf_s = ptx::smem_u32(ebuf_all + e * NB * kHalfBox);
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
     const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(tempty), 0);  // + 8 * b for accumulator b
     uint32_t ch = 0, aux_ph = 0;
@@ -806,10 +818,13 @@ __global__ void __launch_bounds__(k2Threads, 1)
       const int row0 = mp * 256 + (int)crank * 128 + q * 32;
       const bool live = row0 < prm.M;
       const int colw = nt * k2BN + h * k2CW;
-      if (bwd && live && lane == 0) {
+      if (bwd && live && lane == 0) {  // prefetch aprev of the first groups while the MMAs run
         ptx::bulk_wait_read0();
-        ptx::mbar_arrive_expect_tx(&auxbar[e], kHalfBox);
-        ptx::tma_load_3d(ptx_ptr(ebuf_s), &tAux, &auxbar[e], colw, row0, p);
+#pragma unroll
+        for (int g = 0; g < kAuxAhead && g < k2CW / 16; ++g) {
+          ptx::mbar_arrive_expect_tx(&auxbar[e * NB + g], kHalfBox);
+          ptx::tma_load_3d(ptx_ptr(ebuf_s + g * kHalfBox), &tAux, &auxbar[e * NB + g], colw + 16 * g, row0, p);
+        }
       }
       const float4 bias4 = load_bias4<k2CW, EPI>(prm, lane, colw, p);
       float acc[k2CW];
@@ -838,7 +853,8 @@ __global__ void __launch_bounds__(k2Threads, 1)
       }
       if (!live || (prm.dbg & 2)) continue;
       const int pz = EPI == EPI_STORE ? split * prm.batch + p : p;
-      epi_tile_act<k2CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e], aux_ph, ebuf_s, lane, row0, colw, p, pz, bias4);
+      epi_tile_act<k2CW, EPI>(acc, prm, &tOut, &tAux, &auxbar[e * NB], aux_ph, ebuf_s, lane, row0, colw, p, pz,
+                              bias4);
     }
     if (lane == 0) ptx::bulk_wait0();
   }
@@ -905,7 +921,7 @@ push_status make_operand_map(const float* ptr, const Operand& op, int mn_extent,
 
 template <int BN, bool AMN, bool BMN, bool BS, int EPI>
 push_status launch_t(const CUtensorMap* maps, const KParams& kp, cudaStream_t stream) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, EpiBoxes<EPI>::NB>;
   static bool attr_set = false;
   if (!attr_set) {
     PUSH_CUDA_TRY(cudaFuncSetAttribute(gemm3xtf32_kernel<BN, AMN, BMN, BS, EPI>,
@@ -956,12 +972,13 @@ push_status launch2_t(const CUtensorMap* maps, const KParams& kp, cudaStream_t s
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.blockDim = dim3(k2Threads);
-  cfg.dynamicSmemBytes = Cfg2<PBN>::SMEM_BYTES;
+  cfg.dynamicSmemBytes = Cfg2<PBN, EpiBoxes<EPI>::NB>::SMEM_BYTES;
   cfg.stream = stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (!max_pairs) {
-    PUSH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<PBN>::SMEM_BYTES));
+    PUSH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Cfg2<PBN, EpiBoxes<EPI>::NB>::SMEM_BYTES));
     cfg.gridDim = dim3(g_sms);
     int n = 0;
     PUSH_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
