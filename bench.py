@@ -393,6 +393,23 @@ def run_ours(args, w):
         if tf32_meas:
             roof["cublas_tf32_tflops_measured"] = tf32_meas
             roof["frac_vs_cublas_tf32"] = ach / (tf32_meas / 3.0)
+    else:
+        # FP32 CUDA-core peak: 148 SMs x 128 FP32 lanes x 2 flops (FMA) x the max SM clock
+        fp32_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        ridge = fp32_peak * 1e12 / (peaks["hbm_gbs"] * 1e9)  # flop per byte
+        if dom.get("alg_flops") and dom["alg_bytes"] and dom["alg_flops"] / dom["alg_bytes"] > ridge:
+            ach = dom["alg_flops"] / (dom["ms"] / 1e3) / 1e12
+            roof = {"bound": "alu", "kernel": dom["name"], "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
+                    "frac": ach / fp32_peak, "traffic": traffic,
+                    "algorithmic_per_launch": dom["alg_flops"] / per_launch,
+                    "peak_note": f"FP32 FMA issue: 148 SMs x 128 lanes x 2 x {peaks.get('sm_max_mhz', 1965.0):.0f} MHz "
+                                 f"(intensity {dom['alg_flops'] / dom['alg_bytes']:.1f} flop/B > ridge {ridge:.1f})"}
+        else:
+            peak = peaks["hbm_gbs"]
+            ach = dom["alg_bytes"] / (dom["ms"] / 1e3) / 1e9
+            roof = {"bound": "hbm", "kernel": dom["name"], "achieved": ach, "peak": peak, "unit": "GB/s",
+                    "frac": ach / peak, "traffic": traffic, "algorithmic_per_launch": dom["alg_bytes"] / per_launch,
+                    "peak_note": f"{peak_kind} hbm_gbs"}
     if traffic_src:
         roof["traffic_note"] = "DRAM bytes per launch (read + write) from " + traffic_src
     npath = os.path.join(ROOT, "profiles", f"ncu_{w.name}.json")

@@ -165,6 +165,15 @@ void update_lhs(const float* K, int nl, int npad, int n, int pitch, const float*
                 cudaStream_t s);
 void update_fixup(const float* theta_own, int64_t ld, int nl, const float* srow, const float* h, float eps_n,
                   float* next_own, cudaStream_t s);
+// a10 streaming on the tensor cores with the update in the epilogue (upd.cu), n <= 64, rows <= 64:
+// out[i][c] = th_i[c] + eps_n (sum_q lhs[i][q] B[q][c] + r s_i th_i[c]), B = the 2n x w operand at b
+// ([G; Theta] when g_first), th_i = Theta row own_row + i of B, lhs = [K, -rK] / [-rK, K] split into tf32
+// hi / lo (lhs_hi, lhs_lo: scratch of update_tc_npad(rows) x round_up(2n, 4) floats each); w % 128 == 0
+constexpr int kUpdTcMaxRows = 64;
+int update_tc_npad(int rows);
+push_status update_tc_stream(const float* b, bool g_first, int n, int64_t w, int rows, int own_row, const float* K,
+                             const float* h, float* lhs_hi, float* lhs_lo, float* out, const float* srow, float eps_n,
+                             cudaStream_t s);
 // NEXT-2 variants: column segments of <= kVarSegCols columns inside one tensor (x = begin, y = end, z = tensor)
 constexpr int kVarSegCols = 128;
 std::vector<int4> var_segments(int tensors, const int64_t* toff, const int64_t* tsize);

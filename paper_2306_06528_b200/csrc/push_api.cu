@@ -52,7 +52,8 @@ struct LayerPlan {
 
 constexpr int kGramMinN = 32;       // a7 in the Gram form from this many particles (measured crossover)
 constexpr int kNcclMaxCtas = 16;    // SMs the NCCL collectives may take while the GEMMs run (ncclConfig maxCTAs)
-constexpr int kTcUpdateMinN = 128;  // a10 on the tensor cores from this many particles (measured crossover)
+constexpr int kTcUpdateMinN = 128;
+constexpr int kTcStreamMinN = 32;  // a10 as the streaming tensor-core contraction for 32 <= n <= 64  // a10 on the tensor cores from this many particles (measured crossover)
 constexpr int kMaxX0 = 4;  // thin first layer whose weight grads are fused into layer 1's BWD epilogue
 
 struct Plan {
@@ -77,6 +78,7 @@ struct Plan {
   int ds_smax = 0;      // most splits on one rank (the all-gathered partial slots per rank)
   bool gram = false;    // a7 as the centred symmetric Gram product (gram.cu); dist holds its split plan
   bool tc_update = false;  // a10 as the contraction [K, -rK] x [G; Theta] on the tensor cores
+  bool tc_stream = false;  // a10 as the streaming transposed contraction with the fused update (upd.cu)
   // byte offsets into the workspace
   size_t o_ulhs = 0, o_gsum = 0;
   size_t o_theta0, o_theta1, o_grad, o_whi, o_wlo, o_dlt0, o_dlt1, o_err2, o_loss, o_loss_all, o_opw, o_opb,
@@ -240,6 +242,10 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   // depends on n only (never on n_local or the exchange mode), so every sharding and the d-sharded
   // panels take the same arithmetic (P-invariance).
   P.tc_update = c->variant == 0 && P.n >= kTcUpdateMinN && P.ld % 128 == 0;
+  // 32 <= n <= 64 (C3, S1): the streaming contraction (upd.cu) with the update in its epilogue: B read
+  // once from HBM, no U round trip (the staged CUDA-core kernel was FP32-issue / latency bound at ~0.3 of
+  // HBM there).  n only, as above.
+  P.tc_stream = c->variant == 0 && P.n >= kTcStreamMinN && P.n <= kern::kUpdTcMaxRows && P.ld % 128 == 0;
   if (P.ds) {
     const int S = P.dist.splits;
     for (int q = 0; q <= world; ++q) P.ds_s0.push_back((int)((int64_t)q * S / world));
@@ -290,7 +296,8 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   P.o_xpart = take(P.fuse_x0 ? (int64_t)P.RB * P.nl * P.layers[0].out * P.layers[0].in : 1);
   P.o_dpart = take((int64_t)(P.ds ? world * P.ds_smax : P.dist.splits) *
                    (P.gram ? kern::gram_part_floats(P.n) : (int64_t)P.n * P.n));
-  P.o_ulhs = take(P.tc_update ? (int64_t)(P.ds ? P.n : P.nl) * round_up(2 * P.n, 4) : 1);
+  P.o_ulhs = take(P.tc_update ? (int64_t)(P.ds ? P.n : P.nl) * round_up(2 * P.n, 4)
+                               : (P.tc_stream ? 2 * (int64_t)kern::kUpdTcMaxRows * round_up(2 * P.n, 4) : 1));
   P.o_gsum = take(P.gram ? kern::gram_part_floats(P.n) : 1);
   P.o_D = take((int64_t)P.tensors * P.n * P.n);
   P.o_K = take((int64_t)P.tensors * (P.ds ? P.n : P.nl) * P.n);  // d-sharded: K of all n rows
@@ -831,9 +838,14 @@ static push_status ds_phase2(push_ctx* c, cudaStream_t s) {
   });
   if (st != PUSH_OK || wo == 0) return st;
   const float eps_n = c->cfg.step_size / (float)P.n;
-  return run_k(c, PC_UPDATE, P.tc_update ? 3 : 1, 12.0 * P.n * (double)wo, 2.0 * P.n * (double)P.n * wo, s,
+  return run_k(c, PC_UPDATE, P.tc_update ? 3 : (P.tc_stream ? 2 : 1), 12.0 * P.n * (double)wo, 2.0 * P.n * (double)P.n * wo, s,
                [&]() -> push_status {
     float* pth = pan_theta(c);
+    if (P.tc_stream) {  // every row of the panel; operand order as the all-gather path at this parity
+      const int64_t half = (int64_t)kern::kUpdTcMaxRows * round_up(2 * P.n, 4);
+      return kern::update_tc_stream(c->cur ? c->pg : pth, c->cur == 1, P.n, wo, P.n, 0, c->K, c->h, c->ulhs,
+                                    c->ulhs + half, c->pth2, c->srow, eps_n, s);
+    }
     if (P.tc_update)  // every row of the panel; [Theta; G] or [G; Theta] as the all-gather path at this parity
       return update_tc(c, c->cur ? c->pg : pth, c->cur == 1, wo, P.n, c->K, c->srow, pth, c->pth2, eps_n, s);
     kern::svgd_update(pth, c->pg, wo, P.n, 0, P.n, c->K, c->srow, c->h, eps_n, c->pth2, s);
@@ -927,9 +939,14 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   const float eps_n = c->cfg.step_size / (float)P.n;
   float* next = c->theta[c->cur ^ 1];
   const int var = c->cfg.variant;
-  st = run_k(c, PC_UPDATE, (var == 0 && P.tc_update) ? 3 : 1, 2.0 * nd4 + 4.0 * P.nl * (double)P.d,
+  st = run_k(c, PC_UPDATE, (var == 0 && P.tc_update) ? 3 : ((var == 0 && P.tc_stream) ? 2 : 1), 2.0 * nd4 + 4.0 * P.nl * (double)P.d,
              2.0 * P.nl * (double)P.n * P.d, s, [&] {
-    if (var == 0 && P.tc_update) {
+    if (var == 0 && P.tc_stream) {
+      const bool g_first = c->grad < th;  // layout Theta[0], G, Theta[1]
+      const int64_t half = (int64_t)kern::kUpdTcMaxRows * round_up(2 * P.n, 4);
+      return kern::update_tc_stream(g_first ? c->grad : th, g_first, P.n, P.ld, P.nl, c->row0, c->K, c->h, c->ulhs,
+                                    c->ulhs + half, next + (int64_t)c->row0 * P.ld, c->srow, eps_n, s);
+    } else if (var == 0 && P.tc_update) {
       // layout Theta[0], G, Theta[1]: [G; Theta_cur] or [Theta_cur; G] is one 2n x ld operand
       const bool g_first = c->grad < th;
       return update_tc(c, g_first ? c->grad : th, g_first, P.ld, P.nl, c->K, c->srow,

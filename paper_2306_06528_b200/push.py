@@ -253,9 +253,9 @@ class Context:
         check(lib().push_profile_enable(self._h, 1 if on else 0))
 
     def profile_read(self):
-        rows = (ProfileRow * 16)()
+        rows = (ProfileRow * 32)()
         n = c_int32(0)
-        check(lib().push_profile_read(self._h, rows, 16, ctypes.byref(n)))
+        check(lib().push_profile_read(self._h, rows, 32, ctypes.byref(n)))
         return [dict(name=r.name.decode(), ms=r.ms, launches=r.launches, alg_bytes=r.alg_bytes,
                      alg_flops=r.alg_flops) for r in rows[:n.value]]
 

@@ -60,6 +60,9 @@ GRAD_CASES = [
     (2, [3, 1024, 1], 300, "tanh", "gaussian", 1.5, 1.0, "burgers"),     # 8-row slabs, 3-deep ring, ragged
     (2, [2, 2048, 1], 100, "tanh", "uniform", 1.0, 1.0, "gauss"),         # 4-row slabs, 8 features / thread
     (2, [2, 300, 2], 77, "relu", "uniform", 1.0, 1.0, "gauss"),           # H % 256 != 0, d_out = 2, relu
+    # small ragged widths with relu + Gaussian prior; the C4 net shape
+    (3, [2, 48, 40, 2], 130, "relu", "gaussian", 0.7, 1.5, "gauss"),
+    (5, [1, 64, 64, 64, 1], 128, "tanh", "uniform", 1.0, 1.0, "random"),
 ]
 
 
