@@ -21,3 +21,13 @@ timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytes
 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x \
   -k "sharding and 128" > $OUT/memcheck3.log 2>&1; echo "memcheck3 exit $?" >> $OUT/memcheck3.log
 for f in memcheck memcheck_gemm racecheck racecheck2 memcheck2 memcheck3; do tail -n 4 $OUT/$f.log; done
+# round 2: the Gram-form distances (gram.cu, n = 33..256), the streaming update (upd.cu, n = 33..64),
+# both through the d-sharded panels too
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x \
+  -k "(step_from_set_grads and (33-777 or 64-2048 or 100-96 or 160-3000)) or (clustered and (64-0.1 or 256))" \
+  > $OUT/memcheck_r02.log 2>&1; echo "memcheck_r02 exit $?" >> $OUT/memcheck_r02.log
+timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x \
+  -k "step_from_set_grads and (33-777 or 64-2048 or 160-3000)" > $OUT/racecheck_r02.log 2>&1; echo "racecheck_r02 exit $?" >> $OUT/racecheck_r02.log
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_dshard.py -q -x \
+  -k "dims5" > $OUT/memcheck_r02_dshard.log 2>&1; echo "memcheck_r02_dshard exit $?" >> $OUT/memcheck_r02_dshard.log
+for f in memcheck_r02 racecheck_r02 memcheck_r02_dshard; do tail -n 3 $OUT/$f.log; done
