@@ -214,7 +214,10 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
             // prefetch aprev of group g + kAuxAhead into box (g + kAuxAhead) % NB once the store of its
             // previous tenant (group g - 2) has read it: only the latest store (group g - 1) may be pending
             if (g + kAuxAhead < G && lane == 0) {
-              ptx::bulk_wait_read1();
+              if constexpr (NB - 1 - kAuxAhead == 0)
+                ptx::bulk_wait_read0();
+              else
+                ptx::bulk_wait_read1();
               const int nbx = (g + kAuxAhead) % NB;
               ptx::mbar_arrive_expect_tx(auxbar + nbx, kHalfBox);
               ptx::tma_load_3d(ptx_ptr(ebuf_s + nbx * kHalfBox), tAux, auxbar + nbx, col + 16 * kAuxAhead, row0, p);
