@@ -370,7 +370,7 @@ def run_ours(args, w):
     dom = max(roofable or prof, key=lambda r: r["ms"])
     phases = {r["name"]: {"ms_per_step": r["ms"] / args.steps, "share": r["ms"] / tot,
                           "launches_per_step": r["launches"] / args.steps} for r in prof if r["launches"] or r["ms"]}
-    traffic, traffic_src = None, None
+    traffic, traffic_src, ncu_tensor = None, None, None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{w.name}.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
@@ -378,6 +378,7 @@ def run_ours(args, w):
         if dom["name"] in tj.get("classes", {}):
             traffic = tj["classes"][dom["name"]]["dram_bytes_per_launch"]
             traffic_src = f"profiles/traffic_{w.name}.json ({tj.get('how', '')})"
+            ncu_tensor = tj["classes"][dom["name"]].get("tensor_pipe_pct")
     per_launch = max(dom["launches"], 1)
     if dom["name"].endswith("gemm"):
         # the profiled pass times the kernel inside a sub-second run at full clock: the BURST bf16 figure
@@ -412,6 +413,8 @@ def run_ours(args, w):
                     "peak_note": f"{peak_kind} hbm_gbs"}
     if traffic_src:
         roof["traffic_note"] = "DRAM bytes per launch (read + write) from " + traffic_src
+        if ncu_tensor is not None and dom["name"].endswith("gemm"):
+            roof["ncu_tensor_pipe_pct"] = ncu_tensor  # same capture, time-weighted over the class's launches
     npath = os.path.join(ROOT, "profiles", f"ncu_{w.name}.json")
     if os.path.exists(npath):  # ncu --set full summary of this config's step (scripts/ncu_summary.py --json)
         with open(npath) as f:

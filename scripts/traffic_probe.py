@@ -1,7 +1,8 @@
 """Per-kernel-class DRAM traffic of one SVGD step, for bench.py's roofline `traffic` field.
 
 Run under ncu (one GPU):
-  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,\
+sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed --clock-control none \
       --csv --log-file gpurun_out/traffic_C2.csv python scripts/traffic_probe.py --config C2
 then, on the dev host:
   python scripts/traffic_probe.py --summarise gpurun_out/traffic_C2.csv --config C2   -> profiles/traffic_C2.json
@@ -51,17 +52,24 @@ else:
     kern = [per[k] for k in order][-len(trace):]
     out = {}
     for cls, k in zip(trace, kern):
-        e = out.setdefault(cls, {"launches": 0, "dram_bytes": 0.0, "ncu_time_ns": 0.0, "kernels": set()})
+        e = out.setdefault(cls, {"launches": 0, "dram_bytes": 0.0, "ncu_time_ns": 0.0, "kernels": set(),
+                                 "tensor_ns": 0.0})
         e["launches"] += 1
         e["dram_bytes"] += k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0)
-        e["ncu_time_ns"] += k.get("gpu__time_duration.sum", 0)
+        tn = k.get("gpu__time_duration.sum", 0)
+        e["ncu_time_ns"] += tn
+        # time-weighted tensor-pipe activity (% of the elapsed peak) of the class's launches
+        e["tensor_ns"] += tn * k.get("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", 0) / 100
         e["kernels"].add(k["kernel"].split("(")[0][:60])
     res = {c: {"launches": e["launches"], "dram_bytes_per_launch": e["dram_bytes"] / e["launches"],
-               "ncu_time_us_per_launch": e["ncu_time_ns"] / e["launches"] / 1e3, "kernels": sorted(e["kernels"])}
+               "ncu_time_us_per_launch": e["ncu_time_ns"] / e["launches"] / 1e3,
+               "tensor_pipe_pct": 100 * e["tensor_ns"] / e["ncu_time_ns"] if e["ncu_time_ns"] else 0.0,
+               "kernels": sorted(e["kernels"])}
            for c, e in out.items()}
     path = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     json.dump({"config": args.config, "source": os.path.basename(args.summarise),
-               "how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
+               "how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+                      "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed "
                       "--clock-control none over one eager step (scripts/traffic_probe.py)",
                "classes": res}, open(path, "w"), indent=1)
     print(json.dumps(res, indent=1))
