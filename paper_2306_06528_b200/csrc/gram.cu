@@ -54,12 +54,13 @@ struct GCfg {
   static constexpr int STAGES = std::min(8, kGSmemTiles / STAGE);
   static constexpr int NACC = NP <= 128 ? 2 : 1;               // TMEM accumulators of NP columns
   static constexpr int ASET = KPS * 32;                      // TMEM columns of one stage's A operand
-  static constexpr int ASLOT0 = NACC * NP;                     // kGGroups A sets (one per transform group)
+  static constexpr int ASLOT0 = NACC * NP;                     // NSET A sets (stage i uses set i % NSET)
+  static constexpr int NSET = std::min(4, (512 - ASLOT0) / ASET);
   static constexpr int CW = NP >= 32 ? NP / 2 : 16;            // accumulator columns per epilogue thread
   static constexpr int EPI_SPLIT = NP / CW;                    // epilogue warps per TMEM lane quarter
   static constexpr int OUTER = NP > 64 ? (NP - 64) * 8 / 128 : 0;  // 16-B units per thread outside the i-block
   static constexpr int SMEM = 1024 + STAGES * (STAGE + 512) + 512;
-  static_assert(ASLOT0 + ASET * kGGroups <= 512, "tmem");
+  static_assert(NSET >= kGGroups && ASLOT0 + ASET * NSET <= 512, "tmem");
   static_assert(CW % 16 == 0 && STAGES >= 2 && STAGES % kGGroups == 0, "cfg");
 };
 
@@ -79,8 +80,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(cbuf + C::STAGES * 512);
   uint64_t* ready = full + C::STAGES;
   uint64_t* empty = ready + C::STAGES;
-  uint64_t* aempty = empty + C::STAGES;  // [kGGroups] A set g free
-  uint64_t* tfull = aempty + kGGroups;
+  uint64_t* aempty = empty + C::STAGES;  // [NSET] A set free
+  uint64_t* tfull = aempty + C::NSET;
   uint64_t* tempty = tfull + C::NACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::NACC);
 
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       ptx::mbar_init(&ready[s], 128);  // the 4 warps of the group that transforms stage s
       ptx::mbar_init(&empty[s], 1);
     }
-    for (int j = 0; j < kGGroups; ++j) ptx::mbar_init(&aempty[j], 1);
+    for (int j = 0; j < C::NSET; ++j) ptx::mbar_init(&aempty[j], 1);
     for (int b = 0; b < C::NACC; ++b) {
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], 32 * 4 * C::EPI_SPLIT);
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       int ch = 0;
       for (int i = 0; i < nst; ++i) {
         const bool first = i % C::CHUNK == 0, last = i % C::CHUNK == C::CHUNK - 1 || i == nst - 1;
-        const int b = ch % C::NACC, s = i % C::STAGES, g = i % kGGroups;
+        const int b = ch % C::NACC, s = i % C::STAGES, g = i % C::NSET;
         if (first) ptx::mbar_wait(&tempty[b], ((ch / C::NACC) & 1) ^ 1);
         ptx::mbar_wait(&ready[s], (i / C::STAGES) & 1);
         ptx::tc_fence_after();
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       }
     }
   } else if (warp < kGEpi0) {
-    // ---------------- transform group g: stages g, g + kGGroups, ... into A set g.  Thread: TMEM lane
+    // ---------------- transform group g: stages g, g + kGGroups, ... into A set i % NSET.  Thread: TMEM lane
     // 32q + lane = Hi or Lo of i-block row lane_row(q, lane); the Hi thread writes the row's Hi back in
     // place (the B operand).  Rows of the tile outside the i-block (n > 64) are converted unit by unit.
     const int g = (warp - kGXf0) >> 2, q = warp & 3, t = threadIdx.x - 32 * (kGXf0 + 4 * g);
@@ -165,11 +166,11 @@ __global__ void __launch_bounds__(kGThreads, 1)
     const bool want_lo = lane & 1;
     const bool in_tile = arow < NP;
     const bool live = arow < n;
-    const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + C::ASLOT0 + g * C::ASET;
     for (int i = g; i < nst; i += kGGroups) {
-      const int s = i % C::STAGES;
+      const int s = i % C::STAGES, set = i % C::NSET;
+      const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + C::ASLOT0 + set * C::ASET;
       ptx::mbar_wait(&full[s], (i / C::STAGES) & 1);
-      ptx::mbar_wait(&aempty[g], ((i / kGGroups) & 1) ^ 1);
+      ptx::mbar_wait(&aempty[set], ((i / C::NSET) & 1) ^ 1);
       ptx::tc_fence_after();
       const uint32_t cs = ptx::smem_u32(cbuf + s * 512);
 #pragma unroll 1

@@ -32,7 +32,8 @@ namespace {
 constexpr int kUK = 32;                 // rows of B (K) per stage
 constexpr int kUCols = 128;             // columns per tile (M)
 constexpr int kUThreads = 32 * 14;
-constexpr int kUStages = 5;
+constexpr int kUStages = 4;
+constexpr int kUOwnBufs = 3;            // own-theta tile buffers: the transform runs two tiles ahead
 constexpr int kUMaxKB = 4;              // 2n <= 128
 constexpr int kUStage = kUK * kUCols * 4;  // 16 KB
 
@@ -43,7 +44,7 @@ struct UCfg {
   static constexpr int ASLOT0 = 2 * NPAD;                  // two accumulators, then kUMaxKB A slots of 64
   static constexpr int CW = NPAD / 2;                      // accumulator columns per epilogue thread
   static constexpr int OWN = NPAD * kUCols * 4;             // own theta rows of one tile (fp32)
-  static constexpr int SMEM = 1024 + RES + kUStages * kUStage + 2 * OWN + 1024;
+  static constexpr int SMEM = 1024 + RES + kUStages * kUStage + kUOwnBufs * OWN + 1024;
   static_assert(ASLOT0 + 64 * kUMaxKB <= 512, "tmem");
   static_assert(CW % 8 == 0, "cfg");
 };
@@ -59,8 +60,8 @@ __global__ void __launch_bounds__(kUThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* res = smem;                       // lhs hi: kb * LTILE; lhs lo: (kUMaxKB + kb) * LTILE
   uint8_t* stg = smem + C::RES;
-  float* ownb = reinterpret_cast<float*>(stg + kUStages * kUStage);  // [2][NPAD][128]: own theta rows of tile lt & 1
-  float* rsv = ownb + 2 * NPAD * kUCols;                              // [NPAD]: r s_i
+  float* ownb = reinterpret_cast<float*>(stg + kUStages * kUStage);  // [3][NPAD][128]: own theta rows of tile lt % 3
+  float* rsv = ownb + kUOwnBufs * NPAD * kUCols;                      // [NPAD]: r s_i
   uint64_t* full = reinterpret_cast<uint64_t*>(rsv + 64);
   uint64_t* ready = full + kUStages;
   uint64_t* empty = ready + kUStages;
@@ -68,9 +69,9 @@ __global__ void __launch_bounds__(kUThreads, 1)
   uint64_t* tfull = aempty + kUMaxKB;        // [2]
   uint64_t* tempty = tfull + 2;              // [2]
   uint64_t* bres = tempty + 2;               // resident lhs landed
-  uint64_t* ownfull = bres + 1;              // [2] the transform has copied tile lt's own rows
-  uint64_t* ownempty = ownfull + 2;          // [2] the epilogue has read them
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ownempty + 2);
+  uint64_t* ownfull = bres + 1;              // [3] the transform has copied tile lt's own rows
+  uint64_t* ownempty = ownfull + kUOwnBufs;  // [3] the epilogue has read them
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ownempty + kUOwnBufs);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = (K2 + kUK - 1) / kUK;
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
       ptx::mbar_init(&tempty[b], 256);
     }
     ptx::mbar_init(bres, 1);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kUOwnBufs; ++b) {
       ptx::mbar_init(&ownfull[b], 128);
       ptx::mbar_init(&ownempty[b], 256);
     }
@@ -159,8 +160,9 @@ __global__ void __launch_bounds__(kUThreads, 1)
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;
     int it = 0;
     for (int lt = 0; lt < nt; ++lt) {
-      float* own = ownb + (lt & 1) * NPAD * kUCols;
-      ptx::mbar_wait(&ownempty[lt & 1], ((lt >> 1) & 1) ^ 1);  // the epilogue of tile lt - 2 is done with it
+      const int ob = lt % kUOwnBufs;
+      float* own = ownb + ob * NPAD * kUCols;
+      ptx::mbar_wait(&ownempty[ob], ((lt / kUOwnBufs) & 1) ^ 1);  // the epilogue of tile lt - 3 is done with it
       for (int kb = 0; kb < KB; ++kb, ++it) {
         const int s = it % kUStages;
         ptx::mbar_wait(&full[s], (it / kUStages) & 1);
@@ -184,7 +186,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
         ptx::tc_fence_before();
         ptx::mbar_arrive(&ready[s]);
       }
-      ptx::mbar_arrive(&ownfull[lt & 1]);  // tile lt's own rows are in `own`
+      ptx::mbar_arrive(&ownfull[ob]);  // tile lt's own rows are in `own`
     }
   } else {
     // ---------------- epilogue: quarter q (columns c = 32q + lane of the tile), half h of the rows i
@@ -207,8 +209,9 @@ __global__ void __launch_bounds__(kUThreads, 1)
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[b]);
-      ptx::mbar_wait(&ownfull[lt & 1], (lt >> 1) & 1);
-      const float* own = ownb + (lt & 1) * NPAD * kUCols;
+      const int ob = lt % kUOwnBufs;
+      ptx::mbar_wait(&ownfull[ob], (lt / kUOwnBufs) & 1);
+      const float* own = ownb + ob * NPAD * kUCols;
       const int cl = 32 * q + lane;
       const int64_t col = (t0 + lt) * kUCols + cl;
 #pragma unroll 8
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
           out[(int64_t)i * w + col] = fmaf(eps_n, fmaf(rsv[i], t, acc[j]), t);
         }
       }
-      ptx::mbar_arrive(&ownempty[lt & 1]);
+      ptx::mbar_arrive(&ownempty[ob]);
     }
   }
   ptx::tc_fence_before();
