@@ -824,7 +824,7 @@ static push_status ds_phase2(push_ctx* c, cudaStream_t s) {
     });
     if (st != PUSH_OK) return st;
   }
-  st = run_k(c, PC_DIST, 1, 4.0 * P.n * P.n * (double)P.dist.splits, 0, s, [&] {
+  st = run_k(c, PC_DIST, P.gram ? 2 : 1, 4.0 * P.n * P.n * (double)P.dist.splits, 0, s, [&] {
     if (P.gram)
       kern::gram_dist(c->dpart, P.n, P.dist.splits, c->slots, c->gsum, c->D, s);
     else
@@ -915,7 +915,7 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   const float* th = c->theta[c->cur];
   const double nd4 = 4.0 * P.n * (double)P.d;
   if (P.gram) {
-    st = run_k(c, PC_DIST, 2, nd4, 2.0 * P.n * (double)P.n * P.ld, s, [&]() -> push_status {
+    st = run_k(c, PC_DIST, 3, nd4, 2.0 * P.n * (double)P.n * P.ld, s, [&]() -> push_status {
       push_status g = kern::gram_partial(th, P.ld, P.n, P.dist.splits, c->dranges, c->dpart, s);
       if (g != PUSH_OK) return g;
       kern::gram_dist(c->dpart, P.n, P.dist.splits, c->slots, c->gsum, c->D, s);

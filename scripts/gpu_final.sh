@@ -21,7 +21,7 @@ timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:'gemm3xtf32|svgd_update|dist_|gram_|output_stream|finalize' \
   -s 40 -c 8 -o $OUT/prof python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-graph > $OUT/ncu_full.log 2>&1
 for C in C2 C3 C4 C5 S1; do
-  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed --clock-control none \
+  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active --clock-control none \
     --csv --log-file gpurun_out/traffic_$C.csv python scripts/traffic_probe.py --config $C > $OUT/traffic_$C.log 2>&1
 done
 tail -3 $OUT/pytest_gpu.log; tail -2 $OUT/smoke.log; head -c 400 $OUT/bench.json; echo; head -c 300 $OUT/bench_reference.json

@@ -2,7 +2,7 @@
 
 Run under ncu (one GPU):
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,\
-sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed --clock-control none \
+sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active --clock-control none \
       --csv --log-file gpurun_out/traffic_C2.csv python scripts/traffic_probe.py --config C2
 then, on the dev host:
   python scripts/traffic_probe.py --summarise gpurun_out/traffic_C2.csv --config C2   -> profiles/traffic_C2.json
@@ -48,7 +48,10 @@ else:
         if key not in per:
             per[key] = {"kernel": r["Kernel Name"]}
             order.append(key)
-        per[key][r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+        try:
+            per[key][r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+        except ValueError:  # "n/a"
+            pass
     kern = [per[k] for k in order][-len(trace):]
     out = {}
     for cls, k in zip(trace, kern):
@@ -59,7 +62,7 @@ else:
         tn = k.get("gpu__time_duration.sum", 0)
         e["ncu_time_ns"] += tn
         # time-weighted tensor-pipe activity (% of the elapsed peak) of the class's launches
-        e["tensor_ns"] += tn * k.get("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", 0) / 100
+        e["tensor_ns"] += tn * k.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", 0) / 100
         e["kernels"].add(k["kernel"].split("(")[0][:60])
     res = {c: {"launches": e["launches"], "dram_bytes_per_launch": e["dram_bytes"] / e["launches"],
                "ncu_time_us_per_launch": e["ncu_time_ns"] / e["launches"] / 1e3,
@@ -69,7 +72,7 @@ else:
     path = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     json.dump({"config": args.config, "source": os.path.basename(args.summarise),
                "how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
-                      "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed "
+                      "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active "
                       "--clock-control none over one eager step (scripts/traffic_probe.py)",
                "classes": res}, open(path, "w"), indent=1)
     print(json.dumps(res, indent=1))
