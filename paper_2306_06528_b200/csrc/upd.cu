@@ -1,21 +1,26 @@
-// upd.cu — a10 as a streaming tensor-core contraction with the update fused into its epilogue.
+// upd.cu — a10 as ONE streaming tensor-core contraction that produces theta' directly.
 //
 //   theta'_i = theta_i + (eps/n) [ sum_j K_ij (g_j - r theta_j) + r s_i theta_i ],  r = 2/h
 //
 // (north star; phi(theta_i) = (1/n) sum_j [K_ij grad log p(theta_j) + grad_{theta_j}
-// K_ij] with grad_{theta_j} K_ij = r (theta_i - theta_j) K_ij).  Per column c of theta the sum over j is
-// U_i[c] = sum_q lhs[i][q] B[q][c] with B = the 2n x w operand [G; Theta] (or [Theta; G], the row order
-// of the adjacent buffers) and lhs = [K, -rK] (or [-rK, K]).  The contraction runs TRANSPOSED so that the
-// streamed operand is the MMA's A (from TMEM) and the small lhs stays resident in shared memory:
-//   D[c][i] (TMEM lane c of a 128-column tile, column i) = sum_q B[q][c] lhs[i][q]   (M = 128, N = NPAD)
+// K_ij] with grad_{theta_j} K_ij = r (theta_i - theta_j) K_ij).  Every term is linear in the rows of the
+// 2n x w operand B = [G; Theta] (or [Theta; G], the row order of the adjacent buffers), so the whole
+// update is theta'_i[c] = sum_q L[i][q] B[q][c] with the folded coefficient matrix
+//   L[i][j_G]     = (eps/n) K_ij
+//   L[i][j_Theta] = -(eps/n) r K_ij + [j = own_row + i] (1 + (eps/n) r (s_i - K_ii))
+// (update_lhs_split_kernel; R29).  The contraction runs TRANSPOSED so that the streamed operand is
+// the MMA's A (from TMEM) and the small L stays resident in shared memory:
+//   D[c][i] (TMEM lane c of a 128-column tile, column i) = sum_q B[q][c] L[i][q]   (M = 128, N = NPAD)
 // 3xTF32 (both operands split hi + lo, lo*lo dropped), K = 2n <= 128: one TMEM accumulation chunk.
 //
-// One persistent CTA per SM streams whole 128-column tiles of B (each element read once from HBM):
-//   warp 0 lane 0   TMA producer: the resident lhs hi/lo (once), then 32-row x 128-column stages of B
-//   warp 1 lane 0   MMA issuer; warp 1 owns TMEM (A slots of one tile + two accumulators)
-//   warps 2-5       transform: thread = column c, 32 values of the stage -> tf32 hi / lo -> TMEM
-//   warps 6-13      epilogue: drain U[c][i]; theta_i[c] from the own rows the transform copied out of the
-//                   stages (no second read from memory); write theta'_i[c] (coalesced along c)
+// One persistent CTA per SM streams whole 128-column tiles of B (each element read once from HBM) through
+// a deep ring of 512-B-row TMA boxes (scripts/micro/tma_stream.cu: 128-column x 32-row boxes reach 0.94 of
+// the HBM copy rate at >= 128 KB in flight per SM; 32-column boxes cap at 0.66):
+//   warp 0 lane 0   TMA producer: the resident L hi/lo (once), then 32-row x 128-column stages of B
+//   warp 1 lane 0   MMA issuer; warp 1 owns TMEM (two accumulators + a ring of A slots)
+//   warps 2-9       two transform groups taking alternate stages: thread = column c, 32 values -> tf32
+//                   hi / lo -> an A slot in TMEM; the stage is released as soon as it is in registers
+//   warps 10-17     epilogue: drain theta'[c][i] and store it (coalesced along c)
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -31,70 +36,65 @@ namespace kern {
 namespace {
 constexpr int kUK = 32;                 // rows of B (K) per stage
 constexpr int kUCols = 128;             // columns per tile (M)
-constexpr int kUThreads = 32 * 14;
-constexpr int kUStages = 4;
-constexpr int kUOwnBufs = 3;            // own-theta tile buffers: the transform runs two tiles ahead
+constexpr int kUXf0 = 2, kUGroups = 2, kUEpi0 = kUXf0 + 4 * kUGroups;
+constexpr int kUThreads = 32 * (kUEpi0 + 8);
 constexpr int kUMaxKB = 4;              // 2n <= 128
 constexpr int kUStage = kUK * kUCols * 4;  // 16 KB
+constexpr int kUSmemMax = 227 * 1024;
 
 template <int NPAD>
 struct UCfg {
-  static constexpr int LTILE = NPAD * 128;                 // one k-block of lhs (hi or lo): NPAD rows x 128 B
-  static constexpr int RES = 2 * kUMaxKB * LTILE;          // resident lhs hi + lo
-  static constexpr int ASLOT0 = 2 * NPAD;                  // two accumulators, then kUMaxKB A slots of 64
+  static constexpr int LTILE = NPAD * 128;                 // one k-block of L (hi or lo): NPAD rows x 128 B
+  static constexpr int RES = 2 * kUMaxKB * LTILE;          // resident L hi + lo
+  static constexpr int STAGES = std::min(10, (kUSmemMax - 2048 - RES) / kUStage);
+  static constexpr int ASLOT0 = 2 * NPAD;                  // two accumulators, then NSLOT A slots of 64 columns
+  static constexpr int NSLOT = std::min(6, (512 - ASLOT0) / 64);
   static constexpr int CW = NPAD / 2;                      // accumulator columns per epilogue thread
-  static constexpr int OWN = NPAD * kUCols * 4;             // own theta rows of one tile (fp32)
-  static constexpr int SMEM = 1024 + RES + kUStages * kUStage + kUOwnBufs * OWN + 1024;
-  static_assert(ASLOT0 + 64 * kUMaxKB <= 512, "tmem");
-  static_assert(CW % 8 == 0, "cfg");
+  static constexpr int SMEM = 1024 + RES + STAGES * kUStage + 1024;
+  static_assert(ASLOT0 + 64 * NSLOT <= 512 && NSLOT >= kUGroups, "tmem");
+  static_assert(CW % 8 == 0 && SMEM <= kUSmemMax, "cfg");
 };
 
 template <int NPAD>
 __global__ void __launch_bounds__(kUThreads, 1)
     svgd_update_tc_kernel(const __grid_constant__ CUtensorMap tB, const __grid_constant__ CUtensorMap tLhi,
-                          const __grid_constant__ CUtensorMap tLlo, int K2, int64_t w, int rows, int own_q0,
-                          float* __restrict__ out, const float* __restrict__ srow, const float* __restrict__ hptr,
-                          float eps_n) {
+                          const __grid_constant__ CUtensorMap tLlo, int K2, int64_t w, int rows,
+                          float* __restrict__ out) {
   using C = UCfg<NPAD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* res = smem;                       // lhs hi: kb * LTILE; lhs lo: (kUMaxKB + kb) * LTILE
+  uint8_t* res = smem;                       // L hi: kb * LTILE; L lo: (kUMaxKB + kb) * LTILE
   uint8_t* stg = smem + C::RES;
-  float* ownb = reinterpret_cast<float*>(stg + kUStages * kUStage);  // [3][NPAD][128]: own theta rows of tile lt % 3
-  float* rsv = ownb + kUOwnBufs * NPAD * kUCols;                      // [NPAD]: r s_i
-  uint64_t* full = reinterpret_cast<uint64_t*>(rsv + 64);
-  uint64_t* ready = full + kUStages;
-  uint64_t* empty = ready + kUStages;
-  uint64_t* aempty = empty + kUStages;       // [kUMaxKB] A slot free
-  uint64_t* tfull = aempty + kUMaxKB;        // [2]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + C::STAGES * kUStage);
+  uint64_t* empty = full + C::STAGES;        // [STAGES] the transform has the stage in registers
+  uint64_t* aready = empty + C::STAGES;      // [NSLOT] A slot written
+  uint64_t* aempty = aready + C::NSLOT;      // [NSLOT] A slot consumed by the MMAs
+  uint64_t* tfull = aempty + C::NSLOT;       // [2]
   uint64_t* tempty = tfull + 2;              // [2]
-  uint64_t* bres = tempty + 2;               // resident lhs landed
-  uint64_t* ownfull = bres + 1;              // [3] the transform has copied tile lt's own rows
-  uint64_t* ownempty = ownfull + kUOwnBufs;  // [3] the epilogue has read them
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ownempty + kUOwnBufs);
+  uint64_t* bres = tempty + 2;               // resident L landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = (K2 + kUK - 1) / kUK;
   const int64_t ntile = w / kUCols;
   const int64_t t0 = blockIdx.x * ntile / gridDim.x, t1 = (blockIdx.x + 1) * ntile / gridDim.x;
   const int nt = (int)(t1 - t0);
+  const int nit = nt * KB;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kUStages; ++s) {
+    for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&ready[s], 128);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], 128);
     }
-    for (int j = 0; j < kUMaxKB; ++j) ptx::mbar_init(&aempty[j], 1);
+    for (int a = 0; a < C::NSLOT; ++a) {
+      ptx::mbar_init(&aready[a], 128);
+      ptx::mbar_init(&aempty[a], 1);
+    }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], 256);
     }
     ptx::mbar_init(bres, 1);
-    for (int b = 0; b < kUOwnBufs; ++b) {
-      ptx::mbar_init(&ownfull[b], 128);
-      ptx::mbar_init(&ownempty[b], 256);
-    }
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tB);
   }
@@ -102,7 +102,6 @@ __global__ void __launch_bounds__(kUThreads, 1)
     ptx::tmem_alloc(tmem_slot, 512);
     ptx::tmem_relinquish();
   }
-  if (threadIdx.x < NPAD) rsv[threadIdx.x] = threadIdx.x < rows ? (2.0f / __ldg(hptr)) * __ldg(srow + threadIdx.x) : 0.f;
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -115,15 +114,11 @@ __global__ void __launch_bounds__(kUThreads, 1)
         ptx::tma_load_3d(res + kb * C::LTILE, &tLhi, bres, kb * kUK, 0, 0);
         ptx::tma_load_3d(res + (kUMaxKB + kb) * C::LTILE, &tLlo, bres, kb * kUK, 0, 0);
       }
-      int it = 0;
-      for (int lt = 0; lt < nt; ++lt) {
-        const int c0 = (int)((t0 + lt) * kUCols);
-        for (int kb = 0; kb < KB; ++kb, ++it) {
-          const int s = it % kUStages;
-          ptx::mbar_wait(&empty[s], ((it / kUStages) & 1) ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[s], kUStage);
-          ptx::tma_load_3d(stg + s * kUStage, &tB, &full[s], c0, kb * kUK, 0);
-        }
+      for (int it = 0; it < nit; ++it) {
+        const int lt = it / KB, kb = it - lt * KB, s = it % C::STAGES;
+        ptx::mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[s], kUStage);
+        ptx::tma_load_3d(stg + s * kUStage, &tB, &full[s], (int)((t0 + lt) * kUCols), kb * kUK, 0);
       }
     }
   } else if (warp == 1) {
@@ -136,10 +131,10 @@ __global__ void __launch_bounds__(kUThreads, 1)
         ptx::mbar_wait(&tempty[b], ((lt >> 1) & 1) ^ 1);
         const uint32_t d = tmem_base + b * NPAD;
         for (int kb = 0; kb < KB; ++kb, ++it) {
-          const int s = it % kUStages;
-          ptx::mbar_wait(&ready[s], (it / kUStages) & 1);
+          const int a = it % C::NSLOT;
+          ptx::mbar_wait(&aready[a], (it / C::NSLOT) & 1);
           ptx::tc_fence_after();
-          const uint32_t ta_hi = tmem_base + C::ASLOT0 + kb * 64, ta_lo = ta_hi + 32;
+          const uint32_t ta_hi = tmem_base + C::ASLOT0 + a * 64, ta_lo = ta_hi + 32;
           const uint32_t bhi = ptx::smem_u32(res + kb * C::LTILE), blo = ptx::smem_u32(res + (kUMaxKB + kb) * C::LTILE);
 #pragma unroll
           for (int ks = 0; ks < kUK / 8; ++ks) {
@@ -148,50 +143,44 @@ __global__ void __launch_bounds__(kUThreads, 1)
             ptx::mma_tf32_ts(d, ta_hi + ks * 8, dl, idesc, 1u);
             ptx::mma_tf32_ts(d, ta_hi + ks * 8, dh, idesc, 1u);
           }
-          ptx::mma_commit(&empty[s]);
-          ptx::mma_commit(&aempty[kb]);
+          ptx::mma_commit(&aempty[a]);
         }
         ptx::mma_commit(&tfull[b]);
       }
     }
-  } else if (warp < 6) {
-    // ---------------- transform: TMEM lane = column c of the tile (quarter warp & 3)
-    const int q = warp & 3, c = 32 * q + lane;
+  } else if (warp < kUEpi0) {
+    // ---------------- transform group g: k-blocks it = g, g + 2, ...  TMEM lane = column c of the tile
+    const int g = (warp - kUXf0) >> 2, q = warp & 3, c = 32 * q + lane;
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;
-    int it = 0;
-    for (int lt = 0; lt < nt; ++lt) {
-      const int ob = lt % kUOwnBufs;
-      float* own = ownb + ob * NPAD * kUCols;
-      ptx::mbar_wait(&ownempty[ob], ((lt / kUOwnBufs) & 1) ^ 1);  // the epilogue of tile lt - 3 is done with it
-      for (int kb = 0; kb < KB; ++kb, ++it) {
-        const int s = it % kUStages;
-        ptx::mbar_wait(&full[s], (it / kUStages) & 1);
-        ptx::mbar_wait(&aempty[kb], (lt & 1) ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t st = ptx::smem_u32(stg + s * kUStage);
-        uint32_t hi[32], lo[32];
+    for (int it = g; it < nit; it += kUGroups) {
+      const int s = it % C::STAGES, a = it % C::NSLOT;
+      ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
+      const uint32_t st = ptx::smem_u32(stg + s * kUStage);
+      float x[32];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const float x = ptx::lds_f32(st + k * (kUCols * 4) + c * 4);
-          const int oi = kb * kUK + k - own_q0;  // own row index of B row kb * 32 + k
-          if (oi >= 0 && oi < rows) own[oi * kUCols + c] = x;
-          const float h = ptx::tf32_rna_fast(x);
-          hi[k] = __float_as_uint(h);
-          lo[k] = __float_as_uint(x - h);
-        }
-        const uint32_t ta = tmem_base + lane_off + C::ASLOT0 + kb * 64;
-        ptx::tmem_st_32x32b_x32(ta, hi);
-        ptx::tmem_st_32x32b_x32(ta + 32, lo);
-        ptx::tmem_st_wait();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&ready[s]);
+      for (int k = 0; k < 32; ++k) x[k] = ptx::lds_f32(st + k * (kUCols * 4) + c * 4);
+      ptx::mbar_arrive(&empty[s]);  // release-ordered after the loads: the ring slot is free for the TMA
+      uint32_t hi[32], lo[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float h = ptx::tf32_rna_fast(x[k]);
+        hi[k] = __float_as_uint(h);
+        lo[k] = __float_as_uint(x[k] - h);
       }
-      ptx::mbar_arrive(&ownfull[ob]);  // tile lt's own rows are in `own`
+      ptx::mbar_wait(&aempty[a], ((it / C::NSLOT) & 1) ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t ta = tmem_base + lane_off + C::ASLOT0 + a * 64;
+      ptx::tmem_st_32x32b_x32(ta, hi);
+      ptx::tmem_st_32x32b_x32(ta + 32, lo);
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&aready[a]);
     }
   } else {
     // ---------------- epilogue: quarter q (columns c = 32q + lane of the tile), half h of the rows i
-    const int e = warp - 6, q = warp & 3, h = e >> 2;
+    const int e = warp - kUEpi0, q = warp & 3, h = e >> 2;
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+    const int cl = 32 * q + lane;
     for (int lt = 0; lt < nt; ++lt) {
       const int b = lt & 1;
       ptx::mbar_wait(&tfull[b], (lt >> 1) & 1);
@@ -209,20 +198,12 @@ __global__ void __launch_bounds__(kUThreads, 1)
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[b]);
-      const int ob = lt % kUOwnBufs;
-      ptx::mbar_wait(&ownfull[ob], (lt / kUOwnBufs) & 1);
-      const float* own = ownb + ob * NPAD * kUCols;
-      const int cl = 32 * q + lane;
       const int64_t col = (t0 + lt) * kUCols + cl;
-#pragma unroll 8
+#pragma unroll
       for (int j = 0; j < C::CW; ++j) {
         const int i = h * C::CW + j;
-        if (i < rows) {
-          const float t = own[i * kUCols + cl];
-          out[(int64_t)i * w + col] = fmaf(eps_n, fmaf(rsv[i], t, acc[j]), t);
-        }
+        if (i < rows) out[(int64_t)i * w + col] = acc[j];
       }
-      ptx::mbar_arrive(&ownempty[ob]);
     }
   }
   ptx::tc_fence_before();
@@ -232,7 +213,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
 
 template <int NPAD>
 push_status update_tc_launch(const float* b, int n, int64_t w, int rows, const float* lhi, const float* llo, int pitch,
-                             int own_q0, float* out, const float* srow, const float* h, float eps_n, cudaStream_t s) {
+                             float* out, cudaStream_t s) {
   CUtensorMap tB, tLhi, tLlo;
   push_status st = gemm::make_map(&tB, b, (uint64_t)w, (uint64_t)(2 * n), 1, (uint64_t)w, 0, kUK,
                                   CU_TENSOR_MAP_SWIZZLE_NONE, kUCols);
@@ -249,16 +230,18 @@ push_status update_tc_launch(const float* b, int n, int64_t w, int rows, const f
   }
   const int64_t ntile = w / kUCols;
   const int grid = (int)std::min<int64_t>(ntile, gemm::sm_count() > 0 ? gemm::sm_count() : 148);
-  svgd_update_tc_kernel<NPAD><<<grid, kUThreads, UCfg<NPAD>::SMEM, s>>>(tB, tLhi, tLlo, 2 * n, w, rows, own_q0, out,
-                                                                       srow, h, eps_n);
+  svgd_update_tc_kernel<NPAD><<<grid, kUThreads, UCfg<NPAD>::SMEM, s>>>(tB, tLhi, tLlo, 2 * n, w, rows, out);
   PUSH_CUDA_TRY(cudaGetLastError());
   return PUSH_OK;
 }
 
-// lhs split: rows i < npad (zero past nl) of [K, -rK] (g_first) or [-rK, K] as tf32 hi / lo at `pitch`
-__global__ void update_lhs_split_kernel(const float* __restrict__ K, int nl, int npad, int n, int pitch,
-                                        const float* __restrict__ hptr, int g_first, float* __restrict__ hi,
-                                        float* __restrict__ lo) {
+// L split (R29): rows i < npad (zero past nl) of the folded coefficient matrix over the B rows q
+// ([G; Theta] when g_first, else [Theta; G]), as tf32 hi / lo at `pitch`:
+//   G row j:      (eps/n) K_ij
+//   Theta row j:  -(eps/n) r K_ij, plus 1 + (eps/n) r (s_i - K_ii) on the own particle j = own_row + i
+__global__ void update_lhs_split_kernel(const float* __restrict__ K, int nl, int npad, int n, int pitch, int own_row,
+                                        const float* __restrict__ hptr, const float* __restrict__ srow, float eps_n,
+                                        int g_first, float* __restrict__ hi, float* __restrict__ lo) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)npad * pitch) return;
   const int i = (int)(e / pitch), q = (int)(e - (int64_t)i * pitch);
@@ -267,7 +250,13 @@ __global__ void update_lhs_split_kernel(const float* __restrict__ K, int nl, int
     const int j = q < n ? q : q - n;
     const bool gpart = (q < n) == (g_first != 0);
     const float k = K[(int64_t)i * n + j];
-    v = gpart ? k : -(2.0f / *hptr) * k;
+    const float er = eps_n * (2.0f / *hptr);
+    if (gpart)
+      v = eps_n * k;
+    else if (j == own_row + i)
+      v = fmaf(er, srow[i] - k, 1.0f);
+    else
+      v = -er * k;
   }
   const float hv = ptx::tf32_rna_fast(v);
   hi[e] = hv;
@@ -291,13 +280,12 @@ push_status update_tc_stream(const float* b, bool g_first, int n, int64_t w, int
   if (st != PUSH_OK) return st;
   const int npad = update_tc_npad(rows), pitch = ((2 * n + 3) / 4) * 4;
   const int64_t tot = (int64_t)npad * pitch;
-  update_lhs_split_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(K, rows, npad, n, pitch, h, g_first ? 1 : 0,
-                                                                         lhs_hi, lhs_lo);
-  const int own_q0 = (g_first ? n : 0) + own_row;  // B row of the first own theta row
+  update_lhs_split_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(K, rows, npad, n, pitch, own_row, h, srow,
+                                                                         eps_n, g_first ? 1 : 0, lhs_hi, lhs_lo);
   switch (npad) {
-    case 16: return update_tc_launch<16>(b, n, w, rows, lhs_hi, lhs_lo, pitch, own_q0, out, srow, h, eps_n, s);
-    case 32: return update_tc_launch<32>(b, n, w, rows, lhs_hi, lhs_lo, pitch, own_q0, out, srow, h, eps_n, s);
-    default: return update_tc_launch<64>(b, n, w, rows, lhs_hi, lhs_lo, pitch, own_q0, out, srow, h, eps_n, s);
+    case 16: return update_tc_launch<16>(b, n, w, rows, lhs_hi, lhs_lo, pitch, out, s);
+    case 32: return update_tc_launch<32>(b, n, w, rows, lhs_hi, lhs_lo, pitch, out, s);
+    default: return update_tc_launch<64>(b, n, w, rows, lhs_hi, lhs_lo, pitch, out, s);
   }
 }
 
