@@ -11,16 +11,22 @@
 // (update_lhs_split_kernel; R29).  The contraction runs TRANSPOSED so that the streamed operand is
 // the MMA's A (from TMEM) and the small L stays resident in shared memory:
 //   D[c][i] (TMEM lane c of a 128-column tile, column i) = sum_q B[q][c] L[i][q]   (M = 128, N = NPAD)
-// 3xTF32 (both operands split hi + lo, lo*lo dropped), K = 2n <= 128: one TMEM accumulation chunk.
+// 3xTF32 (both operands split hi + lo, lo*lo dropped), K = 2n <= 128: one TMEM accumulation chunk.  The
+// MMAs read their A operand from TMEM, and that read (4 KB per MMA) rather than the math bounds a narrow
+// MMA (N = 64: ~115 cycles per MMA measured, tensor pipe 14 % active), so the three products run as TWO
+// MMAs per k-step with L's hi and lo rows stacked along N:
+//   acc[c][0 .. NPAD)       += Bhi . [Lhi]         (N = 2 NPAD: also acc[c][NPAD .. 2 NPAD) += Bhi . Llo)
+//   acc[c][0 .. NPAD)       += Blo . Lhi           (N = NPAD)
+// and the epilogue adds the two column halves: theta'_i = acc[i] + acc[NPAD + i].
 //
 // One persistent CTA per SM streams whole 128-column tiles of B (each element read once from HBM) through
 // a deep ring of 512-B-row TMA boxes (scripts/micro/tma_stream.cu: 128-column x 32-row boxes reach 0.94 of
 // the HBM copy rate at >= 128 KB in flight per SM; 32-column boxes cap at 0.66):
 //   warp 0 lane 0   TMA producer: the resident L hi/lo (once), then 32-row x 128-column stages of B
-//   warp 1 lane 0   MMA issuer; warp 1 owns TMEM (two accumulators + a ring of A slots)
+//   warp 1 lane 0   MMA issuer; warp 1 owns TMEM (two accumulators of 2 NPAD columns + a ring of A slots)
 //   warps 2-9       two transform groups taking alternate stages: thread = column c, 32 values -> tf32
 //                   hi / lo -> an A slot in TMEM; the stage is released as soon as it is in registers
-//   warps 10-17     epilogue: drain theta'[c][i] and store it (coalesced along c)
+//   warps 10-17     epilogue: drain theta'[c][i] = acc[i] + acc[NPAD + i] and store it (coalesced along c)
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -44,10 +50,11 @@ constexpr int kUSmemMax = 227 * 1024;
 
 template <int NPAD>
 struct UCfg {
-  static constexpr int LTILE = NPAD * 128;                 // one k-block of L (hi or lo): NPAD rows x 128 B
-  static constexpr int RES = 2 * kUMaxKB * LTILE;          // resident L hi + lo
+  static constexpr int LTILE = 2 * NPAD * 128;             // one k-block of L: [hi; lo] rows (2 NPAD) x 128 B
+  static constexpr int RES = kUMaxKB * LTILE;              // resident L
   static constexpr int STAGES = std::min(10, (kUSmemMax - 2048 - RES) / kUStage);
-  static constexpr int ASLOT0 = 2 * NPAD;                  // two accumulators, then NSLOT A slots of 64 columns
+  static constexpr int ACC = 2 * NPAD;                     // accumulator columns (N of the stacked MMA)
+  static constexpr int ASLOT0 = 2 * ACC;                   // two accumulators, then NSLOT A slots of 64 columns
   static constexpr int NSLOT = std::min(6, (512 - ASLOT0) / 64);
   static constexpr int CW = NPAD / 2;                      // accumulator columns per epilogue thread
   static constexpr int SMEM = 1024 + RES + STAGES * kUStage + 1024;
@@ -63,7 +70,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
   using C = UCfg<NPAD>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* res = smem;                       // L hi: kb * LTILE; L lo: (kUMaxKB + kb) * LTILE
+  uint8_t* res = smem;                       // k-block kb of L at kb * LTILE: hi rows, then lo rows
   uint8_t* stg = smem + C::RES;
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + C::STAGES * kUStage);
   uint64_t* empty = full + C::STAGES;        // [STAGES] the transform has the stage in registers
@@ -109,10 +116,10 @@ __global__ void __launch_bounds__(kUThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
-      ptx::mbar_arrive_expect_tx(bres, 2 * KB * C::LTILE);
+      ptx::mbar_arrive_expect_tx(bres, KB * C::LTILE);
       for (int kb = 0; kb < KB; ++kb) {
         ptx::tma_load_3d(res + kb * C::LTILE, &tLhi, bres, kb * kUK, 0, 0);
-        ptx::tma_load_3d(res + (kUMaxKB + kb) * C::LTILE, &tLlo, bres, kb * kUK, 0, 0);
+        ptx::tma_load_3d(res + kb * C::LTILE + NPAD * 128, &tLlo, bres, kb * kUK, 0, 0);
       }
       for (int it = 0; it < nit; ++it) {
         const int lt = it / KB, kb = it - lt * KB, s = it % C::STAGES;
@@ -123,25 +130,24 @@ __global__ void __launch_bounds__(kUThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer: tile lt into accumulator lt & 1
-      constexpr uint32_t idesc = ptx::idesc_tf32(128, NPAD, false, false);
+      constexpr uint32_t idesc2 = ptx::idesc_tf32(128, 2 * NPAD, false, false), idesc1 = ptx::idesc_tf32(128, NPAD, false, false);
       ptx::mbar_wait(bres, 0);
       int it = 0;
       for (int lt = 0; lt < nt; ++lt) {
         const int b = lt & 1;
         ptx::mbar_wait(&tempty[b], ((lt >> 1) & 1) ^ 1);
-        const uint32_t d = tmem_base + b * NPAD;
+        const uint32_t d = tmem_base + b * C::ACC;
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int a = it % C::NSLOT;
           ptx::mbar_wait(&aready[a], (it / C::NSLOT) & 1);
           ptx::tc_fence_after();
           const uint32_t ta_hi = tmem_base + C::ASLOT0 + a * 64, ta_lo = ta_hi + 32;
-          const uint32_t bhi = ptx::smem_u32(res + kb * C::LTILE), blo = ptx::smem_u32(res + (kUMaxKB + kb) * C::LTILE);
+          const uint32_t lb = ptx::smem_u32(res + kb * C::LTILE);
 #pragma unroll
           for (int ks = 0; ks < kUK / 8; ++ks) {
-            const uint64_t dh = ptx::umma_desc(bhi + ks * 32, 16, 1024, 2), dl = ptx::umma_desc(blo + ks * 32, 16, 1024, 2);
-            ptx::mma_tf32_ts(d, ta_lo + ks * 8, dh, idesc, (kb == 0 && ks == 0) ? 0u : 1u);
-            ptx::mma_tf32_ts(d, ta_hi + ks * 8, dl, idesc, 1u);
-            ptx::mma_tf32_ts(d, ta_hi + ks * 8, dh, idesc, 1u);
+            const uint64_t dl = ptx::umma_desc(lb + ks * 32, 16, 1024, 2);  // rows [Lhi; Llo] (N = 2 NPAD) or Lhi
+            ptx::mma_tf32_ts(d, ta_hi + ks * 8, dl, idesc2, (kb == 0 && ks == 0) ? 0u : 1u);
+            ptx::mma_tf32_ts(d, ta_lo + ks * 8, dl, idesc1, 1u);
           }
           ptx::mma_commit(&aempty[a]);
         }
@@ -188,13 +194,16 @@ __global__ void __launch_bounds__(kUThreads, 1)
       float acc[C::CW];
 #pragma unroll
       for (int cb = 0; cb < C::CW; cb += 8) {
-        uint32_t v[8];
+        uint32_t v[8], u[8];
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                     : "r"(lane_base + b * NPAD + h * C::CW + cb));
+                     : "r"(lane_base + b * C::ACC + h * C::CW + cb));
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7])
+                     : "r"(lane_base + b * C::ACC + NPAD + h * C::CW + cb));
         ptx::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[cb + j] = __uint_as_float(v[j]);
+        for (int j = 0; j < 8; ++j) acc[cb + j] = __uint_as_float(v[j]) + __uint_as_float(u[j]);
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[b]);

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(64, 1) ring_kernel(const __grid_constant__ CUt
   __syncthreads();
   const long long c0 = blockIdx.x * cols_per_cta;
   // steps: column blocks x row groups
-  const int rgroups = (mode == 0) ? 1 : nrows / (R * (mode == 1 ? nbox : 1));
+  const int rgroups = (mode == 0 || mode == 3) ? 1 : nrows / (R * (mode == 1 ? nbox : 1));
   const int csteps = (int)(cols_per_cta / cols_per_stage);
   const int nst = csteps * rgroups;
   if (warp == 0) {
@@ -58,6 +58,11 @@ __global__ void __launch_bounds__(64, 1) ring_kernel(const __grid_constant__ CUt
           for (int j = 0; j < nbox; ++j)
             ptx::tma_load_3d(smem + s * stage_bytes + j * (R * 512), &map, &full[s], (int)col,
                              (rg * nbox + j) * R, 0);
+        }
+      } else if (mode == 3) {
+        if (lane == 0) {
+          ptx::mbar_arrive_expect_tx(&full[s], stage_bytes);
+          ptx::tma_load_3d(smem + s * stage_bytes, &map, &full[s], (int)col, 0, 0);
         }
       } else {
         const int seg = cols_per_stage * 4;
@@ -149,7 +154,24 @@ int main() {
   };
   cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   char name[128];
-  for (int per_sm : {1, 2, 3, 4}) {
+  for (int bw : {128, 132, 136, 144}) {
+    for (int R : {32, 64}) {
+      for (int stages : {3, 4, 6}) {
+        const int sb = bw * R * 4;
+        if (stages * sb > 224 * 1024) continue;
+        CUtensorMap m;
+        mkmap(&m, bw, R, CU_TENSOR_MAP_SWIZZLE_NONE);
+        const int grid = 148, cps = 128;
+        const long long cpc = (ld / grid) / cps * cps;
+        const double bytes = 4.0 * R * cpc * grid;
+        snprintf(name, sizeof name, "padded box %dx%d stages %d (%d KB)", bw, R, stages, stages * sb / 1024);
+        timeit([&] {
+          ring_kernel<<<grid, 64, stages * sb + 2048>>>(m, th, ld, 3, R, 1, sb, stages, cpc, cps, R, sink);
+        }, bytes, name);
+      }
+    }
+  }
+  for (int per_sm : {1, 2}) {
     const int grid = 148 * per_sm;
     const int budget = (224 / per_sm) * 1024;  // ring bytes per CTA
     // mode 0: gram pattern
