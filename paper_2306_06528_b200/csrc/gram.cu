@@ -17,12 +17,18 @@
 //
 // One CTA streams one column split of Theta (the split plan's ranges, fixed by (n, ld) only, so the
 // partials are the same whichever rank computes them: P-invariance, NEXT-4) for one i-block:
-//   warp 0 lane 0   TMA producer: NP x 32 fp32 tiles (SWIZZLE_128B, K-major) into a STAGES ring
+//   warp 0 lane 0   TMA producer: raw stages of RC columns x NP rows, unswizzled, at a padded row pitch of
+//                   RC + 4 floats (the box over-reads 4 columns): 512-B row requests keep the ring at the HBM
+//                   rate (scripts/micro/tma_stream.cu: 32-column SWIZZLE_128B boxes cap at ~0.5-0.66 of the
+//                   copy rate, 128 + 4-column boxes reach 0.95), and the 16-B row skew makes the transform's
+//                   row-wise reads conflict-free
 //   warp 1 lane 0   MMA issuer (tcgen05.mma kind::tf32, A from TMEM, B from smem); warp 1 owns TMEM
-//   warps 2-5       transform: centre, split, A rows -> TMEM (tcgen05.st), B tile -> Hi in place
-//   warps 6-13      epilogue: TMEM partial added into fp32 registers every 128 of K (the tensor-core
+//   warps 2-9       two transform groups taking alternate raw stages: per k-block (32 columns) centre,
+//                   split, A rows -> a TMEM slot (tcgen05.st), Hi rows -> a SWIZZLE_128B K-major B tile; the
+//                   raw stage is released as soon as it has been read, the slot / tile by the MMA commit
+//   warps 10-17     epilogue: TMEM partial added into fp32 registers every 128 of K (the tensor-core
 //                   accumulator truncates each add), then the split's [X; Y] block stored to `part`
-// The reduction over splits and the distance formula run in gram_dist_kernel (fixed ascending order).
+// The reduction over splits and the distance formula run in gram_dist (fixed ascending order).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -37,73 +43,75 @@ namespace kern {
 
 namespace {
 constexpr int kGBK = 32;              // fp32 of K per k-block (one 128-B SWIZZLE_128B row per particle)
-constexpr int kGGroups = 2;           // transform groups (4 warps each) taking alternate stages
+constexpr int kGGroups = 2;           // transform groups (4 warps each) taking alternate raw stages
 constexpr int kGXf0 = 2, kGEpi0 = kGXf0 + 4 * kGGroups;
 constexpr int kGThreads = 32 * (kGEpi0 + 8);  // + 8 epilogue warps
-constexpr int kGSmemTiles = 192 * 1024;
+constexpr int kGSmemMax = 227 * 1024;
 
-// A stage carries KPS k-blocks (every per-stage barrier round trip — TMA landing, transform, MMA
-// issue, commit — amortised over 4 k-blocks: one k-block per stage measured 0.5 us per k-block at S1,
-// latency-bound) and equals the fp32 promotion chunk, so one accumulator drain per stage.
 template <int NP>
 struct GCfg {
-  static constexpr int KPS = NP <= 64 ? 4 : (NP <= 128 ? 2 : 1);  // k-blocks per stage (<= 128 of K)
-  static constexpr int TILE = NP * kGBK * 4;                  // one k-block: NP rows x 128 B
-  static constexpr int STAGE = KPS * TILE;
-  static constexpr int CHUNK = 4 / KPS;                        // stages per accumulation chunk (128 of K)
-  static constexpr int STAGES = std::min(8, kGSmemTiles / STAGE);
+  static constexpr int RC = NP <= 64 ? 128 : (NP == 128 ? 64 : 32);  // raw columns per stage
+  static constexpr int KPS = RC / kGBK;                        // k-blocks per raw stage
+  static constexpr int PITCH = (RC + 4) * 4;                   // raw row pitch (bytes): 16-B skew per row
+  static constexpr int RAW = NP * PITCH;                       // one raw stage
+  static constexpr int TILE = NP * kGBK * 4;                   // one B tile (k-block): NP rows x 128 B
   static constexpr int NACC = NP <= 128 ? 2 : 1;               // TMEM accumulators of NP columns
-  static constexpr int ASET = KPS * 32;                      // TMEM columns of one stage's A operand
-  static constexpr int ASLOT0 = NACC * NP;                     // NSET A sets (stage i uses set i % NSET)
-  static constexpr int NSET = std::min(4, (512 - ASLOT0) / ASET);
+  static constexpr int ASLOT0 = NACC * NP;                     // NE entries of KPS A slots of 32 columns
+  // ring of NE entries, one per raw stage: its KPS A slots (TMEM) and KPS B tiles (smem); one barrier
+  // round trip (transform -> MMA -> transform) per stage, not per k-block
+  static constexpr int NE = std::min(4, std::min((512 - ASLOT0) / (32 * KPS), 98304 / (KPS * TILE)));
+  static constexpr int STAGES = std::min(12, (kGSmemMax - 3072 - NE * KPS * TILE) / RAW);
   static constexpr int CW = NP >= 32 ? NP / 2 : 16;            // accumulator columns per epilogue thread
   static constexpr int EPI_SPLIT = NP / CW;                    // epilogue warps per TMEM lane quarter
   static constexpr int OUTER = NP > 64 ? (NP - 64) * 8 / 128 : 0;  // 16-B units per thread outside the i-block
-  static constexpr int SMEM = 1024 + STAGES * (STAGE + 512) + 512;
-  static_assert(NSET >= kGGroups && ASLOT0 + ASET * NSET <= 512, "tmem");
-  static_assert(CW % 16 == 0 && STAGES >= 2 && STAGES % kGGroups == 0, "cfg");
+  static constexpr int SMEM = 1024 + NE * KPS * TILE + STAGES * RAW + 1024;
+  static_assert(ASLOT0 + 32 * KPS * NE <= 512, "tmem");
+  static_assert(CW % 16 == 0 && STAGES >= 2 && NE >= 2 && SMEM <= kGSmemMax, "cfg");
 };
 
 // TMEM lane L of the A operand / accumulator <-> i-block row and part: lane quarter q holds rows
 // 16q .. 16q + 15, lane 2r' the Hi (X) and lane 2r' + 1 the Lo (Y) of row 16q + r'.  Hi and Lo of a row
-// sit in the SAME warp, so the pair syncs with __syncwarp before the raw row is overwritten in place.
+// sit in the SAME warp (adjacent lanes read the same raw row: a broadcast).
 __device__ __forceinline__ int lane_row(int q, int lane) { return 16 * q + (lane >> 1); }
 
 template <int NP>
 __global__ void __launch_bounds__(kGThreads, 1)
-    gram_partial_kernel(const __grid_constant__ CUtensorMap tTh, const __grid_constant__ CUtensorMap tC,
-                        const int64_t* __restrict__ ranges, int n, int n_ib, float* __restrict__ part) {
+    gram_partial_kernel(const __grid_constant__ CUtensorMap tTh, const int64_t* __restrict__ ranges, int n, int n_ib,
+                        float* __restrict__ part) {
   using C = GCfg<NP>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* cbuf = smem + C::STAGES * C::STAGE;  // [STAGES][128] fp32: row 0 (the centre c) of the stage
-  uint64_t* full = reinterpret_cast<uint64_t*>(cbuf + C::STAGES * 512);
-  uint64_t* ready = full + C::STAGES;
-  uint64_t* empty = ready + C::STAGES;
-  uint64_t* aempty = empty + C::STAGES;  // [NSET] A set free
-  uint64_t* tfull = aempty + C::NSET;
+  uint8_t* btile = smem;                       // [NE][KPS] B tiles (SWIZZLE_128B, 1024-B aligned)
+  uint8_t* raw = smem + C::NE * C::KPS * C::TILE;  // [STAGES] raw stages
+  uint64_t* full = reinterpret_cast<uint64_t*>(raw + C::STAGES * C::RAW);
+  uint64_t* empty = full + C::STAGES;          // raw stage read by its transform group
+  uint64_t* ready = empty + C::STAGES;         // [NE] A slots + B tiles of a stage written
+  uint64_t* freed = ready + C::NE;             // [NE] consumed by the MMAs
+  uint64_t* tfull = freed + C::NE;
   uint64_t* tempty = tfull + C::NACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::NACC);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, ib = blockIdx.y;
   const int64_t c0 = ranges[2 * split], c1 = ranges[2 * split + 1];
-  const int nst = (int)((c1 - c0) / (kGBK * C::KPS));  // ranges are whole 128-column units
+  const int nst = (int)((c1 - c0) / C::RC);  // ranges are whole 128-column units
+  const int nkb = nst * C::KPS;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&ready[s], 128);  // the 4 warps of the group that transforms stage s
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], 128);
     }
-    for (int j = 0; j < C::NSET; ++j) ptx::mbar_init(&aempty[j], 1);
+    for (int e = 0; e < C::NE; ++e) {
+      ptx::mbar_init(&ready[e], 128);
+      ptx::mbar_init(&freed[e], 1);
+    }
     for (int b = 0; b < C::NACC; ++b) {
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], 32 * 4 * C::EPI_SPLIT);
     }
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tTh);
-    ptx::prefetch_tmap(&tC);
   }
   if (warp == 1) {
     ptx::tmem_alloc(tmem_slot, 512);
@@ -115,123 +123,108 @@ __global__ void __launch_bounds__(kGThreads, 1)
   const uint32_t tmem_base = ptx::lds_u32(ptx::smem_u32(tmem_slot));
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer: C::KPS tiles of rows 0..NP-1 (OOB rows zero-filled) per stage and
-      // the stage's 128 columns of row 0 (the centre)
+    if (lane == 0) {  // ---------------- TMA producer: RC (+4) columns of rows 0..NP-1 (OOB zero-filled)
       for (int i = 0; i < nst; ++i) {
         const int s = i % C::STAGES;
-        const int k = (int)(c0 + (int64_t)i * kGBK * C::KPS);
         ptx::mbar_wait(&empty[s], ((i / C::STAGES) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[s], C::STAGE + 128 * C::KPS);
-#pragma unroll
-        for (int j = 0; j < C::KPS; ++j)
-          ptx::tma_load_3d(smem + s * C::STAGE + j * C::TILE, &tTh, &full[s], k + j * kGBK, 0, 0);
-        ptx::tma_load_3d(cbuf + s * 512, &tC, &full[s], k, 0, 0);
+        ptx::mbar_arrive_expect_tx(&full[s], C::RAW);
+        ptx::tma_load_3d(raw + s * C::RAW, &tTh, &full[s], (int)(c0 + (int64_t)i * C::RC), 0, 0);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer: CHUNK stages = one accumulation chunk into buffer ch % NACC
+    if (lane == 0) {  // ---------------- MMA issuer: per raw stage; 4 k-blocks (128 of K) = one accumulation chunk
       constexpr uint32_t idesc = ptx::idesc_tf32(128, NP, false, false);
       int ch = 0;
       for (int i = 0; i < nst; ++i) {
-        const bool first = i % C::CHUNK == 0, last = i % C::CHUNK == C::CHUNK - 1 || i == nst - 1;
-        const int b = ch % C::NACC, s = i % C::STAGES, g = i % C::NSET;
-        if (first) ptx::mbar_wait(&tempty[b], ((ch / C::NACC) & 1) ^ 1);
-        ptx::mbar_wait(&ready[s], (i / C::STAGES) & 1);
+        const int e = i % C::NE;
+        ptx::mbar_wait(&ready[e], (i / C::NE) & 1);
         ptx::tc_fence_after();
-        const uint32_t d = tmem_base + b * NP;
-        const uint32_t ta = tmem_base + C::ASLOT0 + g * C::ASET;
 #pragma unroll
         for (int j = 0; j < C::KPS; ++j) {
-          const uint32_t bb = ptx::smem_u32(smem + s * C::STAGE + j * C::TILE);
+          const int k = i * C::KPS + j;
+          const bool first = (k & 3) == 0, last = (k & 3) == 3 || k == nkb - 1;
+          const int b = ch % C::NACC;
+          if (first) {
+            ptx::mbar_wait(&tempty[b], ((ch / C::NACC) & 1) ^ 1);
+            ptx::tc_fence_after();
+          }
+          const uint32_t d = tmem_base + b * NP, ta = tmem_base + C::ASLOT0 + (e * C::KPS + j) * 32;
+          const uint32_t bb = ptx::smem_u32(btile + (e * C::KPS + j) * C::TILE);
 #pragma unroll
           for (int ks = 0; ks < kGBK / 8; ++ks)
-            ptx::mma_tf32_ts(d, ta + j * 32 + ks * 8, ptx::umma_desc(bb + ks * 32, 16, 1024, 2), idesc,
-                             (first && j == 0 && ks == 0) ? 0u : 1u);
+            ptx::mma_tf32_ts(d, ta + ks * 8, ptx::umma_desc(bb + ks * 32, 16, 1024, 2), idesc,
+                             (first && ks == 0) ? 0u : 1u);
+          if (last) {
+            ptx::mma_commit(&tfull[b]);
+            ++ch;
+          }
         }
-        ptx::mma_commit(&empty[s]);
-        ptx::mma_commit(&aempty[g]);
-        if (last) {
-          ptx::mma_commit(&tfull[b]);
-          ++ch;
-        }
+        ptx::mma_commit(&freed[e]);
       }
     }
   } else if (warp < kGEpi0) {
-    // ---------------- transform group g: stages g, g + kGGroups, ... into A set i % NSET.  Thread: TMEM lane
-    // 32q + lane = Hi or Lo of i-block row lane_row(q, lane); the Hi thread writes the row's Hi back in
-    // place (the B operand).  Rows of the tile outside the i-block (n > 64) are converted unit by unit.
+    // ---------------- transform group g: raw stages g, g + 2, ...  Thread: TMEM lane 32q + lane = Hi or Lo
+    // of i-block row lane_row(q, lane); the Hi thread also writes the row's Hi into the B tile.  Rows of the
+    // tile outside the i-block (n > 64) are converted 16-B unit by unit.
     const int g = (warp - kGXf0) >> 2, q = warp & 3, t = threadIdx.x - 32 * (kGXf0 + 4 * g);
     const int arow = ib * 64 + lane_row(q, lane);
     const bool want_lo = lane & 1;
     const bool in_tile = arow < NP;
     const bool live = arow < n;
     for (int i = g; i < nst; i += kGGroups) {
-      const int s = i % C::STAGES, set = i % C::NSET;
-      const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + C::ASLOT0 + set * C::ASET;
+      const int s = i % C::STAGES;
+      const int e = i % C::NE;
+      const uint32_t rs = ptx::smem_u32(raw + s * C::RAW);
       ptx::mbar_wait(&full[s], (i / C::STAGES) & 1);
-      ptx::mbar_wait(&aempty[set], ((i / C::NSET) & 1) ^ 1);
-      ptx::tc_fence_after();
-      const uint32_t cs = ptx::smem_u32(cbuf + s * 512);
 #pragma unroll 1
       for (int j = 0; j < C::KPS; ++j) {
-        const uint32_t st = ptx::smem_u32(smem + s * C::STAGE + j * C::TILE);
+        const uint32_t bt = ptx::smem_u32(btile + (e * C::KPS + j) * C::TILE);
         uint32_t a[32];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) a[k] = 0u;
+        for (int u = 0; u < 32; ++u) a[u] = 0u;
         if (live) {
-          float4 v[8], cv[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
-            cv[u] = ptx::lds_f4(cs + j * 128 + (u << 4));
-            v[u] = ptx::lds_f4(st + arow * 128 + ((u ^ (arow & 7)) << 4));
-          }
+            const float4 cv = ptx::lds_f4(rs + j * 128 + (u << 4));
+            const float4 v = ptx::lds_f4(rs + arow * C::PITCH + j * 128 + (u << 4));
+            const float xv[4] = {v.x - cv.x, v.y - cv.y, v.z - cv.z, v.w - cv.w};
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const float xv[4] = {v[u].x - cv[u].x, v[u].y - cv[u].y, v[u].z - cv[u].z, v[u].w - cv[u].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float h = ptx::tf32_rna_fast(xv[e]);
-              a[4 * u + e] = __float_as_uint(want_lo ? xv[e] - h : h);
+            for (int ee = 0; ee < 4; ++ee) {
+              const float h = ptx::tf32_rna_fast(xv[ee]);
+              a[4 * u + ee] = __float_as_uint(want_lo ? xv[ee] - h : h);
             }
           }
         }
-        ptx::tmem_st_32x32b_x32(ta + j * 32, a);
-        __syncwarp();  // the Lo thread of the pair has read the raw row
+        if (j == 0) ptx::mbar_wait(&freed[e], ((i / C::NE) & 1) ^ 1);  // entry e (A slots, B tiles) is free
+        if constexpr (C::OUTER > 0) {
+#pragma unroll 4
+          for (int m = 0; m < C::OUTER; ++m) {
+            const int u = t + 128 * m, ro = u >> 3, cc = u & 7;
+            const int r = ro < ib * 64 ? ro : ro + 64;  // skip the i-block's own 64 rows
+            const float4 x = ptx::lds_f4(rs + r * C::PITCH + j * 128 + cc * 16);
+            const float4 c = ptx::lds_f4(rs + j * 128 + cc * 16);
+            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (r < n)
+              o = make_float4(ptx::tf32_rna_fast(x.x - c.x), ptx::tf32_rna_fast(x.y - c.y),
+                              ptx::tf32_rna_fast(x.z - c.z), ptx::tf32_rna_fast(x.w - c.w));
+            ptx::sts_f4(bt + r * 128 + ((cc ^ (r & 7)) << 4), o);
+          }
+        }
+        if (j == C::KPS - 1) ptx::mbar_arrive(&empty[s]);  // every read of the raw stage is done above
+        ptx::tc_fence_after();
+        ptx::tmem_st_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + C::ASLOT0 + (e * C::KPS + j) * 32, a);
         if (!want_lo && in_tile) {
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            ptx::sts_f4(st + arow * 128 + ((u ^ (arow & 7)) << 4),
+            ptx::sts_f4(bt + arow * 128 + ((u ^ (arow & 7)) << 4),
                         make_float4(__uint_as_float(a[4 * u]), __uint_as_float(a[4 * u + 1]),
                                     __uint_as_float(a[4 * u + 2]), __uint_as_float(a[4 * u + 3])));
-        }
-        if constexpr (C::OUTER > 0) {
-          float4 v[C::OUTER];
-          uint32_t ad[C::OUTER];
-          int rows[C::OUTER];
-#pragma unroll
-          for (int k = 0; k < C::OUTER; ++k) {
-            const int u = t + 128 * k, ro = u >> 3, cc = u & 7;
-            const int r = ro < ib * 64 ? ro : ro + 64;  // skip the i-block's own 64 rows
-            rows[k] = r;
-            ad[k] = st + r * 128 + ((cc ^ (r & 7)) << 4);
-            v[k] = ptx::lds_f4(ad[k]);
-          }
-#pragma unroll
-          for (int k = 0; k < C::OUTER; ++k) {
-            const float4 c4 = ptx::lds_f4(cs + j * 128 + ((t + 128 * k) & 7) * 16);
-            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (rows[k] < n)
-              o = make_float4(ptx::tf32_rna_fast(v[k].x - c4.x), ptx::tf32_rna_fast(v[k].y - c4.y),
-                              ptx::tf32_rna_fast(v[k].z - c4.z), ptx::tf32_rna_fast(v[k].w - c4.w));
-            ptx::sts_f4(ad[k], o);
-          }
         }
       }
       ptx::tmem_st_wait();
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&ready[s]);
+      ptx::mbar_arrive(&ready[e]);
     }
   } else {
     // ---------------- epilogue: quarter q of the 128 lanes, column half h
@@ -241,7 +234,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       float acc[C::CW];
 #pragma unroll
       for (int j = 0; j < C::CW; ++j) acc[j] = 0.f;
-      const int nch = (nst + C::CHUNK - 1) / C::CHUNK;
+      const int nch = (nkb + 3) / 4;
       for (int i = 0; i < nch; ++i) {
         const int b = i % C::NACC;
         ptx::mbar_wait(&tfull[b], (i / C::NACC) & 1);
@@ -273,21 +266,18 @@ __global__ void __launch_bounds__(kGThreads, 1)
 template <int NP>
 push_status gram_launch(const float* theta, int64_t ld, int n, int splits, const int64_t* ranges, float* part,
                         cudaStream_t s) {
-  CUtensorMap map, cmap;
+  using C = GCfg<NP>;
+  CUtensorMap map;
   push_status st = gemm::make_map(&map, theta, (uint64_t)ld, (uint64_t)n, 1, (uint64_t)ld, 0, NP,
-                                  CU_TENSOR_MAP_SWIZZLE_128B);
-  if (st != PUSH_OK) return st;
-  st = gemm::make_map(&cmap, theta, (uint64_t)ld, 1, 1, (uint64_t)ld, 0, 1, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      kGBK * GCfg<NP>::KPS);
+                                  CU_TENSOR_MAP_SWIZZLE_NONE, C::RC + 4);
   if (st != PUSH_OK) return st;
   static bool attr = false;
   if (!attr) {
-    PUSH_CUDA_TRY(cudaFuncSetAttribute(gram_partial_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       GCfg<NP>::SMEM));
+    PUSH_CUDA_TRY(cudaFuncSetAttribute(gram_partial_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
   const int n_ib = (n + 63) / 64;
-  gram_partial_kernel<NP><<<dim3(splits, n_ib), kGThreads, GCfg<NP>::SMEM, s>>>(map, cmap, ranges, n, n_ib, part);
+  gram_partial_kernel<NP><<<dim3(splits, n_ib), kGThreads, C::SMEM, s>>>(map, ranges, n, n_ib, part);
   PUSH_CUDA_TRY(cudaGetLastError());
   return PUSH_OK;
 }
