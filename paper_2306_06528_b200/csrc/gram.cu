@@ -34,6 +34,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "gram_d.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
 #include "tma_host.h"
@@ -366,8 +367,7 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const float* __restric
   }
 }
 
-// D_ij = D_ji = max(G_ii + G_jj - 2 G_ij, 0) for i < j, D_ii = +0, with G_ab = (SX_ab + SY_ab) + SY_ba
-// (SX / SY: the summed X / Y blocks; row a of i-block a/64 at (a/64)*128 + a%64, Y 64 rows further)
+// D_ij = D_ji (gram_d_value, gram_d.cuh) for i < j, D_ii = +0
 __global__ void gram_d_kernel(const float* __restrict__ sums, int n, int np, float* __restrict__ D) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)n * n) return;
@@ -377,19 +377,17 @@ __global__ void gram_d_kernel(const float* __restrict__ sums, int n, int np, flo
     D[e] = 0.f;
     return;
   }
-  auto xrow = [&](int a) { return ((int64_t)(a >> 6) * 128 + (a & 63)) * np; };
-  const int64_t xi = xrow(i), xj = xrow(j), yo = 64 * (int64_t)np;
-  const float gij = (sums[xi + j] + sums[xi + yo + j]) + sums[xj + yo + i];
-  const float gii = (sums[xi + i] + sums[xi + yo + i]) + sums[xi + yo + i];
-  const float gjj = (sums[xj + j] + sums[xj + yo + j]) + sums[xj + yo + j];
-  const float d = fmaxf(fmaf(-2.0f, gij, gii + gjj), 0.f);
+  const float d = gram_d_value(sums, np, i, j);
   D[e] = d;
   D[(int64_t)j * n + i] = d;
 }
 
+bool gram_d_in_bandwidth(int n) { return n <= kGramDInBandwidth; }
+
 void gram_dist(const float* part, int n, int S, const RankSlots& rs, float* sums, float* D, cudaStream_t s) {
   const int64_t pb = gram_part_floats(n);
   gram_reduce_kernel<<<(unsigned)((pb + 31) / 32), 256, 0, s>>>(part, pb, S, rs, sums);
+  if (gram_d_in_bandwidth(n)) return;  // the bandwidth kernel evaluates D while staging its keys
   const int64_t nn = (int64_t)n * n;
   gram_d_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(sums, n, gram_np(n), D);
 }

@@ -143,14 +143,19 @@ int64_t gram_part_floats(int n);    // floats of one split's partial block: ceil
 push_status gram_partial(const float* theta, int64_t ld, int n, int splits, const int64_t* ranges_dev, float* part,
                          cudaStream_t s);
 // sums = the S split blocks summed in ascending order (split s's block at slot rs(s), as dist_reduce;
-// gram_part_floats(n) floats), then D_ij = D_ji = max(G_ii + G_jj - 2 G_ij, 0), D_ii = +0 (two launches)
+// gram_part_floats(n) floats), then (n > kGramDInBandwidth) D_ij = D_ji = max(G_ii + G_jj - 2 G_ij, 0), D_ii = +0;
+// for smaller n the bandwidth kernel evaluates D from the sums (bandwidth_kernel's gsums argument)
+constexpr int kGramDInBandwidth = 128;
+bool gram_d_in_bandwidth(int n);
 void gram_dist(const float* part, int n, int S, const RankSlots& rs, float* sums, float* D, cudaStream_t s);
 
 // ---------------------------------------------------------------- a8 + a9 bandwidth and kernel matrix
 // Per tensor t (one CTA each): h_t from D_t (rule, c = fp32 1/ln n or 1/ln(n+1), or fixed bw_h);
 // K[t][i][j] = exp(-D_t[row0+i][j]/h_t), srow[t][i] = sum_j K[t][i][j]
+// gsums != nullptr (Gram form, one tensor, n <= kGramDInBandwidth): D is first evaluated from the summed Gram
+// blocks (gram_np(n) columns) and written to D, then used as above.
 void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c_ln, float bw_h, float* h, float* K,
-                      float* srow, int tensors, cudaStream_t s);
+                      float* srow, int tensors, cudaStream_t s, const float* gsums = nullptr);
 
 // ---------------------------------------------------------------- a10 fused update
 // theta_next[row0+i][c] = theta_i[c] + (eps/n)[ sum_j K_ij (g_j[c] - r theta_j[c]) + r s_i theta_i[c] ], r = 2/h

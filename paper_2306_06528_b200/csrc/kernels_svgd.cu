@@ -11,6 +11,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "gram_d.cuh"
 #include "kernels.h"
 
 namespace push {
@@ -581,10 +582,12 @@ __device__ __forceinline__ void kernel_row(const float* __restrict__ D, int n, i
   for (int m = 16; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
   if (lane == 0) srow[i] = acc;
 }
-__global__ void __launch_bounds__(1024) bandwidth_kernel_impl(const float* __restrict__ D, int n, int row0, int nl,
+// D is written here in the Gram mode (gsums), so it is neither const nor __restrict__ (no read-only cache path)
+__global__ void __launch_bounds__(1024) bandwidth_kernel_impl(float* D, int n, int row0, int nl,
                                                               int rule, float c_ln, float bw_h, float* __restrict__ h_out,
                                                               float* __restrict__ K, float* __restrict__ srow,
-                                                              int use_tri, int krows_here) {
+                                                              int use_tri, int krows_here,
+                                                              const float* __restrict__ gsums, int gnp) {
   extern __shared__ float skeys[];
   // CTA b: tensor b's distance matrix, bandwidth, kernel rows and row sums
   D += (int64_t)blockIdx.x * n * n;
@@ -598,6 +601,24 @@ __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(const float* __res
   __shared__ float cand[1024];           // the selected bin's keys
   __shared__ float s_h;
   const int64_t N = (int64_t)n * n;
+  if (gsums != nullptr) {
+    // Gram form (one tensor): D from the summed Gram blocks, written to D (K rows and push_gather read it)
+    // and, when the keys are staged, straight into skeys (strictly-upper row-major, as the staging below)
+    float* Dw = D;
+    for (int64_t e = threadIdx.x; e < N; e += blockDim.x) {
+      const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
+      if (j < i) continue;
+      if (j == i) {
+        Dw[e] = 0.f;
+        continue;
+      }
+      const float d = gram_d_value(gsums, gnp, i, j);
+      Dw[e] = d;
+      Dw[(int64_t)j * n + i] = d;
+      if (use_tri) skeys[(int64_t)i * n - (int64_t)i * (i + 1) / 2 + (j - i - 1)] = d;
+    }
+    __syncthreads();  // D (global) and the keys are visible to the whole CTA
+  }
   if (rule == PUSH_BW_FIXED) {
     if (threadIdx.x == 0) s_h = bw_h;
   } else if (n == 1) {
@@ -608,7 +629,7 @@ __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(const float* __res
       const int64_t m = (int64_t)n * (n - 1) / 2;
       // staging: warp w copies the strictly-upper part of rows w, w + 32, ... (lanes along j, 4 loads in
       // flight, no 64-bit index division per element, which dominated the old element-indexed loop)
-      {
+      if (gsums == nullptr) {
         const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31, nw = blockDim.x >> 5;
         for (int i = wid; i < n; i += nw) {
           const float* drow = D + (int64_t)i * n;
@@ -662,7 +683,7 @@ __global__ void kernel_rows_kernel(const float* __restrict__ D, int n, int row0,
   if (i < nl) kernel_row(D, n, row0, i, h_in[t], K, srow, threadIdx.x & 31);
 }
 void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c_ln, float bw_h, float* h, float* K,
-                      float* srow, int tensors, cudaStream_t s) {
+                      float* srow, int tensors, cudaStream_t s, const float* gsums) {
   const int64_t m = (int64_t)n * (n - 1) / 2;
   const int use_tri = rule != PUSH_BW_FIXED && n > 1 && m <= kTriKeys;
   static bool attr = false;
@@ -673,8 +694,9 @@ void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c
   // K rows in the same CTA for small n_local * n, else spread over the SMs by a second launch (C4: 256
   // rows x 256 exp on one SM were a third of the kernel)
   const int split = (int64_t)nl * n >= 16384;
-  bandwidth_kernel_impl<<<tensors, 1024, use_tri ? (size_t)m * 4 : 0, s>>>(D, n, row0, nl, rule, c_ln, bw_h, h, K, srow,
-                                                                    use_tri, split ? 0 : 1);
+  bandwidth_kernel_impl<<<tensors, 1024, use_tri ? (size_t)m * 4 : 0, s>>>(const_cast<float*>(D), n, row0, nl, rule, c_ln, bw_h, h, K, srow,
+                                                                    use_tri, split ? 0 : 1, gsums,
+                                                                    gsums ? gram_np(n) : 0);
   if (split) kernel_rows_kernel<<<dim3((nl + 7) / 8, tensors), 256, 0, s>>>(D, n, row0, nl, h, K, srow);
 }
 

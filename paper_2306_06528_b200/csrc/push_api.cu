@@ -824,7 +824,7 @@ static push_status ds_phase2(push_ctx* c, cudaStream_t s) {
     });
     if (st != PUSH_OK) return st;
   }
-  st = run_k(c, PC_DIST, P.gram ? 2 : 1, 4.0 * P.n * P.n * (double)P.dist.splits, 0, s, [&] {
+  st = run_k(c, PC_DIST, P.gram ? (kern::gram_d_in_bandwidth(P.n) ? 1 : 2) : 1, 4.0 * P.n * P.n * (double)P.dist.splits, 0, s, [&] {
     if (P.gram)
       kern::gram_dist(c->dpart, P.n, P.dist.splits, c->slots, c->gsum, c->D, s);
     else
@@ -833,7 +833,8 @@ static push_status ds_phase2(push_ctx* c, cudaStream_t s) {
   });
   if (st != PUSH_OK) return st;
   st = run_k(c, PC_BANDWIDTH, (int64_t)P.n * P.n >= 16384 ? 2 : 1, 4.0 * P.n * P.n, 0, s, [&] {
-    kern::bandwidth_kernel(c->D, P.n, 0, P.n, c->cfg.bw_rule, c->c_ln, c->cfg.bw_h, c->h, c->K, c->srow, 1, s);
+    kern::bandwidth_kernel(c->D, P.n, 0, P.n, c->cfg.bw_rule, c->c_ln, c->cfg.bw_h, c->h, c->K, c->srow, 1, s,
+                           P.gram && kern::gram_d_in_bandwidth(P.n) ? c->gsum : nullptr);
     return PUSH_OK;
   });
   if (st != PUSH_OK || wo == 0) return st;
@@ -915,7 +916,7 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   const float* th = c->theta[c->cur];
   const double nd4 = 4.0 * P.n * (double)P.d;
   if (P.gram) {
-    st = run_k(c, PC_DIST, 3, nd4, 2.0 * P.n * (double)P.n * P.ld, s, [&]() -> push_status {
+    st = run_k(c, PC_DIST, kern::gram_d_in_bandwidth(P.n) ? 2 : 3, nd4, 2.0 * P.n * (double)P.n * P.ld, s, [&]() -> push_status {
       push_status g = kern::gram_partial(th, P.ld, P.n, P.dist.splits, c->dranges, c->dpart, s);
       if (g != PUSH_OK) return g;
       kern::gram_dist(c->dpart, P.n, P.dist.splits, c->slots, c->gsum, c->D, s);
@@ -931,7 +932,7 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   if (st != PUSH_OK) return st;
   st = run_k(c, PC_BANDWIDTH, (int64_t)P.nl * P.n >= 16384 ? 2 : 1, 4.0 * P.tensors * P.n * P.n, 0, s, [&] {
     kern::bandwidth_kernel(c->D, P.n, c->row0, P.nl, c->cfg.bw_rule, c->c_ln, c->cfg.bw_h, c->h, c->K, c->srow,
-                           P.tensors, s);
+                           P.tensors, s, P.gram && kern::gram_d_in_bandwidth(P.n) ? c->gsum : nullptr);
     return PUSH_OK;
   });
   if (st != PUSH_OK) return st;
