@@ -44,8 +44,9 @@ namespace kern {
 
 namespace {
 constexpr int kGBK = 32;              // fp32 of K per k-block (one 128-B SWIZZLE_128B row per particle)
-constexpr int kGGroups = 2;           // transform groups (4 warps each) taking alternate raw stages
-constexpr int kGXf0 = 2, kGEpi0 = kGXf0 + 4 * kGGroups;
+constexpr int kGGroups = 2;           // transform super-groups taking alternate raw stages
+constexpr int kGSub = 1;              // 4-warp groups per super-group, splitting a stage's k-blocks
+constexpr int kGXf0 = 2, kGEpi0 = kGXf0 + 4 * kGGroups * kGSub;
 constexpr int kGThreads = 32 * (kGEpi0 + 8);  // + 8 epilogue warps
 constexpr int kGSmemMax = 227 * 1024;
 
@@ -101,10 +102,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 128);
+      ptx::mbar_init(&empty[s], 128 * kGSub);
     }
     for (int e = 0; e < C::NE; ++e) {
-      ptx::mbar_init(&ready[e], 128);
+      ptx::mbar_init(&ready[e], 128 * kGSub);
       ptx::mbar_init(&freed[e], 1);
     }
     for (int b = 0; b < C::NACC; ++b) {
@@ -164,21 +165,28 @@ __global__ void __launch_bounds__(kGThreads, 1)
       }
     }
   } else if (warp < kGEpi0) {
-    // ---------------- transform group g: raw stages g, g + 2, ...  Thread: TMEM lane 32q + lane = Hi or Lo
-    // of i-block row lane_row(q, lane); the Hi thread also writes the row's Hi into the B tile.  Rows of the
-    // tile outside the i-block (n > 64) are converted 16-B unit by unit.
-    const int g = (warp - kGXf0) >> 2, q = warp & 3, t = threadIdx.x - 32 * (kGXf0 + 4 * g);
+    // ---------------- transform super-group sg: raw stages sg, sg + 2, ...; its group hb takes the stage's
+    // k-blocks hb, hb + kGSub, ...  Thread: TMEM lane 32q + lane = Hi or Lo of i-block row lane_row(q, lane);
+    // the Hi thread also writes the row's Hi into the B tile.  Rows of the tile outside the i-block (n > 64)
+    // are converted 16-B unit by unit.
+    const int gg = (warp - kGXf0) >> 2, sg = gg / kGSub, hb = gg % kGSub, q = warp & 3;
+    const int t = threadIdx.x - 32 * (kGXf0 + 4 * gg);
     const int arow = ib * 64 + lane_row(q, lane);
     const bool want_lo = lane & 1;
     const bool in_tile = arow < NP;
     const bool live = arow < n;
-    for (int i = g; i < nst; i += kGGroups) {
+    for (int i = sg; i < nst; i += kGGroups) {
       const int s = i % C::STAGES;
       const int e = i % C::NE;
       const uint32_t rs = ptx::smem_u32(raw + s * C::RAW);
       ptx::mbar_wait(&full[s], (i / C::STAGES) & 1);
+      if (hb >= C::KPS) {  // no k-block of this stage for this group
+        ptx::mbar_arrive(&empty[s]);
+        ptx::mbar_arrive(&ready[e]);
+        continue;
+      }
 #pragma unroll 1
-      for (int j = 0; j < C::KPS; ++j) {
+      for (int j = hb; j < C::KPS; j += kGSub) {
         const uint32_t bt = ptx::smem_u32(btile + (e * C::KPS + j) * C::TILE);
         uint32_t a[32];
 #pragma unroll
@@ -196,7 +204,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
             }
           }
         }
-        if (j == 0) ptx::mbar_wait(&freed[e], ((i / C::NE) & 1) ^ 1);  // entry e (A slots, B tiles) is free
+        if (j == hb) ptx::mbar_wait(&freed[e], ((i / C::NE) & 1) ^ 1);  // entry e (A slots, B tiles) is free
         if constexpr (C::OUTER > 0) {
 #pragma unroll 4
           for (int m = 0; m < C::OUTER; ++m) {
@@ -211,7 +219,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
             ptx::sts_f4(bt + r * 128 + ((cc ^ (r & 7)) << 4), o);
           }
         }
-        if (j == C::KPS - 1) ptx::mbar_arrive(&empty[s]);  // every read of the raw stage is done above
+        if (j + kGSub >= C::KPS) ptx::mbar_arrive(&empty[s]);  // this group's reads of the raw stage are done
         ptx::tc_fence_after();
         ptx::tmem_st_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + C::ASLOT0 + (e * C::KPS + j) * 32, a);
         if (!want_lo && in_tile) {
