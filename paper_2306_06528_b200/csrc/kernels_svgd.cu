@@ -602,20 +602,32 @@ __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(float* D, int n, i
   __shared__ float s_h;
   const int64_t N = (int64_t)n * n;
   if (gsums != nullptr) {
-    // Gram form (one tensor): D from the summed Gram blocks, written to D (K rows and push_gather read it)
-    // and, when the keys are staged, straight into skeys (strictly-upper row-major, as the staging below)
+    // Gram form (one tensor): D from the summed Gram blocks (gram_d_value's arithmetic, the diagonal G_jj
+    // evaluated once into shared memory), written to D (K rows and push_gather read it) and, when the keys
+    // are staged, straight into skeys (strictly-upper row-major, as the staging below): warp per row i,
+    // lanes along j (the X / Y row loads coalesced)
     float* Dw = D;
-    for (int64_t e = threadIdx.x; e < N; e += blockDim.x) {
-      const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
-      if (j < i) continue;
-      if (j == i) {
-        Dw[e] = 0.f;
-        continue;
+    __shared__ float gdiag[kGramDInBandwidth];
+    const int64_t np = gnp, yo = 64 * (int64_t)gnp;
+    auto xrow = [&](int a) { return ((int64_t)(a >> 6) * 128 + (a & 63)) * np; };
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const float y = __ldcg(gsums + xrow(t) + yo + t);
+      gdiag[t] = (__ldcg(gsums + xrow(t) + t) + y) + y;
+      Dw[(int64_t)t * n + t] = 0.f;
+    }
+    __syncthreads();
+    const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int i = wid; i < n; i += nw) {
+      const int64_t xi = xrow(i);
+      const float gii = gdiag[i];
+      float* krow = skeys + (int64_t)i * n - (int64_t)i * (i + 1) / 2 - (i + 1);  // krow[j] for j > i
+      for (int j = i + 1 + ln; j < n; j += 32) {
+        const float gij = (__ldcg(gsums + xi + j) + __ldcg(gsums + xi + yo + j)) + __ldcg(gsums + xrow(j) + yo + i);
+        const float d = fmaxf(fmaf(-2.0f, gij, gii + gdiag[j]), 0.f);
+        Dw[(int64_t)i * n + j] = d;
+        Dw[(int64_t)j * n + i] = d;
+        if (use_tri) krow[j] = d;
       }
-      const float d = gram_d_value(gsums, gnp, i, j);
-      Dw[e] = d;
-      Dw[(int64_t)j * n + i] = d;
-      if (use_tri) skeys[(int64_t)i * n - (int64_t)i * (i + 1) / 2 + (j - i - 1)] = d;
     }
     __syncthreads();  // D (global) and the keys are visible to the whole CTA
   }
