@@ -58,6 +58,10 @@ constexpr int kDistPad = 4;  // row stride CW+4 floats: 16-B aligned rows, 2-way
 // staged sub-chunk width per tile shape: small tiles stream wider sub-chunks (fewer syncs per byte)
 template <int T>
 struct DistCW { static constexpr int v = T == 8 ? 256 : (T == 16 ? 128 : 64); };
+// staging buffers (cp.async ring depth): 4 for the small tiles, whose per-CTA bytes in flight otherwise
+// bound the stream (C2: 2 buffers of 8 KB -> 0.9 TB/s), 2 for the 32/64-row tiles
+template <int T>
+struct DistBufs { static constexpr int v = T <= 16 ? 4 : 2; };
 
 DistPlan dist_plan(int n, int tensors, const int64_t* toff, const int64_t* tsize, int64_t total) {
   DistPlan pl;
@@ -97,9 +101,9 @@ template <int T, int RT>
 __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restrict__ theta, int64_t ld, int n,
                                                            int ntile, const int64_t* __restrict__ ranges,
                                                            float* __restrict__ part) {
-  constexpr int CW = DistCW<T>::v;
+  constexpr int CW = DistCW<T>::v, NBUF = DistBufs<T>::v;
   constexpr int TP = T / RT, PT = TP * TP, G = 256 / PT, RS = CW + kDistPad;
-  extern __shared__ __align__(16) float dsm[];  // [2 bufs][2 tiles][T][RS], then G*PT*RT*RT reduction
+  extern __shared__ __align__(16) float dsm[];  // [NBUF bufs][2 tiles][T][RS], then G*PT*RT*RT reduction
   int q = blockIdx.x, bi = 0;  // decode upper-triangular tile pair (bi <= bj)
   while (q >= ntile - bi) { q -= ntile - bi; ++bi; }
   const int bj = bi + q;
@@ -113,7 +117,7 @@ __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restri
   const int nsub = (int)((c_end - c_al + CW - 1) / CW);
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));
   auto stage = [&](int sub) {
-    const int buf = sub & 1;
+    const int buf = sub % NBUF;
     const int64_t c0 = c_al + (int64_t)sub * CW;
     const int ntiles_ld = diag ? 1 : 2;
     for (int idx = tid; idx < ntiles_ld * T * (CW / 4); idx += 256) {
@@ -143,14 +147,17 @@ __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restri
   for (int r = 0; r < RT; ++r)
 #pragma unroll
     for (int c = 0; c < RT; ++c) acc[r][c] = 0.f;
-  stage(0);
-  cp_async_commit();
-  for (int sub = 0; sub < nsub; ++sub) {
-    if (sub + 1 < nsub) stage(sub + 1);
+#pragma unroll
+  for (int q = 0; q < NBUF - 1; ++q) {
+    if (q < nsub) stage(q);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  for (int sub = 0; sub < nsub; ++sub) {
+    if (sub + NBUF - 1 < nsub) stage(sub + NBUF - 1);
+    cp_async_commit();
+    cp_async_wait<NBUF - 1>();
     __syncthreads();
-    const float* si = dsm + (size_t)((sub & 1) * 2) * T * RS;
+    const float* si = dsm + (size_t)((sub % NBUF) * 2) * T * RS;
     const float* sj = diag ? si : si + T * RS;
 #pragma unroll 4
     for (int k = g; k < CW; k += G) {
@@ -170,7 +177,7 @@ __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restri
     __syncthreads();
   }
   if constexpr (G > 1) {  // combine the column groups in ascending g
-    float* red = dsm + 4 * T * RS;
+    float* red = dsm + 2 * NBUF * T * RS;
 #pragma unroll
     for (int r = 0; r < RT; ++r)
 #pragma unroll
@@ -291,7 +298,8 @@ template <int T, int RT>
 static void dist_launch(const float* theta, int64_t ld, int n, const DistPlan& pl, const int64_t* ranges, float* part,
                         cudaStream_t s) {
   constexpr int TP = T / RT, PT = TP * TP, G = 256 / PT;
-  const size_t smem = sizeof(float) * (4 * T * (DistCW<T>::v + kDistPad) + (G > 1 ? G * PT * RT * RT : 0));
+  const size_t smem =
+      sizeof(float) * (2 * DistBufs<T>::v * T * (DistCW<T>::v + kDistPad) + (G > 1 ? G * PT * RT * RT : 0));
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(dist_partial_kernel<T, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -320,13 +328,17 @@ void dist_partial(const float* theta, int64_t ld, int n, const DistPlan& pl, con
   else dist_launch<64, 4>(theta, ld, n, pl, ranges, part, s);
 }
 
-// A CTA per 32 consecutive D entries of one tensor: lane = entry (coalesced partial rows), warp w
-// sums the tensor's splits s = s0 + w, s0 + w + 8, ... ascending (8 loads in flight per lane), then the
-// 8 warp sums are added in ascending w.  The order depends only on the split table (n and the tensor
-// ranges), never on the sharding; the rank-block slot of split s is its owner's (NEXT-4).
-__global__ void __launch_bounds__(256) dist_reduce_kernel(const float* __restrict__ part, int n, int tensors,
-                                                          const TSplit ts, const RankSlots rs, float* __restrict__ D) {
-  __shared__ float red[8][33];
+// A CTA per 32 consecutive D entries of one tensor: lane = entry (coalesced partial rows), warp w of
+// kRedWarps sums the tensor's splits s = s0 + w, s0 + w + kRedWarps, ... ascending (8 loads in flight per
+// lane), then the warp sums are added in ascending w.  The order depends only on the split table (n and
+// the tensor ranges), never on the sharding; the rank-block slot of split s is its owner's (NEXT-4).
+// 32 warps: C2's 296 splits x 256 entries are 8 CTAs, so the per-warp chain of dependent L2 rounds is
+// the kernel's time (8 warps: 9.5 us).
+constexpr int kRedWarps = 32;
+__global__ void __launch_bounds__(32 * kRedWarps) dist_reduce_kernel(const float* __restrict__ part, int n, int tensors,
+                                                                     const TSplit ts, const RankSlots rs,
+                                                                     float* __restrict__ D) {
+  __shared__ float red[kRedWarps][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nn = (int64_t)n * n;
   const int64_t groups = (nn + 31) / 32;
@@ -338,11 +350,11 @@ __global__ void __launch_bounds__(256) dist_reduce_kernel(const float* __restric
   if (ok && i != j) {
     const int s0 = ts.s[tt], s1 = ts.s[tt + 1];
     int q = 0;  // owner rank of split s (monotone in s)
-    for (int sb = s0 + warp; sb < s1; sb += 64) {
+    for (int sb = s0 + warp; sb < s1; sb += 8 * kRedWarps) {
       float t[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const int s = sb + 8 * k;
+        const int s = sb + kRedWarps * k;
         if (s < s1) {
           while (q + 1 < rs.P && s >= rs.s0[q + 1]) ++q;
           t[k] = __ldg(part + (int64_t)(q * rs.smax + s - rs.s0[q]) * nn + e);
@@ -352,7 +364,7 @@ __global__ void __launch_bounds__(256) dist_reduce_kernel(const float* __restric
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (sb + 8 * k < s1) v += t[k];
+        if (sb + kRedWarps * k < s1) v += t[k];
     }
   }
   red[warp][lane] = v;
@@ -360,13 +372,13 @@ __global__ void __launch_bounds__(256) dist_reduce_kernel(const float* __restric
   if (warp == 0 && ok) {
     float r = red[0][lane];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) r += red[w][lane];
+    for (int w = 1; w < kRedWarps; ++w) r += red[w][lane];
     D[(int64_t)tt * nn + e] = (i == j) ? 0.f : r;  // diagonal is exactly +0
   }
 }
 void dist_reduce(const float* part, int n, const DistPlan& pl, const RankSlots& rs, float* D, cudaStream_t s) {
   const int64_t groups = ((int64_t)n * n + 31) / 32;
-  dist_reduce_kernel<<<(unsigned)(groups * pl.tensors), 256, 0, s>>>(part, n, pl.tensors, pl.tsplit, rs, D);
+  dist_reduce_kernel<<<(unsigned)(groups * pl.tensors), 32 * kRedWarps, 0, s>>>(part, n, pl.tensors, pl.tsplit, rs, D);
 }
 
 // ---------------------------------------------------------------- a8 + a9
