@@ -8,7 +8,7 @@
 // update is theta'_i[c] = sum_q L[i][q] B[q][c] with the folded coefficient matrix
 //   L[i][j_G]     = (eps/n) K_ij
 //   L[i][j_Theta] = -(eps/n) r K_ij + [j = own_row + i] (1 + (eps/n) r (s_i - K_ii))
-// (update_lhs_split_kernel; R29).  The contraction runs TRANSPOSED so that the streamed operand is
+// (update_lhs_split_kernel; R28).  The contraction runs TRANSPOSED so that the streamed operand is
 // the MMA's A (from TMEM) and the small L stays resident in shared memory:
 //   D[c][i] (TMEM lane c of a 128-column tile, column i) = sum_q B[q][c] L[i][q]   (M = 128, N = NPAD)
 // 3xTF32 (both operands split hi + lo, lo*lo dropped), K = 2n <= 128: one TMEM accumulation chunk.  The
@@ -244,7 +244,7 @@ push_status update_tc_launch(const float* b, int n, int64_t w, int rows, const f
   return PUSH_OK;
 }
 
-// L split (R29): rows i < npad (zero past nl) of the folded coefficient matrix over the B rows q
+// L split (R28): rows i < npad (zero past nl) of the folded coefficient matrix over the B rows q
 // ([G; Theta] when g_first, else [Theta; G]), as tf32 hi / lo at `pitch`:
 //   G row j:      (eps/n) K_ij
 //   Theta row j:  -(eps/n) r K_ij, plus 1 + (eps/n) r (s_i - K_ii) on the own particle j = own_row + i
