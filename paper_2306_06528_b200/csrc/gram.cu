@@ -18,14 +18,15 @@
 // One CTA streams one column split of Theta (the split plan's ranges, fixed by (n, ld) only, so the
 // partials are the same whichever rank computes them: P-invariance, NEXT-4) for one i-block:
 //   warp 0 lane 0   TMA producer: raw stages of RC columns x NP rows, unswizzled, at a padded row pitch of
-//                   RC + 4 floats (the box over-reads 4 columns): 512-B row requests keep the ring at the HBM
+//                   RC + 8 floats (the box over-reads 8 columns): 512-B row requests keep the ring at the HBM
 //                   rate (scripts/micro/tma_stream.cu: 32-column SWIZZLE_128B boxes cap at ~0.5-0.66 of the
-//                   copy rate, 128 + 4-column boxes reach 0.95), and the 16-B row skew makes the transform's
-//                   row-wise reads conflict-free
+//                   copy rate, 128 + 4-column boxes reach 0.95), and the 32-B row skew makes the transform's
+//                   row-wise 8-B reads (8 rows x 32 B per instruction) conflict-free
 //   warp 1 lane 0   MMA issuer (tcgen05.mma kind::tf32, A from TMEM, B from smem); warp 1 owns TMEM
-//   warps 2-9       two transform groups taking alternate raw stages: per k-block (32 columns) centre,
-//                   split, A rows -> a TMEM slot (tcgen05.st), Hi rows -> a SWIZZLE_128B K-major B tile; the
-//                   raw stage is released as soon as it has been read, the slot / tile by the MMA commit
+//   warps 2-9       two transform groups taking alternate raw stages: per k-block (32 columns) centre and
+//                   split each element once (tcgen05.st.16x256b puts its Hi and Lo in two TMEM lanes), Hi
+//                   rows -> a SWIZZLE_128B K-major B tile; the raw stage is released as soon as it has been
+//                   read, the slot / tile by the MMA commit
 //   warps 10-17     epilogue: TMEM partial added into fp32 registers every 128 of K (the tensor-core
 //                   accumulator truncates each add), then the split's [X; Y] block stored to `part`
 // The reduction over splits and the distance formula run in gram_dist (fixed ascending order).
@@ -54,7 +55,7 @@ template <int NP>
 struct GCfg {
   static constexpr int RC = NP <= 64 ? 128 : (NP == 128 ? 64 : 32);  // raw columns per stage
   static constexpr int KPS = RC / kGBK;                        // k-blocks per raw stage
-  static constexpr int PITCH = (RC + 4) * 4;                   // raw row pitch (bytes): 16-B skew per row
+  static constexpr int PITCH = (RC + 8) * 4;                   // raw row pitch (bytes): 32-B skew per row
   static constexpr int RAW = NP * PITCH;                       // one raw stage
   static constexpr int TILE = NP * kGBK * 4;                   // one B tile (k-block): NP rows x 128 B
   static constexpr int NACC = NP <= 128 ? 2 : 1;               // TMEM accumulators of NP columns
@@ -71,10 +72,11 @@ struct GCfg {
   static_assert(CW % 16 == 0 && STAGES >= 2 && NE >= 2 && SMEM <= kGSmemMax, "cfg");
 };
 
-// TMEM lane L of the A operand / accumulator <-> i-block row and part: lane quarter q holds rows
-// 16q .. 16q + 15, lane 2r' the Hi (X) and lane 2r' + 1 the Lo (Y) of row 16q + r'.  Hi and Lo of a row
-// sit in the SAME warp (adjacent lanes read the same raw row: a broadcast).
-__device__ __forceinline__ int lane_row(int q, int lane) { return 16 * q + (lane >> 1); }
+// TMEM lane 32q + l of the A operand / accumulator <-> i-block row and part: lane quarter q holds rows
+// 16q .. 16q + 15 in two 16-lane blocks (l >> 4); in block hh, lanes 0-7 are the Hi (X) and lanes 8-15 the
+// Lo (Y) of rows 16q + 8hh + 0..7 — the tcgen05.st.16x256b layout, where one thread writes both.
+__device__ __forceinline__ int lane_row(int q, int lane) { return 16 * q + 8 * (lane >> 4) + (lane & 7); }
+__device__ __forceinline__ int lane_part(int lane) { return (lane >> 3) & 1; }
 
 template <int NP>
 __global__ void __launch_bounds__(kGThreads, 1)
@@ -166,15 +168,22 @@ __global__ void __launch_bounds__(kGThreads, 1)
     }
   } else if (warp < kGEpi0) {
     // ---------------- transform super-group sg: raw stages sg, sg + 2, ...; its group hb takes the stage's
-    // k-blocks hb, hb + kGSub, ...  Thread: TMEM lane 32q + lane = Hi or Lo of i-block row lane_row(q, lane);
-    // the Hi thread also writes the row's Hi into the B tile.  Rows of the tile outside the i-block (n > 64)
-    // are converted 16-B unit by unit.
+    // k-blocks hb, hb + kGSub, ...  Each element is converted ONCE: with tcgen05.st.16x256b, thread
+    // (t0 = lane & 3, t1 = lane >> 2) writes columns 2 t0, 2 t0 + 1 (+ 8 per repetition) of TMEM lanes t1 (Hi)
+    // and t1 + 8 (Lo) of a 16-lane block, so one thread holds both parts of its row (lane_part below); the
+    // thread also writes the row's Hi into the B tile.  Rows of the tile outside the i-block (n > 64) are
+    // converted 16-B unit by unit.
     const int gg = (warp - kGXf0) >> 2, sg = gg / kGSub, hb = gg % kGSub, q = warp & 3;
     const int t = threadIdx.x - 32 * (kGXf0 + 4 * gg);
-    const int arow = ib * 64 + lane_row(q, lane);
-    const bool want_lo = lane & 1;
-    const bool in_tile = arow < NP;
-    const bool live = arow < n;
+    const int t0 = lane & 3, t1 = lane >> 2;
+    int arow[2];
+    bool live[2], in_tile[2];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {  // 16-lane block hh of the quarter: rows 16q + 8hh + t1
+      arow[hh] = ib * 64 + 16 * q + 8 * hh + t1;
+      live[hh] = arow[hh] < n;
+      in_tile[hh] = arow[hh] < NP;
+    }
     for (int i = sg; i < nst; i += kGGroups) {
       const int s = i % C::STAGES;
       const int e = i % C::NE;
@@ -188,20 +197,26 @@ __global__ void __launch_bounds__(kGThreads, 1)
 #pragma unroll 1
       for (int j = hb; j < C::KPS; j += kGSub) {
         const uint32_t bt = ptx::smem_u32(btile + (e * C::KPS + j) * C::TILE);
-        uint32_t a[32];
+        // a[hh][4r + {0,1}] = Hi of columns 8r + 2t0 + {0,1}, a[hh][4r + {2,3}] = Lo of the same columns
+        uint32_t a[2][16];
+        float2 cv[4];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) a[u] = 0u;
-        if (live) {
+        for (int r = 0; r < 4; ++r) cv[r] = ptx::lds_f2(rs + (j * 32 + 8 * r + 2 * t0) * 4);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const float4 cv = ptx::lds_f4(rs + j * 128 + (u << 4));
-            const float4 v = ptx::lds_f4(rs + arow * C::PITCH + j * 128 + (u << 4));
-            const float xv[4] = {v.x - cv.x, v.y - cv.y, v.z - cv.z, v.w - cv.w};
+        for (int hh = 0; hh < 2; ++hh) {
 #pragma unroll
-            for (int ee = 0; ee < 4; ++ee) {
-              const float h = ptx::tf32_rna_fast(xv[ee]);
-              a[4 * u + ee] = __float_as_uint(want_lo ? xv[ee] - h : h);
+          for (int r = 0; r < 4; ++r) {
+            float2 v = make_float2(0.f, 0.f), c = make_float2(0.f, 0.f);
+            if (live[hh]) {
+              v = ptx::lds_f2(rs + arow[hh] * C::PITCH + (j * 32 + 8 * r + 2 * t0) * 4);
+              c = cv[r];
             }
+            const float x0 = v.x - c.x, x1 = v.y - c.y;
+            const float h0 = ptx::tf32_rna_fast(x0), h1 = ptx::tf32_rna_fast(x1);
+            a[hh][4 * r] = __float_as_uint(h0);
+            a[hh][4 * r + 1] = __float_as_uint(h1);
+            a[hh][4 * r + 2] = __float_as_uint(x0 - h0);
+            a[hh][4 * r + 3] = __float_as_uint(x1 - h1);
           }
         }
         if (j == hb) ptx::mbar_wait(&freed[e], ((i / C::NE) & 1) ^ 1);  // entry e (A slots, B tiles) is free
@@ -221,13 +236,19 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
         if (j + kGSub >= C::KPS) ptx::mbar_arrive(&empty[s]);  // this group's reads of the raw stage are done
         ptx::tc_fence_after();
-        ptx::tmem_st_32x32b_x32(tmem_base + ((uint32_t)(32 * q) << 16) + C::ASLOT0 + (e * C::KPS + j) * 32, a);
-        if (!want_lo && in_tile) {
+        const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + C::ASLOT0 + (e * C::KPS + j) * 32;
+        ptx::tmem_st_16x256b_x4(ta, a[0]);
+        ptx::tmem_st_16x256b_x4(ta + (16u << 16), a[1]);
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            ptx::sts_f4(bt + arow * 128 + ((u ^ (arow & 7)) << 4),
-                        make_float4(__uint_as_float(a[4 * u]), __uint_as_float(a[4 * u + 1]),
-                                    __uint_as_float(a[4 * u + 2]), __uint_as_float(a[4 * u + 3])));
+        for (int hh = 0; hh < 2; ++hh) {
+          if (!in_tile[hh]) continue;
+          const int ar = arow[hh];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {  // columns 8r + 2t0 + {0,1}: 16-B chunk 2r + t0/2, 8 (t0 & 1) bytes in
+            const int chunk = 2 * r + (t0 >> 1);
+            ptx::sts_f2(bt + ar * 128 + ((chunk ^ (ar & 7)) << 4) + 8 * (t0 & 1),
+                        make_float2(__uint_as_float(a[hh][4 * r]), __uint_as_float(a[hh][4 * r + 1])));
+          }
         }
       }
       ptx::tmem_st_wait();
@@ -260,7 +281,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         ptx::mbar_arrive(&tempty[b]);
       }
       // [X; Y] block of (split, i-block): X row r at r, Y row r at 64 + r; NP columns
-      const int prow = (lane & 1) * 64 + lane_row(q, lane);
+      const int prow = lane_part(lane) * 64 + lane_row(q, lane);
       float* dst = part + (((int64_t)split * n_ib + ib) * 128 + prow) * NP + h * C::CW;
 #pragma unroll
       for (int j = 0; j < C::CW; j += 4)
@@ -278,7 +299,7 @@ push_status gram_launch(const float* theta, int64_t ld, int n, int splits, const
   using C = GCfg<NP>;
   CUtensorMap map;
   push_status st = gemm::make_map(&map, theta, (uint64_t)ld, (uint64_t)n, 1, (uint64_t)ld, 0, NP,
-                                  CU_TENSOR_MAP_SWIZZLE_NONE, C::RC + 4);
+                                  CU_TENSOR_MAP_SWIZZLE_NONE, C::RC + 8);
   if (st != PUSH_OK) return st;
   static bool attr = false;
   if (!attr) {
