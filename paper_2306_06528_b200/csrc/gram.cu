@@ -360,21 +360,24 @@ push_status gram_partial(const float* theta, int64_t ld, int n, int splits, cons
 }
 
 // Sum of the split partials: sums[e] = sum_s part[slot(s)][e] over one partial block (e < pb).  A CTA
-// covers 32 consecutive elements (lane = element, coalesced), warp w sums s = w, w + 8, ... ascending with
-// 8 loads in flight, then the 8 warp sums are added in ascending w: the order depends only on S.
-__global__ void __launch_bounds__(256) gram_reduce_kernel(const float* __restrict__ part, int64_t pb, int S,
-                                                          const RankSlots rs, float* __restrict__ sums) {
-  __shared__ float red[8][33];
+// covers 32 consecutive elements (lane = element, coalesced), warp w of kGRedWarps sums s = w, w + kGRedWarps,
+// ... ascending with 8 loads in flight, then the warp sums are added in ascending w: the order depends only
+// on S.  32 warps: with ~147 splits every warp issues its loads in one round (8 warps: three dependent rounds).
+constexpr int kGRedWarps = 32;
+__global__ void __launch_bounds__(32 * kGRedWarps) gram_reduce_kernel(const float* __restrict__ part, int64_t pb,
+                                                                      int S, const RankSlots rs,
+                                                                      float* __restrict__ sums) {
+  __shared__ float red[kGRedWarps][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t e = (int64_t)blockIdx.x * 32 + lane;
   float v = 0.f;
   if (e < pb) {
     int q = 0;
-    for (int sb = warp; sb < S; sb += 64) {
+    for (int sb = warp; sb < S; sb += 8 * kGRedWarps) {
       float t[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const int s = sb + 8 * k;
+        const int s = sb + kGRedWarps * k;
         t[k] = 0.f;
         if (s < S) {
           while (q + 1 < rs.P && s >= rs.s0[q + 1]) ++q;
@@ -383,7 +386,7 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const float* __restric
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (sb + 8 * k < S) v += t[k];
+        if (sb + kGRedWarps * k < S) v += t[k];
     }
   }
   red[warp][lane] = v;
@@ -391,7 +394,7 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const float* __restric
   if (warp == 0 && e < pb) {
     float r = red[0][lane];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) r += red[w][lane];
+    for (int w = 1; w < kGRedWarps; ++w) r += red[w][lane];
     sums[e] = r;
   }
 }
@@ -415,7 +418,7 @@ bool gram_d_in_bandwidth(int n) { return n <= kGramDInBandwidth; }
 
 void gram_dist(const float* part, int n, int S, const RankSlots& rs, float* sums, float* D, cudaStream_t s) {
   const int64_t pb = gram_part_floats(n);
-  gram_reduce_kernel<<<(unsigned)((pb + 31) / 32), 256, 0, s>>>(part, pb, S, rs, sums);
+  gram_reduce_kernel<<<(unsigned)((pb + 31) / 32), 32 * kGRedWarps, 0, s>>>(part, pb, S, rs, sums);
   if (gram_d_in_bandwidth(n)) return;  // the bandwidth kernel evaluates D while staging its keys
   const int64_t nn = (int64_t)n * n;
   gram_d_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(sums, n, gram_np(n), D);

@@ -392,6 +392,11 @@ struct push_ctx {
   // comm stream: the Theta all-gather (a6/C1) runs beside the gradient kernels (P > 1)
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_theta = nullptr, ev_fork2 = nullptr, ev_grad = nullptr;
+  // captured whole steps: a7-a9 (they read Theta only) forked onto k_stream at the start of the gradient
+  // phase and joined before a10 (kphase_ready: D / h / K of the current Theta are in flight there)
+  cudaStream_t k_stream = nullptr;
+  cudaEvent_t ev_kfork = nullptr, ev_kdone = nullptr;
+  bool kphase_ready = false;
   bool theta_pending = false;
   // CUDA-graph replay of a whole step (push_step_graph): one executable per Theta buffer parity
   struct GraphEntry {
@@ -522,7 +527,12 @@ static ActView layer_input(push_ctx* c, int l, const float* x) {
   return ActView{c->act[l - 1], c->P.act_pst[l - 1]};
 }
 
-static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, cudaStream_t s) {
+static push_status run_kphase(push_ctx* c, cudaStream_t s);
+
+// fork_kphase (captured whole steps): a7-a9 start on k_stream as soon as Theta_all is complete, beside the
+// gradient kernels, and do_step joins them before a10
+static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, cudaStream_t s,
+                            bool fork_kphase = false) {
   const Plan& P = c->P;
   const int nl = P.nl, L = P.L, act = c->cfg.activation;
   const int64_t ld = P.ld;
@@ -552,6 +562,14 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
     if ((st = exchange(c, BUF_THETA, c->comm_stream)) != PUSH_OK) return st;
     PUSH_CUDA_TRY(cudaEventRecord(c->ev_theta, c->comm_stream));
     c->theta_pending = true;
+  }
+  if (fork_kphase && !P.ds) {
+    PUSH_CUDA_TRY(cudaEventRecord(c->ev_kfork, s));
+    PUSH_CUDA_TRY(cudaStreamWaitEvent(c->k_stream, c->ev_kfork, 0));
+    if (c->theta_pending) PUSH_CUDA_TRY(cudaStreamWaitEvent(c->k_stream, c->ev_theta, 0));
+    if ((st = run_kphase(c, c->k_stream)) != PUSH_OK) return st;
+    PUSH_CUDA_TRY(cudaEventRecord(c->ev_kdone, c->k_stream));
+    c->kphase_ready = true;
   }
 
   // a0: tf32 hi/lo copies of tensor-core weights that are not 16-B aligned in Theta (the others, and all
@@ -900,19 +918,11 @@ static push_status ds_group_step(const std::vector<push_ctx*>& m, cudaStream_t s
   return PUSH_OK;
 }
 
-static push_status do_step(push_ctx* c, cudaStream_t s) {
+// a7 (distances) + a8/a9 (bandwidth, K, s) of the current Theta on stream s (all-gather mode: Theta_all must
+// be complete on s).  They read Theta only, so a captured whole step runs them beside the gradient phase.
+static push_status run_kphase(push_ctx* c, cudaStream_t s) {
   const Plan& P = c->P;
   push_status st;
-  if (P.ds) return ds_group_step({c}, s);  // NCCL ranks (or one rank): three collective phases
-  if ((st = join_theta(c, s)) != PUSH_OK) return st;  // the Theta all-gather started by the gradient call
-  // C2: g rows of every rank, on the comm stream while a7-a9 (which read Theta only) run; joined before a10
-  const bool xg = c->world > 1 || c->comm;
-  if (xg) {
-    PUSH_CUDA_TRY(cudaEventRecord(c->ev_fork2, s));
-    PUSH_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_fork2, 0));
-    if ((st = exchange(c, BUF_GRAD, c->comm_stream)) != PUSH_OK) return st;
-    PUSH_CUDA_TRY(cudaEventRecord(c->ev_grad, c->comm_stream));
-  }
   const float* th = c->theta[c->cur];
   const double nd4 = 4.0 * P.n * (double)P.d;
   if (P.gram) {
@@ -930,12 +940,34 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
     });
   }
   if (st != PUSH_OK) return st;
-  st = run_k(c, PC_BANDWIDTH, (int64_t)P.nl * P.n >= 16384 ? 2 : 1, 4.0 * P.tensors * P.n * P.n, 0, s, [&] {
+  return run_k(c, PC_BANDWIDTH, (int64_t)P.nl * P.n >= 16384 ? 2 : 1, 4.0 * P.tensors * P.n * P.n, 0, s, [&] {
     kern::bandwidth_kernel(c->D, P.n, c->row0, P.nl, c->cfg.bw_rule, c->c_ln, c->cfg.bw_h, c->h, c->K, c->srow,
                            P.tensors, s, P.gram && kern::gram_d_in_bandwidth(P.n) ? c->gsum : nullptr);
     return PUSH_OK;
   });
-  if (st != PUSH_OK) return st;
+}
+
+static push_status do_step(push_ctx* c, cudaStream_t s) {
+  const Plan& P = c->P;
+  push_status st;
+  if (P.ds) return ds_group_step({c}, s);  // NCCL ranks (or one rank): three collective phases
+  if ((st = join_theta(c, s)) != PUSH_OK) return st;  // the Theta all-gather started by the gradient call
+  // C2: g rows of every rank, on the comm stream while a7-a9 (which read Theta only) run; joined before a10
+  const bool xg = c->world > 1 || c->comm;
+  if (xg) {
+    PUSH_CUDA_TRY(cudaEventRecord(c->ev_fork2, s));
+    PUSH_CUDA_TRY(cudaStreamWaitEvent(c->comm_stream, c->ev_fork2, 0));
+    if ((st = exchange(c, BUF_GRAD, c->comm_stream)) != PUSH_OK) return st;
+    PUSH_CUDA_TRY(cudaEventRecord(c->ev_grad, c->comm_stream));
+  }
+  const float* th = c->theta[c->cur];
+  const double nd4 = 4.0 * P.n * (double)P.d;
+  if (c->kphase_ready) {  // a7-a9 ran on k_stream beside the gradient phase (captured whole step)
+    PUSH_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_kdone, 0));
+    c->kphase_ready = false;
+  } else if ((st = run_kphase(c, s)) != PUSH_OK) {
+    return st;
+  }
   if (xg) PUSH_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_grad, 0));  // G rows of every rank have landed
   const float eps_n = c->cfg.step_size / (float)P.n;
   float* next = c->theta[c->cur ^ 1];
@@ -1154,6 +1186,9 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_theta, cudaEventDisableTiming));
   PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming));
   PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_grad, cudaEventDisableTiming));
+  PUSH_CUDA_TRY(cudaStreamCreateWithFlags(&c->k_stream, cudaStreamNonBlocking));
+  PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_kfork, cudaEventDisableTiming));
+  PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_kdone, cudaEventDisableTiming));
   cudaStream_t s = nullptr;
   const size_t nld = (size_t)P.n * P.ld;
   PUSH_CUDA_TRY(cudaMemsetAsync(c->theta[0], 0, nld * 4, s));
@@ -1396,7 +1431,7 @@ push_status push_step_graph(push_ctx* c, const float* x_dev, const float* y_dev,
     const int64_t l0 = c->launches;
     cudaGraph_t graph = nullptr;
     PUSH_CUDA_TRY(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
-    st = do_grads(c, c->xbuf, c->ybuf, B, c->cap_stream);
+    st = do_grads(c, c->xbuf, c->ybuf, B, c->cap_stream, /*fork_kphase=*/true);
     if (st == PUSH_OK && loss_dev) {
       cudaError_t e = cudaMemcpyAsync(loss_dev, c->loss, 4 * c->P.nl, cudaMemcpyDeviceToDevice, c->cap_stream);
       if (e != cudaSuccess) st = fail(PUSH_E_CUDA, cudaGetErrorString(e));
@@ -1405,6 +1440,7 @@ push_status push_step_graph(push_ctx* c, const float* x_dev, const float* y_dev,
     cudaError_t e = cudaStreamEndCapture(c->cap_stream, &graph);
     c->cur = cur0;  // capturing executed nothing
     c->theta_pending = false;
+    c->kphase_ready = false;
     if (st != PUSH_OK || e != cudaSuccess) {
       if (graph) cudaGraphDestroy(graph);
       return sticky(c, st != PUSH_OK ? st : fail(PUSH_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e)));
@@ -1634,6 +1670,9 @@ push_status push_destroy(push_ctx* c) {
   if (c->ev_fork2) cudaEventDestroy(c->ev_fork2);
   if (c->ev_grad) cudaEventDestroy(c->ev_grad);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->ev_kfork) cudaEventDestroy(c->ev_kfork);
+  if (c->ev_kdone) cudaEventDestroy(c->ev_kdone);
+  if (c->k_stream) cudaStreamDestroy(c->k_stream);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
   return PUSH_OK;
