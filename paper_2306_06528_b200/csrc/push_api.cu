@@ -394,7 +394,7 @@ struct push_ctx {
   cudaEvent_t ev_fork = nullptr, ev_theta = nullptr, ev_fork2 = nullptr, ev_grad = nullptr;
   // captured whole steps: a7-a9 (they read Theta only) forked onto k_stream at the start of the gradient
   // phase and joined before a10 (kphase_ready: D / h / K of the current Theta are in flight there)
-  cudaStream_t k_stream = nullptr;
+  cudaStream_t k_stream = nullptr, w_stream = nullptr;  // w_stream: side work of the gradient phase
   cudaEvent_t ev_kfork = nullptr, ev_kdone = nullptr;
   bool kphase_ready = false;
   bool theta_pending = false;
@@ -542,6 +542,38 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
   const float lambda = c->cfg.lik_scale;
   const float inv_s2 = c->cfg.prior == PUSH_PRIOR_GAUSSIAN ? 1.0f / (c->cfg.prior_sigma * c->cfg.prior_sigma) : 0.f;
   push_status st;
+  // side stream (captured steps only, fork_kphase): work off the backward critical path — the loss
+  // reduction and each layer's weight gradient — forked from s and joined in order.  side_ev holds the
+  // completion events not yet joined (oldest first); side_join_prev joins all but the newest.
+  cudaStream_t ws = fork_kphase ? c->w_stream : s;
+  std::vector<cudaEvent_t> side_ev;
+  auto side_fork = [&]() -> push_status {
+    if (ws == s) return PUSH_OK;
+    cudaEvent_t e = get_event(c);
+    PUSH_CUDA_TRY(cudaEventRecord(e, s));
+    PUSH_CUDA_TRY(cudaStreamWaitEvent(ws, e, 0));
+    c->ev_pool.push_back(e);
+    return PUSH_OK;
+  };
+  auto side_done = [&]() -> push_status {
+    if (ws == s) return PUSH_OK;
+    cudaEvent_t e = get_event(c);
+    PUSH_CUDA_TRY(cudaEventRecord(e, ws));
+    side_ev.push_back(e);
+    return PUSH_OK;
+  };
+  auto side_join = [&]() -> push_status {
+    if (side_ev.empty()) return PUSH_OK;
+    PUSH_CUDA_TRY(cudaStreamWaitEvent(s, side_ev.front(), 0));
+    c->ev_pool.push_back(side_ev.front());
+    side_ev.erase(side_ev.begin());
+    return PUSH_OK;
+  };
+  auto side_join_prev = [&]() -> push_status {
+    while (side_ev.size() > 1)
+      if (side_join() != PUSH_OK) return PUSH_E_CUDA;
+    return PUSH_OK;
+  };
   // a5 epilogue: every layer's partials are reduced into G by ONE launch after the backward pass
   std::vector<kern::FinalizeJob> jobs;
   // PUSH_VAR_PRIOR_SUM: G keeps the likelihood term only; a10 adds the unweighted prior sum
@@ -634,11 +666,13 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
       return PUSH_OK;
     });
     if (st != PUSH_OK) return st;
-    st = run_k(c, PC_LOSS, 1, 0, 0, s, [&] {
-      kern::loss_reduce(c->err2, P.Bmax, c->loss, B, lp.out, nl, s);
+    if ((st = side_fork()) != PUSH_OK) return st;  // the loss reduction is off the critical path
+    st = run_k(c, PC_LOSS, 1, 0, 0, ws, [&] {
+      kern::loss_reduce(c->err2, P.Bmax, c->loss, B, lp.out, nl, ws);
       return PUSH_OK;
     });
     if (st != PUSH_OK) return st;
+    if ((st = side_done()) != PUSH_OK) return st;
     kern::PartView W{c->opw, RB, oa.wo_sstride, oa.wo_pstride, lp.in};
     kern::PartView Bv{c->opb, RB, oa.bo_sstride, oa.bo_pstride, 1};
     if ((st = finalize(L - 1, W, Bv)) != PUSH_OK) return st;
@@ -667,19 +701,24 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
         pb.out_sstride = (int64_t)nl * lp.out * lp.in;
       }
       const double fl = 2.0 * B * lp.out * (double)lp.in * nl;
-      st = run_k(c, PC_WGRAD_GEMM, 1, 0, fl, s, [&] { return gemm::run(pb, s); });
+      // captured steps: the weight gradient of layer l (reads delta_l and A_{l-1}) beside the backward GEMM
+      // of layer l (reads delta_l too); joined before delta_l's buffer is overwritten (layer l - 1)
+      if ((st = side_join()) != PUSH_OK) return st;
+      if ((st = side_fork()) != PUSH_OK) return st;
+      st = run_k(c, PC_WGRAD_GEMM, 1, 0, fl, ws, [&] { return gemm::run(pb, ws); });
       if (st != PUSH_OK) return st;
       kern::PartView W{c->wpart[l], S, (int64_t)nl * lp.out * lp.in, (int64_t)lp.out * lp.in, lp.in};
       kern::PartView Bv{c->bpart[l], RB, (int64_t)nl * lp.out, lp.out, 1};
       if (!bias_ready[l]) {  // delta_l came from a generic thin backward: column sums here
         int chunks = 0;
-        st = run_k(c, PC_WGRAD_THIN, 1, 4.0 * B * lp.out * nl, 0, s, [&] {
-          chunks = kern::thin_wgrad(dl, P.dlt_pst, nullptr, 0, 0, lp.out, c->tpart[l], B, nl, s);
+        st = run_k(c, PC_WGRAD_THIN, 1, 4.0 * B * lp.out * nl, 0, ws, [&] {
+          chunks = kern::thin_wgrad(dl, P.dlt_pst, nullptr, 0, 0, lp.out, c->tpart[l], B, nl, ws);
           return PUSH_OK;
         });
         if (st != PUSH_OK) return st;
         Bv = kern::PartView{c->tpart[l], chunks, (int64_t)nl * lp.out, lp.out, 1};
       }
+      if ((st = side_done()) != PUSH_OK) return st;
       if ((st = finalize(l, W, Bv, w_in_g)) != PUSH_OK) return st;
     } else if (l == 0 && x0_ready) {
       kern::PartView W{c->xpart, RB, (int64_t)nl * lp.out * lp.in, (int64_t)lp.out * lp.in, lp.in};
@@ -699,7 +738,8 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
       if ((st = finalize(l, W, Bv)) != PUSH_OK) return st;
     }
     if (l == 0) break;
-    // delta_{l-1} = (delta_l W_l) * sigma'(a_{l-1})
+    // delta_{l-1} = (delta_l W_l) * sigma'(a_{l-1}) overwrites delta_{l+1}: the side work reading it is done
+    if ((st = side_join_prev()) != PUSH_OK) return st;
     const ActView aprev = layer_input(c, l, x);  // = A_{l-1}
     float* o = c->dlt[xb ^ 1];
     const double fl = 2.0 * B * lp.out * (double)lp.in * nl;
@@ -732,6 +772,8 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
     if (st != PUSH_OK) return st;
     xb ^= 1;
   }
+  while (!side_ev.empty())
+    if ((st = side_join()) != PUSH_OK) return st;
   return run_k(c, PC_FINALIZE, 1, 0, 0, s, [&] {
     kern::finalize_all(jobs.data(), (int)jobs.size(), th, g, ld, lambda, prior_g, inv_s2, nl, s);
     return PUSH_OK;
@@ -1187,6 +1229,7 @@ static push_status init_one(push_ctx* c, const push_config* cfg, int rank, int w
   PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming));
   PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_grad, cudaEventDisableTiming));
   PUSH_CUDA_TRY(cudaStreamCreateWithFlags(&c->k_stream, cudaStreamNonBlocking));
+  PUSH_CUDA_TRY(cudaStreamCreateWithFlags(&c->w_stream, cudaStreamNonBlocking));
   PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_kfork, cudaEventDisableTiming));
   PUSH_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_kdone, cudaEventDisableTiming));
   cudaStream_t s = nullptr;
@@ -1673,6 +1716,7 @@ push_status push_destroy(push_ctx* c) {
   if (c->ev_kfork) cudaEventDestroy(c->ev_kfork);
   if (c->ev_kdone) cudaEventDestroy(c->ev_kdone);
   if (c->k_stream) cudaStreamDestroy(c->k_stream);
+  if (c->w_stream) cudaStreamDestroy(c->w_stream);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
   return PUSH_OK;
