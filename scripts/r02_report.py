@@ -50,3 +50,20 @@ L += ["", "## Default bench line (S1)", "", "```json", open(f"{out}/bench.json")
       "```json", open(f"{out}/bench_reference.json").read().strip(), "```", "", ncu]
 open("profiles/r02_final.md", "w").write("\n".join(L) + "\n")
 print("\n".join(L[:20]))
+
+# rows for the BASELINE.md results table and DESIGN.md §12 (pasted by hand)
+print("\n-- BASELINE.md rows --")
+for c in order:
+    j = R[c]; r = j["roofline"]; hp = r.get("hbm_passes", {})
+    a7 = hp.get("distances", {}).get("frac", 0); a10 = hp.get("svgd_update", {}).get("frac", 0)
+    tens = r["bound"] == "tensor" and r["frac"] > 0.01
+    print(f"| {c} | 1 | {j['value']:,.0f} | {j['param_updates_per_s']:.1e} | {j['e2e']['value']:,.0f} | "
+          f"{100 * a7:.0f} % / {100 * a10:.0f} % | {str(round(100 * r['frac'])) + ' %' if tens else '—'} | "
+          f"{r.get('all_gemm_tflops', 0):.1f} |")
+print("\n-- DESIGN.md §12 rows --")
+for c in order:
+    j = R[c]; r = j["roofline"]; hp = r.get("hbm_passes", {})
+    a7 = hp.get("distances", {}).get("frac", 0); a10 = hp.get("svgd_update", {}).get("frac", 0)
+    print(f"| {c} | {j['ms_per_step']:.4g} | {j['value']:,.0f} | {j['e2e']['value']:,.0f} | "
+          f"{r['kernel'].split('(')[-1].rstrip(')')} | {r['frac']:.2f} ({r['bound']}) | {r.get('all_gemm_tflops', 0):.1f} | "
+          f"{a7:.2f} / {a10:.2f} |")
