@@ -132,9 +132,7 @@ static push_status validate(const push_config* c, int world) {
 // depends on (B, layer shape, n), never on the sharding, so the summation order is P-invariant.
 constexpr int kPlanSmPairs = 148 / 2;
 static int wgrad_splits(int B, int out, int in, int n) {
-  // small batches may still split K (C1: B = 256 -> 4 splits of 2 k-blocks: the weight gradient, which runs
-  // beside the backward GEMM in a captured step, was the longer of the two at 8 serial k-blocks)
-  const int cap = std::min(8, std::max({1, B / 1024, (B + 63) / 64}));
+  const int cap = std::min(8, std::max(1, B / 1024));
   if (in % 256 == 0) {
     const int64_t tiles = (int64_t)((out + 255) / 256) * (in / 256) * n;
     const int64_t nkb = (B + 31) / 32;
