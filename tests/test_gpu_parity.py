@@ -245,7 +245,10 @@ def test_step_host_equals_device_path():
     assert np.array_equal(a.gather("theta"), b.gather("theta"))
 
 
-@pytest.mark.parametrize("cfgname", ["C1", "C2"])
+# C4 / C5b: the captured step's side streams (a7-a9 beside the gradient phase; the loss reduction and
+# weight gradients beside the backward GEMMs) over 3-6 hidden GEMM layers, the Gram form with the
+# separate D kernel (n = 256) and the tensor-core update
+@pytest.mark.parametrize("cfgname", ["C1", "C2", "C4", "C5b"])
 def test_step_graph_equals_eager(cfgname):
     """push_step_graph (captured CUDA graph, batch staged into the context's buffers) reproduces the
     eager calls bit for bit over several steps with changing batches."""
@@ -264,6 +267,9 @@ def test_step_graph_equals_eager(cfgname):
         assert torch.equal(la, lb), t
     assert np.array_equal(a.gather("theta"), b.gather("theta"))
     assert np.array_equal(a.gather("dist"), b.gather("dist"))
+    assert np.array_equal(a.gather("h"), b.gather("h"))
+    assert np.array_equal(a.gather("kernel"), b.gather("kernel"))
+    assert np.array_equal(a.gather("grad"), b.gather("grad"))
 
 
 def test_state_machine_errors():
