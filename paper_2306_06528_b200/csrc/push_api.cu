@@ -595,7 +595,8 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
     PUSH_CUDA_TRY(cudaEventRecord(c->ev_theta, c->comm_stream));
     c->theta_pending = true;
   }
-  if (fork_kphase && !P.ds) {
+  // single process only: with an exchange, a7-a9 stay in the step where they hide the G all-gather (C2)
+  if (fork_kphase && !P.ds && c->world == 1 && !c->comm) {
     PUSH_CUDA_TRY(cudaEventRecord(c->ev_kfork, s));
     PUSH_CUDA_TRY(cudaStreamWaitEvent(c->k_stream, c->ev_kfork, 0));
     if (c->theta_pending) PUSH_CUDA_TRY(cudaStreamWaitEvent(c->k_stream, c->ev_theta, 0));
