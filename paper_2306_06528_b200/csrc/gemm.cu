@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = ptx::lds_u32(ptx::smem_u32(tmem_slot));
+  PUSH_PDL_ENTRY();  // set-up above touched no global memory (common.cuh)
 
   auto tile_kb = [&](int split, int* kb0) {
     *kb0 = split * prm.kb_per_split;
@@ -655,6 +656,7 @@ __global__ void __launch_bounds__(k2Threads, 1)
   ptx::cluster_sync();  // the peer's barriers are initialised before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem_base = ptx::lds_u32(ptx::smem_u32(tmem_slot));
+  PUSH_PDL_ENTRY();  // set-up above touched no global memory (common.cuh)
 
   const int cid = (int)ptx::cluster_id_x(), ncl = (int)ptx::ncluster_x();
   auto tile_kb = [&](int split, int* kb0) {
@@ -932,8 +934,8 @@ push_status launch_t(const CUtensorMap* maps, const KParams& kp, cudaStream_t st
     attr_set = true;
   }
   const int grid = kp.ntiles < g_sms ? kp.ntiles : g_sms;
-  gemm3xtf32_kernel<BN, AMN, BMN, BS, EPI>
-      <<<grid, kThreads, C::SMEM_BYTES, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], kp);
+  launch_pdl(gemm3xtf32_kernel<BN, AMN, BMN, BS, EPI>, dim3(grid), dim3(kThreads), C::SMEM_BYTES, stream, maps[0],
+             maps[1], maps[2], maps[3], maps[4], kp);
   PUSH_CUDA_TRY(cudaGetLastError());
   return PUSH_OK;
 }
@@ -969,16 +971,18 @@ push_status launch2_t(const CUtensorMap* maps, const KParams& kp, cudaStream_t s
   static int max_pairs = 0;
   auto kern = gemm3xtf32_2sm_kernel<PBN, AMN, BMN, BS, EPI>;
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (common.cuh)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.blockDim = dim3(k2Threads);
   cfg.dynamicSmemBytes = Cfg2<PBN, EpiBoxes<EPI>::NB>::SMEM_BYTES;
   cfg.stream = stream;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 1;  // the occupancy query sees the cluster shape only
   if (!max_pairs) {
     PUSH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Cfg2<PBN, EpiBoxes<EPI>::NB>::SMEM_BYTES));
@@ -989,6 +993,7 @@ push_status launch2_t(const CUtensorMap* maps, const KParams& kp, cudaStream_t s
   }
   const int pairs = kp.ntiles < max_pairs ? kp.ntiles : max_pairs;
   cfg.gridDim = dim3(2 * pairs);
+  cfg.numAttrs = 2;
   PUSH_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], kp));
   return PUSH_OK;
 }

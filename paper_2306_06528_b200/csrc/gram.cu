@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = ptx::lds_u32(ptx::smem_u32(tmem_slot));
+  PUSH_PDL_ENTRY();  // set-up above touched no global memory (common.cuh)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer: RC (+4) columns of rows 0..NP-1 (OOB zero-filled)
@@ -307,7 +308,7 @@ push_status gram_launch(const float* theta, int64_t ld, int n, int splits, const
     attr = true;
   }
   const int n_ib = (n + 63) / 64;
-  gram_partial_kernel<NP><<<dim3(splits, n_ib), kGThreads, C::SMEM, s>>>(map, ranges, n, n_ib, part);
+  launch_pdl(gram_partial_kernel<NP>, dim3(dim3(splits, n_ib)), dim3(kGThreads), C::SMEM, s, map, ranges, n, n_ib, part);
   PUSH_CUDA_TRY(cudaGetLastError());
   return PUSH_OK;
 }
@@ -367,6 +368,7 @@ constexpr int kGRedWarps = 32;
 __global__ void __launch_bounds__(32 * kGRedWarps) gram_reduce_kernel(const float* __restrict__ part, int64_t pb,
                                                                       int S, const RankSlots rs,
                                                                       float* __restrict__ sums) {
+  PUSH_PDL_ENTRY();
   __shared__ float red[kGRedWarps][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t e = (int64_t)blockIdx.x * 32 + lane;
@@ -401,6 +403,7 @@ __global__ void __launch_bounds__(32 * kGRedWarps) gram_reduce_kernel(const floa
 
 // D_ij = D_ji (gram_d_value, gram_d.cuh) for i < j, D_ii = +0
 __global__ void gram_d_kernel(const float* __restrict__ sums, int n, int np, float* __restrict__ D) {
+  PUSH_PDL_ENTRY();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)n * n) return;
   const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
@@ -418,10 +421,10 @@ bool gram_d_in_bandwidth(int n) { return n <= kGramDInBandwidth; }
 
 void gram_dist(const float* part, int n, int S, const RankSlots& rs, float* sums, float* D, cudaStream_t s) {
   const int64_t pb = gram_part_floats(n);
-  gram_reduce_kernel<<<(unsigned)((pb + 31) / 32), 32 * kGRedWarps, 0, s>>>(part, pb, S, rs, sums);
+  launch_pdl(gram_reduce_kernel, dim3((unsigned)((pb + 31) / 32)), dim3(32 * kGRedWarps), 0, s, part, pb, S, rs, sums);
   if (gram_d_in_bandwidth(n)) return;  // the bandwidth kernel evaluates D while staging its keys
   const int64_t nn = (int64_t)n * n;
-  gram_d_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(sums, n, gram_np(n), D);
+  launch_pdl(gram_d_kernel, dim3((unsigned)((nn + 255) / 256)), dim3(256), 0, s, sums, n, gram_np(n), D);
 }
 
 }  // namespace kern

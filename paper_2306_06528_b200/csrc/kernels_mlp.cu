@@ -16,6 +16,7 @@ namespace kern {
 // ---------------------------------------------------------------- split (weights)
 __global__ void split_hilo_kernel(const float* __restrict__ src, int64_t src_pstride, float* __restrict__ hi,
                                   float* __restrict__ lo, int64_t dst_pstride, int64_t count) {
+  PUSH_PDL_ENTRY();
   const int p = blockIdx.y;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
     const float v = src[p * src_pstride + t];
@@ -27,7 +28,7 @@ __global__ void split_hilo_kernel(const float* __restrict__ src, int64_t src_pst
 void split_hilo(const float* src, int64_t src_pstride, float* hi, float* lo, int64_t dst_pstride, int64_t count,
                 int batch, cudaStream_t s) {
   const int blocks = (int)std::min<int64_t>((count + 255) / 256, 4096);
-  split_hilo_kernel<<<dim3(blocks, batch), 256, 0, s>>>(src, src_pstride, hi, lo, dst_pstride, count);
+  launch_pdl(split_hilo_kernel, dim3(dim3(blocks, batch)), dim3(256), 0, s, src, src_pstride, hi, lo, dst_pstride, count);
 }
 
 // ---------------------------------------------------------------- thin forward (narrow input)
@@ -41,6 +42,7 @@ __global__ void __launch_bounds__(256) thin_forward_narrow_kernel(const float* _
                                                                   int64_t off_w, int64_t off_b, int nin, int nout,
                                                                   int act, float* __restrict__ out,
                                                                   int64_t out_pstride, int B) {
+  PUSH_PDL_ENTRY();
   constexpr int NI = NIN > 0 ? NIN : kThinIn;
   const int p = blockIdx.y;
   const int b0 = blockIdx.x * 32, b1 = min(B, b0 + 32);
@@ -87,6 +89,7 @@ __global__ void __launch_bounds__(256) thin_forward_narrow_kernel(const float* _
 __global__ void thin_forward_kernel(const float* __restrict__ in, int64_t in_pstride, const float* __restrict__ theta,
                                     int64_t ld, int64_t off_w, int64_t off_b, int nin, int nout, int act,
                                     float* __restrict__ out, int64_t out_pstride, int B) {
+  PUSH_PDL_ENTRY();
   const int p = blockIdx.y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;  // B * nout < 2^31 (max_batch * width)
   if (t >= B * nout) return;
@@ -107,7 +110,7 @@ void thin_forward(const float* in, int64_t in_pstride, const float* theta, int64
     const int want = (out / per + 31) / 32 * 32;
     const int threads = want > 256 ? 256 : (want < 32 ? 32 : want);
 #define PUSH_THIN_FWD(N, V)                                                                                     \
-  thin_forward_narrow_kernel<N, V><<<grid, threads, 0, s>>>(in, in_pstride, theta, ld_theta, off_w, off_b, in_, \
+  launch_pdl(thin_forward_narrow_kernel<N, V>, dim3(grid), dim3(threads), 0, s, in, in_pstride, theta, ld_theta, off_w, off_b, in_, \
                                                             out, act, dst, out_pstride, B)
     if (v4) {
       if (in_ == 1) PUSH_THIN_FWD(1, 4);
@@ -124,7 +127,7 @@ void thin_forward(const float* in, int64_t in_pstride, const float* theta, int64
     return;
   }
   const int64_t tot = (int64_t)B * out;
-  thin_forward_kernel<<<dim3((unsigned)((tot + 255) / 256), batch), 256, 0, s>>>(in, in_pstride, theta, ld_theta, off_w,
+  launch_pdl(thin_forward_kernel, dim3(dim3((unsigned)((tot + 255) / 256), batch)), dim3(256), 0, s, in, in_pstride, theta, ld_theta, off_w,
                                                                                  off_b, in_, out, act, dst,
                                                                                  out_pstride, B);
 }
@@ -143,6 +146,7 @@ void thin_forward(const float* in, int64_t in_pstride, const float* theta, int64
 constexpr int kOutSmemH = 1024;
 template <int DOUT, bool SMEM>  // compile-time bound on d_out (loops below run to DOUT, masked by a.dout)
 __global__ void __launch_bounds__(256) output_fused_kernel(const OutputArgs a) {
+  PUSH_PDL_ENTRY();
   __shared__ float sdl[32][DOUT];
   __shared__ float serr[32][DOUT];
   extern __shared__ __align__(16) float sA[];
@@ -306,6 +310,7 @@ __device__ __forceinline__ void out_phase2(const float* ai, int H, int nr, const
 }
 template <int DOUT, int FPT>
 __global__ void __launch_bounds__(256) output_stream_kernel(const OutputArgs a, int R, int NST) {
+  PUSH_PDL_ENTRY();
   __shared__ float sdl[32][DOUT];
   __shared__ float serr[32][DOUT];
   extern __shared__ __align__(16) float sm[];  // [DOUT][H] W_L, then NST slabs of [R][H]
@@ -428,7 +433,7 @@ static void output_stream_launch(const OutputArgs& a, int batch, cudaStream_t s)
     cudaFuncSetAttribute(output_stream_kernel<DOUT, FPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  output_stream_kernel<DOUT, FPT><<<dim3((a.B + 31) / 32, batch), 256, smem, s>>>(a, R, NST);
+  launch_pdl(output_stream_kernel<DOUT, FPT>, dim3(dim3((a.B + 31) / 32, batch)), dim3(256), smem, s, a, R, NST);
 }
 template <int DOUT>
 static void output_launch(const OutputArgs& a, int batch, cudaStream_t s) {
@@ -451,9 +456,9 @@ static void output_launch(const OutputArgs& a, int batch, cudaStream_t s) {
                            32 * kOutSmemH * 4);
       attr = true;
     }
-    output_fused_kernel<DOUT, true><<<grid, 256, (size_t)32 * a.H * 4, s>>>(a);
+    launch_pdl(output_fused_kernel<DOUT, true>, dim3(grid), dim3(256), (size_t)32 * a.H * 4, s, a);
   } else {
-    output_fused_kernel<DOUT, false><<<grid, 256, 0, s>>>(a);
+    launch_pdl(output_fused_kernel<DOUT, false>, dim3(grid), dim3(256), 0, s, a);
   }
 }
 void output_fused(const OutputArgs& a, int batch, cudaStream_t s) {
@@ -468,6 +473,7 @@ void output_fused(const OutputArgs& a, int batch, cudaStream_t s) {
 __global__ void output_forward_kernel(const float* __restrict__ A, int64_t a_pstride, const float* __restrict__ theta,
                                       int64_t ld, int64_t off_w, int64_t off_b, int H, int dout,
                                       float* __restrict__ pred, int B) {
+  PUSH_PDL_ENTRY();
   const int p = blockIdx.y, lane = threadIdx.x & 31;
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (b >= B) return;
@@ -483,10 +489,11 @@ __global__ void output_forward_kernel(const float* __restrict__ A, int64_t a_pst
 }
 void output_forward(const float* A, int64_t a_pstride, const float* theta, int64_t ld, int64_t off_w, int64_t off_b,
                     int H, int dout, float* pred, int B, int batch, cudaStream_t s) {
-  output_forward_kernel<<<dim3((B + 7) / 8, batch), 256, 0, s>>>(A, a_pstride, theta, ld, off_w, off_b, H, dout, pred, B);
+  launch_pdl(output_forward_kernel, dim3(dim3((B + 7) / 8, batch)), dim3(256), 0, s, A, a_pstride, theta, ld, off_w, off_b, H, dout, pred, B);
 }
 __global__ void predict_stats_kernel(const float* __restrict__ pred, int n, int64_t m, float* __restrict__ mean,
                                      float* __restrict__ stdev) {
+  PUSH_PDL_ENTRY();
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= m) return;
   float s1 = 0.f;
@@ -501,11 +508,12 @@ __global__ void predict_stats_kernel(const float* __restrict__ pred, int n, int6
   if (stdev) stdev[t] = sqrtf(s2 / (float)n);
 }
 void predict_stats(const float* pred, int n, int64_t m, float* mean, float* stdev, cudaStream_t s) {
-  predict_stats_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(pred, n, m, mean, stdev);
+  launch_pdl(predict_stats_kernel, dim3((unsigned)((m + 255) / 256)), dim3(256), 0, s, pred, n, m, mean, stdev);
 }
 
 __global__ void loss_reduce_kernel(const float* __restrict__ err2, int64_t err_pstride, float* __restrict__ loss,
                                    int B, float denom) {
+  PUSH_PDL_ENTRY();
   __shared__ float sh[256];
   const int p = blockIdx.x;
   float acc = 0.f;
@@ -519,13 +527,14 @@ __global__ void loss_reduce_kernel(const float* __restrict__ err2, int64_t err_p
   if (threadIdx.x == 0) loss[p] = sh[0] / denom;
 }
 void loss_reduce(const float* err2, int64_t err_pstride, float* loss, int B, int d_out, int batch, cudaStream_t s) {
-  loss_reduce_kernel<<<batch, 256, 0, s>>>(err2, err_pstride, loss, B, (float)((int64_t)B * d_out));
+  launch_pdl(loss_reduce_kernel, dim3(batch), dim3(256), 0, s, err2, err_pstride, loss, B, (float)((int64_t)B * d_out));
 }
 
 // ---------------------------------------------------------------- thin backward (generic)
 __global__ void thin_backward_kernel(const float* __restrict__ dl, int64_t d_pstride, const float* __restrict__ theta,
                                      int64_t ld, int64_t off_w, int nin, int nout, const float* __restrict__ aprev,
                                      int64_t a_pstride, int act, float* __restrict__ o, int64_t o_pstride, int B) {
+  PUSH_PDL_ENTRY();
   const int p = blockIdx.y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= B * nin) return;
@@ -540,13 +549,14 @@ void thin_backward(const float* dl, int64_t d_pstride, const float* theta, int64
                    int out, const float* aprev, int64_t a_pstride, int act, float* o, int64_t o_pstride, int B,
                    int batch, cudaStream_t s) {
   const int64_t tot = (int64_t)B * in;
-  thin_backward_kernel<<<dim3((unsigned)((tot + 255) / 256), batch), 256, 0, s>>>(
+  launch_pdl(thin_backward_kernel, dim3(dim3((unsigned)((tot + 255) / 256), batch)), dim3(256), 0, s, 
       dl, d_pstride, theta, ld_theta, off_w, in, out, aprev, a_pstride, act, o, o_pstride, B);
 }
 
 // ---------------------------------------------------------------- thin weight-gradient partials (generic)
 __global__ void thin_wgrad_kernel(const float* __restrict__ dl, int64_t d_pstride, const float* __restrict__ A,
                                   int64_t a_pstride, int nin, int nout, float* __restrict__ part, int B) {
+  PUSH_PDL_ENTRY();
   const int p = blockIdx.z, s = blockIdx.y, P = gridDim.z;
   const int cols = nin + 1;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -570,7 +580,7 @@ int thin_wgrad(const float* dl, int64_t d_pstride, const float* A, int64_t a_pst
                int B, int batch, cudaStream_t s) {
   const int chunks = (B + THIN_CHUNK - 1) / THIN_CHUNK;
   const int64_t tot = (int64_t)out * (in_eff + 1);
-  thin_wgrad_kernel<<<dim3((unsigned)((tot + 255) / 256), chunks, batch), 256, 0, s>>>(dl, d_pstride, A, a_pstride,
+  launch_pdl(thin_wgrad_kernel, dim3(dim3((unsigned)((tot + 255) / 256), chunks, batch)), dim3(256), 0, s, dl, d_pstride, A, a_pstride,
                                                                                        in_eff, out, part, B);
   return chunks;
 }
@@ -710,6 +720,7 @@ struct FinalizeTable {
 __global__ void finalize_all_kernel(const __grid_constant__ FinalizeTable t, const float* __restrict__ theta,
                                     float* __restrict__ grad,
                                     int64_t ld, float lambda, int prior, float inv_sigma2) {
+  PUSH_PDL_ENTRY();
   const int p = blockIdx.y;
   int k = 0;
   while (k + 1 < t.n && (int)blockIdx.x >= t.j[k + 1].blk0) ++k;
@@ -762,18 +773,19 @@ void finalize_all(const FinalizeJob* jobs, int njobs, const float* theta, float*
     t.j[k].blk0 = blk;
     blk += jobs[k].nb_w + jobs[k].nb_b;
   }
-  finalize_all_kernel<<<dim3(blk, batch), 256, 0, s>>>(t, theta, grad, ld, lambda, prior, inv_sigma2);
+  launch_pdl(finalize_all_kernel, dim3(dim3(blk, batch)), dim3(256), 0, s, t, theta, grad, ld, lambda, prior, inv_sigma2);
 }
 
 // ---------------------------------------------------------------- set_grads copy
 __global__ void copy_rows_kernel(const float* __restrict__ src, int64_t d, float* __restrict__ dst, int64_t ld) {
+  PUSH_PDL_ENTRY();
   const int p = blockIdx.y;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < d; t += (int64_t)gridDim.x * blockDim.x)
     dst[p * ld + t] = src[p * d + t];
 }
 void copy_rows(const float* src, int64_t d, float* dst, int64_t ld, int rows, cudaStream_t s) {
   const int blocks = (int)std::min<int64_t>((d + 255) / 256, 2048);
-  copy_rows_kernel<<<dim3(blocks, rows), 256, 0, s>>>(src, d, dst, ld);
+  launch_pdl(copy_rows_kernel, dim3(dim3(blocks, rows)), dim3(256), 0, s, src, d, dst, ld);
 }
 
 }  // namespace kern

@@ -27,6 +27,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 
 __global__ void init_theta_kernel(float* __restrict__ theta, int64_t ld, int row0, int64_t d, uint64_t seed,
                                   InitTable t) {
+  PUSH_PDL_ENTRY();
   const int64_t row = row0 + blockIdx.y;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ld; k += (int64_t)gridDim.x * blockDim.x) {
     float v = 0.f;
@@ -44,7 +45,7 @@ __global__ void init_theta_kernel(float* __restrict__ theta, int64_t ld, int row
 void init_theta(float* theta, int64_t ld, int row0, int rows, int64_t d, uint64_t seed, const InitTable& t,
                 cudaStream_t s) {
   const int blocks = (int)std::min<int64_t>((ld + 255) / 256, 1024);
-  init_theta_kernel<<<dim3(blocks, rows), 256, 0, s>>>(theta, ld, row0, d, seed, t);
+  launch_pdl(init_theta_kernel, dim3(dim3(blocks, rows)), dim3(256), 0, s, theta, ld, row0, d, seed, t);
 }
 
 // ---------------------------------------------------------------- a7 distances
@@ -101,6 +102,7 @@ template <int T, int RT>
 __global__ void __launch_bounds__(256) dist_partial_kernel(const float* __restrict__ theta, int64_t ld, int n,
                                                            int ntile, const int64_t* __restrict__ ranges,
                                                            float* __restrict__ part) {
+  PUSH_PDL_ENTRY();
   constexpr int CW = DistCW<T>::v, NBUF = DistBufs<T>::v;
   constexpr int TP = T / RT, PT = TP * TP, G = 256 / PT, RS = CW + kDistPad;
   extern __shared__ __align__(16) float dsm[];  // [NBUF bufs][2 tiles][T][RS], then G*PT*RT*RT reduction
@@ -221,6 +223,7 @@ template <> struct DistVec<2> { using T = float2; };
 template <int N, int CT>
 __global__ void __launch_bounds__(kDistSmallThreads, N <= 8 ? 2 : 1) dist_small_kernel(
     const float* __restrict__ theta, int64_t ld, const int64_t* __restrict__ ranges, float* __restrict__ part) {
+  PUSH_PDL_ENTRY();
   using V = typename DistVec<CT>::T;
   constexpr int NP = N * (N - 1) / 2;
   __shared__ float red[kDistSmallThreads / 32][NP > 0 ? NP : 1];
@@ -305,13 +308,13 @@ static void dist_launch(const float* theta, int64_t ld, int n, const DistPlan& p
     cudaFuncSetAttribute(dist_partial_kernel<T, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  dist_partial_kernel<T, RT><<<dim3(pl.npairs, pl.splits), 256, smem, s>>>(theta, ld, n, pl.ntile, ranges, part);
+  launch_pdl(dist_partial_kernel<T, RT>, dim3(dim3(pl.npairs, pl.splits)), dim3(256), smem, s, theta, ld, n, pl.ntile, ranges, part);
 }
 void dist_partial(const float* theta, int64_t ld, int n, const DistPlan& pl, const int64_t* ranges, float* part,
                   cudaStream_t s) {
   if (pl.T == 8 && n >= 2) {  // (n = 9..16 through this kernel measured slower at C2: 39 vs 28 us)
     const dim3 grid(1, pl.splits);
-#define PUSH_DIST_SMALL(NN, CT) dist_small_kernel<NN, CT><<<grid, kDistSmallThreads, 0, s>>>(theta, ld, ranges, part)
+#define PUSH_DIST_SMALL(NN, CT) launch_pdl(dist_small_kernel<NN, CT>, dim3(grid), dim3(kDistSmallThreads), 0, s, theta, ld, ranges, part)
     switch (n) {
       case 2: PUSH_DIST_SMALL(2, 4); break;
       case 3: PUSH_DIST_SMALL(3, 4); break;
@@ -338,6 +341,7 @@ constexpr int kRedWarps = 32;
 __global__ void __launch_bounds__(32 * kRedWarps) dist_reduce_kernel(const float* __restrict__ part, int n, int tensors,
                                                                      const TSplit ts, const RankSlots rs,
                                                                      float* __restrict__ D) {
+  PUSH_PDL_ENTRY();
   __shared__ float red[kRedWarps][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nn = (int64_t)n * n;
@@ -378,7 +382,7 @@ __global__ void __launch_bounds__(32 * kRedWarps) dist_reduce_kernel(const float
 }
 void dist_reduce(const float* part, int n, const DistPlan& pl, const RankSlots& rs, float* D, cudaStream_t s) {
   const int64_t groups = ((int64_t)n * n + 31) / 32;
-  dist_reduce_kernel<<<(unsigned)(groups * pl.tensors), 32 * kRedWarps, 0, s>>>(part, n, pl.tensors, pl.tsplit, rs, D);
+  launch_pdl(dist_reduce_kernel, dim3((unsigned)(groups * pl.tensors)), dim3(32 * kRedWarps), 0, s, part, n, pl.tensors, pl.tsplit, rs, D);
 }
 
 // ---------------------------------------------------------------- a8 + a9
@@ -600,6 +604,7 @@ __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(float* D, int n, i
                                                               float* __restrict__ K, float* __restrict__ srow,
                                                               int use_tri, int krows_here,
                                                               const float* __restrict__ gsums, int gnp) {
+  PUSH_PDL_ENTRY();
   extern __shared__ float skeys[];
   // CTA b: tensor b's distance matrix, bandwidth, kernel rows and row sums
   D += (int64_t)blockIdx.x * n * n;
@@ -699,6 +704,7 @@ __global__ void __launch_bounds__(1024) bandwidth_kernel_impl(float* D, int n, i
 // K rows over many CTAs (warp per own row) once h is known: same per-row arithmetic as above
 __global__ void kernel_rows_kernel(const float* __restrict__ D, int n, int row0, int nl, const float* __restrict__ h_in,
                                    float* __restrict__ K, float* __restrict__ srow) {
+  PUSH_PDL_ENTRY();
   const int t = blockIdx.y;  // tensor
   D += (int64_t)t * n * n;
   K += (int64_t)t * nl * n;
@@ -718,10 +724,10 @@ void bandwidth_kernel(const float* D, int n, int row0, int nl, int rule, float c
   // K rows in the same CTA for small n_local * n, else spread over the SMs by a second launch (C4: 256
   // rows x 256 exp on one SM were a third of the kernel)
   const int split = (int64_t)nl * n >= 16384;
-  bandwidth_kernel_impl<<<tensors, 1024, use_tri ? (size_t)m * 4 : 0, s>>>(const_cast<float*>(D), n, row0, nl, rule, c_ln, bw_h, h, K, srow,
+  launch_pdl(bandwidth_kernel_impl, dim3(tensors), dim3(1024), use_tri ? (size_t)m * 4 : 0, s, const_cast<float*>(D), n, row0, nl, rule, c_ln, bw_h, h, K, srow,
                                                                     use_tri, split ? 0 : 1, gsums,
                                                                     gsums ? gram_np(n) : 0);
-  if (split) kernel_rows_kernel<<<dim3((nl + 7) / 8, tensors), 256, 0, s>>>(D, n, row0, nl, h, K, srow);
+  if (split) launch_pdl(kernel_rows_kernel, dim3(dim3((nl + 7) / 8, tensors)), dim3(256), 0, s, D, n, row0, nl, h, K, srow);
 }
 
 // ---------------------------------------------------------------- a10 fused update
@@ -750,6 +756,7 @@ __global__ void __launch_bounds__(128) svgd_update_kernel(const float* __restric
                                                           const float* __restrict__ srow,
                                                           const float* __restrict__ hptr, float eps_n,
                                                           float* __restrict__ theta_next) {
+  PUSH_PDL_ENTRY();
   using V = typename VecT<CT>::T;
   extern __shared__ __align__(16) float sKT[];  // [n][RB]: K_(rb0+i),j at sKT[j*RB + i]
   const int rb0 = blockIdx.y * RB;
@@ -813,7 +820,7 @@ static void update_launch(const float* theta, const float* grad, int64_t ld, int
     attr = true;
   }
   const dim3 grid((unsigned)((ld / CT + kUpdThreads - 1) / kUpdThreads), (unsigned)((nl + RB - 1) / RB));
-  svgd_update_kernel<RB, CT><<<grid, kUpdThreads, smem, s>>>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n,
+  launch_pdl(svgd_update_kernel<RB, CT>, dim3(grid), dim3(kUpdThreads), smem, s, theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n,
                                                              theta_next);
 }
 // Many own rows (n_local >= 32): one CTA covers 64 own rows (4 row groups of 16, one per pair of
@@ -828,6 +835,7 @@ __global__ void __launch_bounds__(256) svgd_update_staged_kernel(const float* __
                                                                  const float* __restrict__ srow,
                                                                  const float* __restrict__ hptr, float eps_n,
                                                                  float* __restrict__ theta_next) {
+  PUSH_PDL_ENTRY();
   extern __shared__ __align__(16) float usm[];
   float* sKT = usm;                                   // [n][64]: K_(rb0+i),j at sKT[j*64 + i]
   float* sTG = usm + (size_t)n * kUpdSRows;           // [2 stages][kUpdJ][2][256]
@@ -917,7 +925,7 @@ static void update_staged_launch(const float* theta, const float* grad, int64_t 
     attr = true;
   }
   const dim3 grid((unsigned)((ld + kUpdSCols - 1) / kUpdSCols), (unsigned)((nl + kUpdSRows - 1) / kUpdSRows));
-  svgd_update_staged_kernel<<<grid, 256, smem, s>>>(theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next);
+  launch_pdl(svgd_update_staged_kernel, dim3(grid), dim3(256), smem, s, theta, grad, ld, n, row0, nl, K, srow, h, eps_over_n, theta_next);
 }
 // (RB, CT) = (16, 4) (8 x 4 when n_local <= 16: twice the CTAs for the L2-resident C2 update, 15 -> 13
 // us): measured fastest (C3 1.7 ms vs 2.2 ms for 32 x 2 and 2.5 ms for 64 x 1, whose lower re-read
@@ -940,6 +948,7 @@ int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int ro
 // ---------------------------------------------------------------- a10 on the tensor cores (n_local >= 32)
 __global__ void update_lhs_kernel(const float* __restrict__ K, int nl, int npad, int n, int pitch,
                                   const float* __restrict__ hptr, int g_first, float* __restrict__ lhs) {
+  PUSH_PDL_ENTRY();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)npad * pitch) return;
   const int i = (int)(e / pitch), q = (int)(e - (int64_t)i * pitch);
@@ -955,11 +964,12 @@ __global__ void update_lhs_kernel(const float* __restrict__ K, int nl, int npad,
 void update_lhs(const float* K, int nl, int npad, int n, int pitch, const float* h, bool g_first, float* lhs,
                 cudaStream_t s) {
   const int64_t tot = (int64_t)npad * pitch;
-  update_lhs_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(K, nl, npad, n, pitch, h, g_first ? 1 : 0, lhs);
+  launch_pdl(update_lhs_kernel, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, s, K, nl, npad, n, pitch, h, g_first ? 1 : 0, lhs);
 }
 
 __global__ void update_fixup_kernel(const float* __restrict__ th, int64_t ld4, const float* __restrict__ srow,
                                     const float* __restrict__ hptr, float eps_n, float* __restrict__ next) {
+  PUSH_PDL_ENTRY();
   const int i = blockIdx.y;
   const float rs = (2.0f / *hptr) * srow[i];
   const float4* t4 = reinterpret_cast<const float4*>(th) + (int64_t)i * ld4;
@@ -978,7 +988,7 @@ void update_fixup(const float* theta_own, int64_t ld, int nl, const float* srow,
                   float* next_own, cudaStream_t s) {
   const int64_t ld4 = ld / 4;
   const int bx = (int)std::min<int64_t>((ld4 + 255) / 256, std::max<int64_t>(1, 4 * 148 / nl + 1));
-  update_fixup_kernel<<<dim3(bx, nl), 256, 0, s>>>(theta_own, ld4, srow, h, eps_n, next_own);
+  launch_pdl(update_fixup_kernel, dim3(dim3(bx, nl)), dim3(256), 0, s, theta_own, ld4, srow, h, eps_n, next_own);
 }
 
 // ---------------------------------------------------------------- NEXT-2: PusH's own update (variants)
@@ -998,6 +1008,7 @@ __global__ void __launch_bounds__(kVarSegCols) svgd_update_var_kernel(
     const float* __restrict__ theta, const float* __restrict__ grad, int64_t ld, int n, int row0, int nl,
     const float* __restrict__ K, const float* __restrict__ srow, const float* __restrict__ hptr,
     const int4* __restrict__ segs, float alpha, float eps_d, float pcoef, float* __restrict__ theta_next) {
+  PUSH_PDL_ENTRY();
   extern __shared__ __align__(16) float sKT[];  // [n][RB]: K^t_(rb0+i),j at sKT[j*RB + i]
   const int4 seg = segs[blockIdx.x];
   const int t = seg.z;
@@ -1051,7 +1062,7 @@ static void update_var_launch(const float* theta, const float* grad, int64_t ld,
     attr = true;
   }
   const dim3 grid((unsigned)nseg, (unsigned)((nl + RB - 1) / RB));
-  svgd_update_var_kernel<RB><<<grid, kVarSegCols, sizeof(float) * RB * n, s>>>(
+  launch_pdl(svgd_update_var_kernel<RB>, dim3(grid), dim3(kVarSegCols), sizeof(float) * RB * n, s, 
       theta, grad, ld, n, row0, nl, K, srow, h, segs, alpha, eps_d, pcoef, theta_next);
 }
 int svgd_update_var(const float* theta, const float* grad, int64_t ld, int n, int row0, int nl, const float* K,
@@ -1066,6 +1077,7 @@ int svgd_update_var(const float* theta, const float* grad, int64_t ld, int n, in
 
 // ---------------------------------------------------------------- NEXT-3: deep ensembles and diagonal SWAG
 __global__ void ensemble_step_kernel(float* __restrict__ theta, const float* __restrict__ grad, int64_t n4, float eps) {
+  PUSH_PDL_ENTRY();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n4; t += (int64_t)gridDim.x * blockDim.x) {
     float4 th = reinterpret_cast<float4*>(theta)[t];
     const float4 g = __ldg(reinterpret_cast<const float4*>(grad) + t);
@@ -1078,10 +1090,11 @@ __global__ void ensemble_step_kernel(float* __restrict__ theta, const float* __r
 }
 void ensemble_step(float* theta, const float* grad, int64_t ld, int rows, float eps, cudaStream_t s) {
   const int64_t n4 = ld * rows / 4;  // ld % 32 == 0: whole float4s, padding stays 0 (g padding is 0)
-  ensemble_step_kernel<<<(unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 32), 256, 0, s>>>(theta, grad, n4, eps);
+  launch_pdl(ensemble_step_kernel, dim3((unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 32)), dim3(256), 0, s, theta, grad, n4, eps);
 }
 __global__ void swag_collect_kernel(const float* __restrict__ x, float* __restrict__ mean, float* __restrict__ sq,
                                     int64_t count, float kf, float inv) {
+  PUSH_PDL_ENTRY();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
     const float v = x[t];
     const float m = kf > 0.f ? mean[t] : 0.f, q = kf > 0.f ? sq[t] : 0.f;
@@ -1091,11 +1104,12 @@ __global__ void swag_collect_kernel(const float* __restrict__ x, float* __restri
 }
 void swag_collect(const float* x, float* mean, float* sq, int64_t count, int64_t k, cudaStream_t s) {
   const float kf = (float)k, inv = 1.0f / (float)(k + 1);
-  swag_collect_kernel<<<(unsigned)std::min<int64_t>((count + 255) / 256, 148 * 32), 256, 0, s>>>(x, mean, sq, count,
+  launch_pdl(swag_collect_kernel, dim3((unsigned)std::min<int64_t>((count + 255) / 256, 148 * 32)), dim3(256), 0, s, x, mean, sq, count,
                                                                                               kf, inv);
 }
 __global__ void swag_sample_kernel(const float* __restrict__ mean, const float* __restrict__ sq, int64_t ld, int64_t d,
                                    int row0, uint64_t seed, float* __restrict__ out) {
+  PUSH_PDL_ENTRY();
   const int r = blockIdx.y;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < d; c += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t ctr = ((static_cast<uint64_t>(row0 + r) << 32) | static_cast<uint64_t>(c)) * 2ull;
@@ -1110,7 +1124,7 @@ __global__ void swag_sample_kernel(const float* __restrict__ mean, const float* 
 void swag_sample(const float* mean, const float* sq, int64_t ld, int64_t d, int row0, int rows, uint64_t seed,
                  float* out, cudaStream_t s) {
   const int blocks = (int)std::min<int64_t>((d + 255) / 256, 1024);
-  swag_sample_kernel<<<dim3(blocks, rows), 256, 0, s>>>(mean, sq, ld, d, row0, seed, out);
+  launch_pdl(swag_sample_kernel, dim3(dim3(blocks, rows)), dim3(256), 0, s, mean, sq, ld, d, row0, seed, out);
 }
 
 }  // namespace kern

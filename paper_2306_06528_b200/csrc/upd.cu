@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = ptx::lds_u32(ptx::smem_u32(tmem_slot));
+  PUSH_PDL_ENTRY();  // set-up above touched no global memory (common.cuh)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -239,7 +240,7 @@ push_status update_tc_launch(const float* b, int n, int64_t w, int rows, const f
   }
   const int64_t ntile = w / kUCols;
   const int grid = (int)std::min<int64_t>(ntile, gemm::sm_count() > 0 ? gemm::sm_count() : 148);
-  svgd_update_tc_kernel<NPAD><<<grid, kUThreads, UCfg<NPAD>::SMEM, s>>>(tB, tLhi, tLlo, 2 * n, w, rows, out);
+  launch_pdl(svgd_update_tc_kernel<NPAD>, dim3(grid), dim3(kUThreads), UCfg<NPAD>::SMEM, s, tB, tLhi, tLlo, 2 * n, w, rows, out);
   PUSH_CUDA_TRY(cudaGetLastError());
   return PUSH_OK;
 }
@@ -251,6 +252,7 @@ push_status update_tc_launch(const float* b, int n, int64_t w, int rows, const f
 __global__ void update_lhs_split_kernel(const float* __restrict__ K, int nl, int npad, int n, int pitch, int own_row,
                                         const float* __restrict__ hptr, const float* __restrict__ srow, float eps_n,
                                         int g_first, float* __restrict__ hi, float* __restrict__ lo) {
+  PUSH_PDL_ENTRY();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)npad * pitch) return;
   const int i = (int)(e / pitch), q = (int)(e - (int64_t)i * pitch);
@@ -289,7 +291,7 @@ push_status update_tc_stream(const float* b, bool g_first, int n, int64_t w, int
   if (st != PUSH_OK) return st;
   const int npad = update_tc_npad(rows), pitch = ((2 * n + 3) / 4) * 4;
   const int64_t tot = (int64_t)npad * pitch;
-  update_lhs_split_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(K, rows, npad, n, pitch, own_row, h, srow,
+  launch_pdl(update_lhs_split_kernel, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, s, K, rows, npad, n, pitch, own_row, h, srow,
                                                                          eps_n, g_first ? 1 : 0, lhs_hi, lhs_lo);
   switch (npad) {
     case 16: return update_tc_launch<16>(b, n, w, rows, lhs_hi, lhs_lo, pitch, out, s);
