@@ -170,10 +170,11 @@ void update_lhs(const float* K, int nl, int npad, int n, int pitch, const float*
                 cudaStream_t s);
 void update_fixup(const float* theta_own, int64_t ld, int nl, const float* srow, const float* h, float eps_n,
                   float* next_own, cudaStream_t s);
-// a10 streaming on the tensor cores with the update in the epilogue (upd.cu), n <= 64, rows <= 64:
-// out[i][c] = th_i[c] + eps_n (sum_q lhs[i][q] B[q][c] + r s_i th_i[c]), B = the 2n x w operand at b
-// ([G; Theta] when g_first), th_i = Theta row own_row + i of B, lhs = [K, -rK] / [-rK, K] split into tf32
-// hi / lo (lhs_hi, lhs_lo: scratch of update_tc_npad(rows) x round_up(2n, 4) floats each); w % 128 == 0
+// a10 as one streaming tensor-core contraction (upd.cu, R28), n <= 64, rows <= 64:
+// out[i][c] = sum_q L[i][q] B[q][c], B = the 2n x w operand at b ([G; Theta] when g_first), L the folded
+// coefficients (eps_n K_ij on G rows; -eps_n r K_ij on Theta rows plus 1 + eps_n r (s_i - K_ii) on the own
+// particle own_row + i), split into tf32 hi / lo (lhs_hi, lhs_lo: scratch of update_tc_npad(rows) x
+// round_up(2n, 4) floats each); = th_i + eps_n (sum_j K_ij (g_j - r th_j) + r s_i th_i); w % 128 == 0
 constexpr int kUpdTcMaxRows = 64;
 int update_tc_npad(int rows);
 push_status update_tc_stream(const float* b, bool g_first, int n, int64_t w, int rows, int own_row, const float* K,

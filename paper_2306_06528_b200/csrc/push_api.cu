@@ -242,9 +242,9 @@ static push_status make_plan(const push_config* c, int world, Plan* p) {
   // depends on n only (never on n_local or the exchange mode), so every sharding and the d-sharded
   // panels take the same arithmetic (P-invariance).
   P.tc_update = c->variant == 0 && P.n >= kTcUpdateMinN && P.ld % 128 == 0;
-  // 32 <= n <= 64 (C3, S1): the streaming contraction (upd.cu) with the update in its epilogue: B read
-  // once from HBM, no U round trip (the staged CUDA-core kernel was FP32-issue / latency bound at ~0.3 of
-  // HBM there).  n only, as above.
+  // 32 <= n <= 64 (C3, S1): theta' as one streaming contraction with the folded coefficients (upd.cu,
+  // DESIGN.md R28): B read once from HBM, no U round trip (the staged CUDA-core kernel was FP32-issue /
+  // latency bound at ~0.3 of HBM there; this one measured 0.77-0.81 of HBM).  n only, as above.
   P.tc_stream = c->variant == 0 && P.n >= kTcStreamMinN && P.n <= kern::kUpdTcMaxRows && P.ld % 128 == 0;
   if (P.ds) {
     const int S = P.dist.splits;
