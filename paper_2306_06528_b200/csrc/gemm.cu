@@ -1058,8 +1058,11 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   // the next tile) are fastest; the 1-CTA kernel covers the remaining (narrow) shapes
   // (profiles/r01_gemm.md).
   const bool dbg_ok = !(pb.passes >> 8 & (1 | 8));
-  const bool pair256 = dbg_ok && !pb.no_pair && pb.N % 256 == 0 && (pb.epi == EPI_STORE || pb.K >= kFb256MinK);
-  const bool pair128 = dbg_ok && !pb.no_pair && !pair256 && pb.N % 128 == 0;
+  // M <= 128 (a batch of 128 in the forward / backward GEMMs, C5b): a 256-row pair tile would spend half
+  // its MMAs on rows past M, so the 1-CTA kernel (128-row tiles) takes those shapes
+  const bool pair_ok = dbg_ok && !pb.no_pair && pb.M > BM;
+  const bool pair256 = pair_ok && pb.N % 256 == 0 && (pb.epi == EPI_STORE || pb.K >= kFb256MinK);
+  const bool pair128 = pair_ok && !pair256 && pb.N % 128 == 0;
   const bool pair = pair256 || pair128;
   const int BN = pair256 ? 256 : (pair128 ? 128 : choose_bn(pb.N));
   const int box_b = pair ? BN / 2 : BN;
