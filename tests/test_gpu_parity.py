@@ -272,6 +272,25 @@ def test_step_graph_equals_eager(cfgname):
     assert np.array_equal(a.gather("grad"), b.gather("grad"))
 
 
+def test_step_graph_recapture_with_changing_batch():
+    """Changing B between captured steps re-captures the graph (side streams, events, programmatic
+    launches recorded afresh); every step stays bit-identical to the eager calls."""
+    w = WORKLOADS["C2"]
+    dims = list(w.dims)
+    a = push.Context(push.make_config(w.n_particles, dims, max_batch=w.batch, seed=8, step_size=1e-2))
+    b = push.Context(push.make_config(w.n_particles, dims, max_batch=w.batch, seed=8, step_size=1e-2))
+    la = torch.empty(w.n_particles, device="cuda")
+    lb = torch.empty(w.n_particles, device="cuda")
+    for t, B in enumerate([w.batch, 1000, w.batch, 37, 37, w.batch]):
+        x, y = synth.workload_batch(w, t)
+        xd, yd = _dev(x[:B]), _dev(y[:B])
+        a.particle_grads(xd, yd, la)
+        a.svgd_step()
+        b.step_graph(xd, yd, lb)
+        assert torch.equal(la, lb), (t, B)
+    assert np.array_equal(a.gather("theta"), b.gather("theta"))
+
+
 def test_state_machine_errors():
     ctx = push.Context(push.make_config(2, [1, 32, 1], max_batch=8))
     with pytest.raises(push.PushError) as e:
