@@ -83,6 +83,8 @@ struct KParams {
                    // bit 3 accumulate the whole K in TMEM (no fp32 promotion)
   const float* bias;
   long long bias_pstride;
+  const float* srow;  // UPD
+  const float* hptr;
   float* bpart;
   long long bp_sstride, bp_pstride;
   const float* x;
@@ -178,7 +180,7 @@ __device__ __forceinline__ float4 load_bias4(const KParams& prm, int lane, int c
 // 2 + kAuxAhead boxes; the others double-buffer their stores.
 constexpr int kAuxAhead = 2;
 template <int EPI>
-struct EpiBoxes { static constexpr int NB = EPI == EPI_BWD ? 2 + kAuxAhead : 2; };
+struct EpiBoxes { static constexpr int NB = (EPI == EPI_BWD || EPI == EPI_UPD) ? 2 + kAuxAhead : 2; };
 
 template <int CW, int EPI, int ACT>
 __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& prm, const CUtensorMap* tOut,
@@ -186,7 +188,13 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
                                          uint32_t ebuf_s, int lane, int row0, int colw, int p, int pz,
                                          float4 bias4) {
   constexpr bool bwd = EPI == EPI_BWD;
+  constexpr bool aux = EPI == EPI_BWD || EPI == EPI_UPD;  // an [m][n] tile is loaded beside the output
   constexpr int NB = EpiBoxes<EPI>::NB;
+  float urs = 0.f;  // UPD: (2/h) s_row for this thread's row (rows past M are never stored)
+  if constexpr (EPI == EPI_UPD) {
+    const int row = row0 + lane;
+    if (row < prm.M) urs = (2.0f / __ldg(prm.hptr)) * __ldg(prm.srow + row);
+  }
         // Output in 16-column groups g, double-buffered: group g is staged in half-box (g & 1)
         // (32 rows x 16 fp32, SWIZZLE_64B: 16-B chunk c of row r sits at chunk c ^ ((r >> 1) & 3)),
         // so the TMA store of group g overlaps the math of group g + 1.
@@ -208,8 +216,8 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
         for (int g = 0; g < G; ++g) {
           const int col = colw + g * 16;
           const uint32_t buf = ebuf_s + (g % NB) * kHalfBox;
-          if constexpr (bwd) {
-            ptx::mbar_wait(auxbar + (g % NB), (aux_ph >> (g % NB)) & 1);  // aprev of group g is in buf
+          if constexpr (aux) {
+            ptx::mbar_wait(auxbar + (g % NB), (aux_ph >> (g % NB)) & 1);  // aux tile of group g is in buf
             aux_ph ^= 1u << (g % NB);
             // prefetch aprev of group g + kAuxAhead into box (g + kAuxAhead) % NB once the store of its
             // previous tenant (group g - 2) has read it: only the latest store (group g - 1) may be pending
@@ -252,6 +260,20 @@ __device__ __forceinline__ void epi_tile(const float (&acc)[CW], const KParams& 
               v.y = acc[g * 16 + 4 * c4 + 1] * act_deriv_from_a(a.y, ACT);
               v.z = acc[g * 16 + 4 * c4 + 2] * act_deriv_from_a(a.z, ACT);
               v.w = acc[g * 16 + 4 * c4 + 3] * act_deriv_from_a(a.w, ACT);
+              ptx::sts_f4(pp, v);
+            }
+          } else if constexpr (EPI == EPI_UPD) {
+            // t + eps (acc + r s t) (the former fix-up pass), row = row0 + lane (rs per thread)
+            const float al = prm.alpha;
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const uint32_t pp = buf + roff + ((c4 ^ swz) << 4);
+              const float4 a = ptx::lds_f4(pp);
+              float4 v;
+              v.x = fmaf(al, fmaf(urs, a.x, acc[g * 16 + 4 * c4 + 0]), a.x);
+              v.y = fmaf(al, fmaf(urs, a.y, acc[g * 16 + 4 * c4 + 1]), a.y);
+              v.z = fmaf(al, fmaf(urs, a.z, acc[g * 16 + 4 * c4 + 2]), a.z);
+              v.w = fmaf(al, fmaf(urs, a.w, acc[g * 16 + 4 * c4 + 3]), a.w);
               ptx::sts_f4(pp, v);
             }
           } else {
@@ -356,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::prefetch_tmap(&tBhi);
     if (!BSPLIT) ptx::prefetch_tmap(&tBlo);
     if (prm.store) ptx::prefetch_tmap(&tOut);
-    if (EPI == EPI_BWD) ptx::prefetch_tmap(&tAux);
+    if (EPI == EPI_BWD || EPI == EPI_UPD) ptx::prefetch_tmap(&tAux);
   }
   if (warp == 1) {
     ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -510,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ebuf_s = ptx::smem_u32(ebuf_all + e * NB * kHalfBox);
       const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
       uint32_t ch = 0, aux_ph = 0;
-      constexpr bool bwd = EPI == EPI_BWD;
+      constexpr bool aux = EPI == EPI_BWD || EPI == EPI_UPD;
       for (int t = blockIdx.x; t < prm.ntiles; t += gridDim.x) {
         TileCoord tc = decode(t, prm);
         const int n0 = tc.nt * BN;
@@ -521,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row0 = tc.m0 + q * 32;
         const bool live = row0 < prm.M;
         const int colw = n0 + h * C::CW;
-        if (bwd && live && lane == 0) {  // prefetch aprev of the first groups while the MMAs run
+        if (aux && live && lane == 0) {  // prefetch aprev / theta of the first groups while the MMAs run
           ptx::bulk_wait_read0();
 #pragma unroll
           for (int g = 0; g < kAuxAhead && g < C::CW / 16; ++g) {
@@ -645,7 +667,7 @@ __global__ void __launch_bounds__(k2Threads, 1)
     ptx::prefetch_tmap(&tBhi);
     if (!BSPLIT) ptx::prefetch_tmap(&tBlo);
     if (prm.store) ptx::prefetch_tmap(&tOut);
-    if (EPI == EPI_BWD) ptx::prefetch_tmap(&tAux);
+    if (EPI == EPI_BWD || EPI == EPI_UPD) ptx::prefetch_tmap(&tAux);
   }
   if (warp == 1) {
     ptx::tmem_alloc2(tmem_slot, C::TMEM_COLS);
@@ -952,6 +974,7 @@ push_status launch_bn(bool amn, bool bmn, bool bs, int epi, const CUtensorMap* m
   if (epi == EPI_BWD && !amn && bmn)
     return bs ? launch_t<BN, false, true, true, EPI_BWD>(maps, kp, s)
               : launch_t<BN, false, true, false, EPI_BWD>(maps, kp, s);
+  if (epi == EPI_UPD && !amn && bmn && bs) return launch_t<BN, false, true, true, EPI_UPD>(maps, kp, s);
   if (epi != EPI_STORE) return fail(PUSH_E_INVALID, "gemm: fused epilogue with an unsupported operand layout");
   const int key = (amn ? 4 : 0) | (bmn ? 2 : 0) | (bs ? 1 : 0);
   switch (key) {
@@ -1045,8 +1068,10 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   if ((pb.A.ld % 4) || (pb.B.ld % 4) || (pb.A.pstride % 4) || (pb.B.pstride % 4) || (pb.ldo % 4) ||
       (pb.out_pstride % 4))
     return fail(PUSH_E_SHAPE, "gemm: strides must be multiples of 4 elements");
-  if (pb.epi == EPI_BWD && (!pb.aprev || (pb.ld_aprev % 4) || (pb.aprev_pstride % 4)))
-    return fail(PUSH_E_SHAPE, "gemm: BWD needs aprev with strides % 4 == 0");
+  if ((pb.epi == EPI_BWD || pb.epi == EPI_UPD) && (!pb.aprev || (pb.ld_aprev % 4) || (pb.aprev_pstride % 4)))
+    return fail(PUSH_E_SHAPE, "gemm: BWD / UPD need aprev with strides % 4 == 0");
+  if (pb.epi == EPI_UPD && (!pb.srow || !pb.hptr || pb.batch != 1))
+    return fail(PUSH_E_INVALID, "gemm: UPD needs srow, hptr and one batch");
   if (pb.epi != EPI_STORE && pb.splits != 1) return fail(PUSH_E_INVALID, "gemm: split-K only with EPI_STORE");
   if (pb.splits > 1 && pb.out_sstride != (int64_t)pb.batch * pb.out_pstride)
     return fail(PUSH_E_INVALID, "gemm: split partials must be [s][p] contiguous");
@@ -1060,7 +1085,7 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   const bool dbg_ok = !(pb.passes >> 8 & (1 | 8));
   // M <= 128 (a batch of 128 in the forward / backward GEMMs, C5b): a 256-row pair tile would spend half
   // its MMAs on rows past M, so the 1-CTA kernel (128-row tiles) takes those shapes
-  const bool pair_ok = dbg_ok && !pb.no_pair && pb.M > BM;
+  const bool pair_ok = dbg_ok && !pb.no_pair && pb.M > BM && pb.epi != EPI_UPD;
   const bool pair256 = pair_ok && pb.N % 256 == 0 && (pb.epi == EPI_STORE || pb.K >= kFb256MinK);
   const bool pair128 = pair_ok && !pair256 && pb.N % 128 == 0;
   const bool pair = pair256 || pair128;
@@ -1082,7 +1107,7 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   if (pb.out && (st = make_map(&maps[3], pb.out, pb.N, pb.M, nout, pb.ldo, pb.out_pstride, 32,
                                CU_TENSOR_MAP_SWIZZLE_64B, 16)) != PUSH_OK)
     return st;
-  if (pb.epi == EPI_BWD &&
+  if ((pb.epi == EPI_BWD || pb.epi == EPI_UPD) &&
       (st = make_map(&maps[4], pb.aprev, pb.N, pb.M, pb.batch, pb.ld_aprev, pb.aprev_pstride, 32,
                      CU_TENSOR_MAP_SWIZZLE_64B, 16)) != PUSH_OK)
     return st;
@@ -1099,6 +1124,7 @@ push_status run(const Problem& pb, cudaStream_t stream) {
   kp.a_pz = pb.A.pstride == 0 ? 0 : 1;
   kp.b_pz = pb.B.pstride == 0 ? 0 : 1;
   kp.bias = pb.bias; kp.bias_pstride = pb.bias_pstride;
+  kp.srow = pb.srow; kp.hptr = pb.hptr;
   kp.alpha = pb.alpha;
   kp.bpart = pb.bpart; kp.bp_sstride = pb.bp_sstride; kp.bp_pstride = pb.bp_pstride;
   kp.x = pb.x; kp.din = pb.xpart ? pb.din : 0; kp.xpart = pb.xpart;

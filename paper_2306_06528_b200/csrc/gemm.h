@@ -12,9 +12,11 @@ namespace gemm {
 enum Epi : int {
   EPI_STORE = 0,  // C[s][p][m][n] = alpha*acc                                (a5 weight-grad split-K partials; debug)
   EPI_FWD = 1,    // A_l[p][m][n] = sigma(acc + b_l[n])                     (a2 hidden forward)
-  EPI_BWD = 2     // delta[p][m][n] = acc * sigma'(aprev[p][m][n])          (a4 backprop)
+  EPI_BWD = 2,    // delta[p][m][n] = acc * sigma'(aprev[p][m][n])          (a4 backprop)
                   //   + column partial sums of delta per 32-row block    (a5 bias grads of the next layer down)
                   //   + optional x-weighted partials sum_r delta[r][n] x[r][i] (a5 weights of a thin first layer)
+  EPI_UPD = 3     // theta'[m][n] = t + alpha (acc + (2/h) s[m] t), t = aprev[m][n]  (a10 on the tensor cores:
+                  //   acc = sum_j K_mj (g_j - r theta_j) [n]; the former fix-up pass folded into the epilogue)
 };
 
 // One fp32 operand, batched over particles.  `split`:
@@ -49,6 +51,8 @@ struct Problem {
   int64_t ld_aprev = 0, aprev_pstride = 0;
   float* bpart = nullptr;        // BWD: bias partials, element (rb, p, n) at rb*bp_sstride + p*bp_pstride + n
   int64_t bp_sstride = 0, bp_pstride = 0;
+  const float* srow = nullptr;   // UPD: s_m (row sums of K) and the bandwidth h (device scalar)
+  const float* hptr = nullptr;
   const float* x = nullptr;      // BWD (optional): x [m][din] row-major, for the thin-first-layer partials
   int din = 0;
   float* xpart = nullptr;        // element (rb, p, n, i) at rb*xp_sstride + p*xp_pstride + n*din + i

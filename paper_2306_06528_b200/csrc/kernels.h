@@ -164,12 +164,10 @@ int svgd_update(const float* theta, const float* grad, int64_t ld, int n, int ro
                 const float* srow, const float* h, float eps_over_n, float* theta_next, cudaStream_t s);
 int update_row_block(int n, int nl, int64_t ld);
 // Tensor-core update (push_api update_tc): lhs [nl][2n] = [K, -rK] (g_first) or [-rK, K], r = 2/h, rows at
-// `pitch` (>= 2n, a multiple of 4), npad >= nl rows (the padding is zeroed); the GEMM writes
-// U = lhs [G; Theta] into theta_next, then theta_next[i][c] = theta[i][c] + eps_n (U[i][c] + r s_i theta[i][c])
+// `pitch` (>= 2n, a multiple of 4), npad >= nl rows (the padding is zeroed); the GEMM (EPI_UPD) contracts
+// U = lhs [G; Theta] and writes theta_next[i][c] = theta[i][c] + eps_n (U[i][c] + r s_i theta[i][c])
 void update_lhs(const float* K, int nl, int npad, int n, int pitch, const float* h, bool g_first, float* lhs,
                 cudaStream_t s);
-void update_fixup(const float* theta_own, int64_t ld, int nl, const float* srow, const float* h, float eps_n,
-                  float* next_own, cudaStream_t s);
 // a10 as one streaming tensor-core contraction (upd.cu, R28), n <= 64, rows <= 64:
 // out[i][c] = sum_q L[i][q] B[q][c], B = the 2n x w operand at b ([G; Theta] when g_first), L the folded
 // coefficients (eps_n K_ij on G rows; -eps_n r K_ij on Theta rows plus 1 + eps_n r (s_i - K_ii) on the own

@@ -967,29 +967,6 @@ void update_lhs(const float* K, int nl, int npad, int n, int pitch, const float*
   launch_pdl(update_lhs_kernel, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, s, K, nl, npad, n, pitch, h, g_first ? 1 : 0, lhs);
 }
 
-__global__ void update_fixup_kernel(const float* __restrict__ th, int64_t ld4, const float* __restrict__ srow,
-                                    const float* __restrict__ hptr, float eps_n, float* __restrict__ next) {
-  PUSH_PDL_ENTRY();
-  const int i = blockIdx.y;
-  const float rs = (2.0f / *hptr) * srow[i];
-  const float4* t4 = reinterpret_cast<const float4*>(th) + (int64_t)i * ld4;
-  float4* n4 = reinterpret_cast<float4*>(next) + (int64_t)i * ld4;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ld4; c += (int64_t)gridDim.x * blockDim.x) {
-    const float4 t = __ldg(t4 + c);
-    float4 u = n4[c];
-    u.x = fmaf(eps_n, fmaf(rs, t.x, u.x), t.x);
-    u.y = fmaf(eps_n, fmaf(rs, t.y, u.y), t.y);
-    u.z = fmaf(eps_n, fmaf(rs, t.z, u.z), t.z);
-    u.w = fmaf(eps_n, fmaf(rs, t.w, u.w), t.w);
-    n4[c] = u;
-  }
-}
-void update_fixup(const float* theta_own, int64_t ld, int nl, const float* srow, const float* h, float eps_n,
-                  float* next_own, cudaStream_t s) {
-  const int64_t ld4 = ld / 4;
-  const int bx = (int)std::min<int64_t>((ld4 + 255) / 256, std::max<int64_t>(1, 4 * 148 / nl + 1));
-  launch_pdl(update_fixup_kernel, dim3(dim3(bx, nl)), dim3(256), 0, s, theta_own, ld4, srow, h, eps_n, next_own);
-}
 
 // ---------------------------------------------------------------- NEXT-2: PusH's own update (variants)
 // One CTA = one segment of <= 128 columns inside a single tensor t x RB own rows; thread = one column.

@@ -794,23 +794,24 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
 // bit-identical for every P.
 // a10 on the tensor cores (P.tc_update): U = lhs B with lhs = [K, -rK] (g_first) or [-rK, K] (`rows` rows
 // of K) and B = the 2n x w operand at `b` (pitch w, MN-major: [G; Theta] when g_first, else [Theta; G]),
-// written into `out`, then out[i] = own[i] + eps_n (U_i + r s_i own[i]) (update_fixup; pitch w).
+// and out[i] = own[i] + eps_n (U_i + r s_i own[i]) written by the GEMM's EPI_UPD epilogue (pitch w).
 static push_status update_tc(push_ctx* c, const float* b, bool g_first, int64_t w, int rows, const float* K,
                              const float* srow, const float* own, float* out, float eps_n, cudaStream_t s) {
   const Plan& P = c->P;
   if (w == 0) return PUSH_OK;
   const int pitch = (int)round_up(2 * P.n, 4);
   kern::update_lhs(K, rows, rows, P.n, pitch, c->h, g_first, c->ulhs, s);
+  // U = [K, -rK] [G; Theta] with theta_i + (eps/n)(U_i + r s_i theta_i) in the GEMM epilogue (EPI_UPD: the
+  // own theta tile is loaded beside the accumulator; the former fix-up pass's arithmetic, no U round trip)
   gemm::Problem pb;
   pb.M = rows; pb.N = (int)w; pb.K = 2 * P.n; pb.batch = 1; pb.splits = 1; pb.passes = 3;
   pb.A = gemm::Operand{c->ulhs, nullptr, true, false, pitch, 0};
   pb.B = gemm::Operand{b, nullptr, true, true, w, 0};
-  pb.epi = gemm::EPI_STORE; pb.no_pair = true;
+  pb.epi = gemm::EPI_UPD; pb.no_pair = true; pb.alpha = eps_n;
+  pb.aprev = own; pb.ld_aprev = w; pb.aprev_pstride = (int64_t)rows * w;
+  pb.srow = srow; pb.hptr = c->h;
   pb.out = out; pb.ldo = w; pb.out_pstride = (int64_t)rows * w;
-  push_status st = gemm::run(pb, s);
-  if (st != PUSH_OK) return st;
-  kern::update_fixup(own, w, rows, srow, c->h, eps_n, out, s);
-  return PUSH_OK;
+  return gemm::run(pb, s);
 }
 
 // the d-sharded Theta panel of the current step (n x w at the own pitch; see Plan.o_pth)
@@ -900,7 +901,7 @@ static push_status ds_phase2(push_ctx* c, cudaStream_t s) {
   });
   if (st != PUSH_OK || wo == 0) return st;
   const float eps_n = c->cfg.step_size / (float)P.n;
-  return run_k(c, PC_UPDATE, P.tc_update ? 3 : (P.tc_stream ? 2 : 1), 12.0 * P.n * (double)wo, 2.0 * P.n * (double)P.n * wo, s,
+  return run_k(c, PC_UPDATE, P.tc_update ? 2 : (P.tc_stream ? 2 : 1), 12.0 * P.n * (double)wo, 2.0 * P.n * (double)P.n * wo, s,
                [&]() -> push_status {
     float* pth = pan_theta(c);
     if (P.tc_stream) {  // every row of the panel; operand order as the all-gather path at this parity
@@ -1015,7 +1016,7 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   const float eps_n = c->cfg.step_size / (float)P.n;
   float* next = c->theta[c->cur ^ 1];
   const int var = c->cfg.variant;
-  st = run_k(c, PC_UPDATE, (var == 0 && P.tc_update) ? 3 : ((var == 0 && P.tc_stream) ? 2 : 1), 2.0 * nd4 + 4.0 * P.nl * (double)P.d,
+  st = run_k(c, PC_UPDATE, (var == 0 && P.tc_update) ? 2 : ((var == 0 && P.tc_stream) ? 2 : 1), 2.0 * nd4 + 4.0 * P.nl * (double)P.d,
              2.0 * P.nl * (double)P.n * P.d, s, [&] {
     if (var == 0 && P.tc_stream) {
       const bool g_first = c->grad < th;  // layout Theta[0], G, Theta[1]
