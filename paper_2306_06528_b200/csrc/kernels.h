@@ -175,12 +175,9 @@ void update_lhs(const float* K, int nl, int npad, int n, int pitch, const float*
 // round_up(2n, 4) floats each); = th_i + eps_n (sum_j K_ij (g_j - r th_j) + r s_i th_i); w % 128 == 0
 constexpr int kUpdTcMaxRows = 64;
 int update_tc_npad(int rows);
-// lhs_ready: L was already split by update_tc_stream_lhs (the captured step builds it beside a8/a9)
 push_status update_tc_stream(const float* b, bool g_first, int n, int64_t w, int rows, int own_row, const float* K,
                              const float* h, float* lhs_hi, float* lhs_lo, float* out, const float* srow, float eps_n,
-                             cudaStream_t s, bool lhs_ready = false);
-void update_tc_stream_lhs(bool g_first, int n, int rows, int own_row, const float* K, const float* h,
-                          const float* srow, float eps_n, float* lhs_hi, float* lhs_lo, cudaStream_t s);
+                             cudaStream_t s);
 // NEXT-2 variants: column segments of <= kVarSegCols columns inside one tensor (x = begin, y = end, z = tensor)
 constexpr int kVarSegCols = 128;
 std::vector<int4> var_segments(int tensors, const int64_t* toff, const int64_t* tsize);

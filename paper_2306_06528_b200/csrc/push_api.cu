@@ -796,12 +796,11 @@ static push_status do_grads(push_ctx* c, const float* x, const float* y, int B, 
 // of K) and B = the 2n x w operand at `b` (pitch w, MN-major: [G; Theta] when g_first, else [Theta; G]),
 // and out[i] = own[i] + eps_n (U_i + r s_i own[i]) written by the GEMM's EPI_UPD epilogue (pitch w).
 static push_status update_tc(push_ctx* c, const float* b, bool g_first, int64_t w, int rows, const float* K,
-                             const float* srow, const float* own, float* out, float eps_n, cudaStream_t s,
-                             bool lhs_ready = false) {
+                             const float* srow, const float* own, float* out, float eps_n, cudaStream_t s) {
   const Plan& P = c->P;
   if (w == 0) return PUSH_OK;
   const int pitch = (int)round_up(2 * P.n, 4);
-  if (!lhs_ready) kern::update_lhs(K, rows, rows, P.n, pitch, c->h, g_first, c->ulhs, s);
+  kern::update_lhs(K, rows, rows, P.n, pitch, c->h, g_first, c->ulhs, s);
   // U = [K, -rK] [G; Theta] with theta_i + (eps/n)(U_i + r s_i theta_i) in the GEMM epilogue (EPI_UPD: the
   // own theta tile is loaded beside the accumulator; the former fix-up pass's arithmetic, no U round trip)
   gemm::Problem pb;
@@ -985,24 +984,9 @@ static push_status run_kphase(push_ctx* c, cudaStream_t s) {
     });
   }
   if (st != PUSH_OK) return st;
-  st = run_k(c, PC_BANDWIDTH, (int64_t)P.nl * P.n >= 16384 ? 2 : 1, 4.0 * P.tensors * P.n * P.n, 0, s, [&] {
+  return run_k(c, PC_BANDWIDTH, (int64_t)P.nl * P.n >= 16384 ? 2 : 1, 4.0 * P.tensors * P.n * P.n, 0, s, [&] {
     kern::bandwidth_kernel(c->D, P.n, c->row0, P.nl, c->cfg.bw_rule, c->c_ln, c->cfg.bw_h, c->h, c->K, c->srow,
                            P.tensors, s, P.gram && kern::gram_d_in_bandwidth(P.n) ? c->gsum : nullptr);
-    return PUSH_OK;
-  });
-  if (st != PUSH_OK || c->cfg.variant != 0 || !(P.tc_stream || P.tc_update)) return st;
-  // the tensor-core update's coefficient matrix needs only K, s and h: built here as part of a9 (profiled
-  // with the bandwidth / kernel-matrix class), beside the gradient phase in a captured step, instead of on
-  // the update's critical path
-  const bool g_first = c->grad < th;  // layout Theta[0], G, Theta[1]
-  const float eps_n = c->cfg.step_size / (float)P.n;
-  return run_k(c, PC_BANDWIDTH, 1, 0, 0, s, [&] {
-    if (P.tc_stream) {
-      const int64_t half = (int64_t)kern::kUpdTcMaxRows * round_up(2 * P.n, 4);
-      kern::update_tc_stream_lhs(g_first, P.n, P.nl, c->row0, c->K, c->h, c->srow, eps_n, c->ulhs, c->ulhs + half, s);
-    } else {
-      kern::update_lhs(c->K, P.nl, P.nl, P.n, (int)round_up(2 * P.n, 4), c->h, g_first, c->ulhs, s);
-    }
     return PUSH_OK;
   });
 }
@@ -1032,20 +1016,18 @@ static push_status do_step(push_ctx* c, cudaStream_t s) {
   const float eps_n = c->cfg.step_size / (float)P.n;
   float* next = c->theta[c->cur ^ 1];
   const int var = c->cfg.variant;
-  // (the tensor-core updates' coefficient matrices were built by run_kphase: one launch each here)
-  st = run_k(c, PC_UPDATE, 1, 2.0 * nd4 + 4.0 * P.nl * (double)P.d,
+  st = run_k(c, PC_UPDATE, (var == 0 && P.tc_update) ? 2 : ((var == 0 && P.tc_stream) ? 2 : 1), 2.0 * nd4 + 4.0 * P.nl * (double)P.d,
              2.0 * P.nl * (double)P.n * P.d, s, [&] {
     if (var == 0 && P.tc_stream) {
       const bool g_first = c->grad < th;  // layout Theta[0], G, Theta[1]
       const int64_t half = (int64_t)kern::kUpdTcMaxRows * round_up(2 * P.n, 4);
       return kern::update_tc_stream(g_first ? c->grad : th, g_first, P.n, P.ld, P.nl, c->row0, c->K, c->h, c->ulhs,
-                                    c->ulhs + half, next + (int64_t)c->row0 * P.ld, c->srow, eps_n, s,
-                                    /*lhs_ready=*/true);
+                                    c->ulhs + half, next + (int64_t)c->row0 * P.ld, c->srow, eps_n, s);
     } else if (var == 0 && P.tc_update) {
       // layout Theta[0], G, Theta[1]: [G; Theta_cur] or [Theta_cur; G] is one 2n x ld operand
       const bool g_first = c->grad < th;
       return update_tc(c, g_first ? c->grad : th, g_first, P.ld, P.nl, c->K, c->srow,
-                       th + (int64_t)c->row0 * P.ld, next + (int64_t)c->row0 * P.ld, eps_n, s, /*lhs_ready=*/true);
+                       th + (int64_t)c->row0 * P.ld, next + (int64_t)c->row0 * P.ld, eps_n, s);
     } else if (var == 0) {
       kern::svgd_update(th, c->grad, P.ld, P.n, c->row0, P.nl, c->K, c->srow, c->h, eps_n, next, s);
     } else {  // NEXT-2 (include/push.h PUSH_VAR_*): weights w_d = eps or eps/n, repulsion eps/n

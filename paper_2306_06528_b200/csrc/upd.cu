@@ -281,24 +281,18 @@ int update_tc_npad(int rows) {
   return np;
 }
 
-void update_tc_stream_lhs(bool g_first, int n, int rows, int own_row, const float* K, const float* h,
-                          const float* srow, float eps_n, float* lhs_hi, float* lhs_lo, cudaStream_t s) {
-  const int npad = update_tc_npad(rows), pitch = ((2 * n + 3) / 4) * 4;
-  const int64_t tot = (int64_t)npad * pitch;
-  launch_pdl(update_lhs_split_kernel, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, s, K, rows, npad, n, pitch,
-             own_row, h, srow, eps_n, g_first ? 1 : 0, lhs_hi, lhs_lo);
-}
-
 push_status update_tc_stream(const float* b, bool g_first, int n, int64_t w, int rows, int own_row, const float* K,
                              const float* h, float* lhs_hi, float* lhs_lo, float* out, const float* srow, float eps_n,
-                             cudaStream_t s, bool lhs_ready) {
+                             cudaStream_t s) {
   if (n < 1 || 2 * n > kUK * kUMaxKB || rows < 1 || rows > kUpdTcMaxRows || w % kUCols)
     return fail(PUSH_E_SHAPE, "update_tc_stream: unsupported shape");
   if (w == 0) return PUSH_OK;
   push_status st = gemm::get_encoder();
   if (st != PUSH_OK) return st;
   const int npad = update_tc_npad(rows), pitch = ((2 * n + 3) / 4) * 4;
-  if (!lhs_ready) update_tc_stream_lhs(g_first, n, rows, own_row, K, h, srow, eps_n, lhs_hi, lhs_lo, s);
+  const int64_t tot = (int64_t)npad * pitch;
+  launch_pdl(update_lhs_split_kernel, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, s, K, rows, npad, n, pitch, own_row, h, srow,
+                                                                         eps_n, g_first ? 1 : 0, lhs_hi, lhs_lo);
   switch (npad) {
     case 16: return update_tc_launch<16>(b, n, w, rows, lhs_hi, lhs_lo, pitch, out, s);
     case 32: return update_tc_launch<32>(b, n, w, rows, lhs_hi, lhs_lo, pitch, out, s);
